@@ -1,0 +1,188 @@
+/*
+ * rg.h -- C-ABI of the B200-native RayGauss hot path (arXiv 2408.03356):
+ * differentiable volume ray casting of anisotropic 3D Gaussians, slab by slab
+ * through a BVH (Alg. 1-2, Eq. 4, Eq. 10-16
+ * P:163-237, supplementary P:500-564).  Implemented by libraygauss.so
+ * (paper_2408_03356_b200/csrc, hand-written sm_100a CUDA).
+ *
+ * Conventions for every entry point
+ *   - Pointers are DEVICE pointers owned by the caller unless stated "host".
+ *   - Every call is asynchronous on `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream).  The library never allocates, frees or
+ *     synchronises; scratch memory is the caller's workspace.
+ *   - Argument validation happens before anything is enqueued; on error nothing
+ *     is launched and a status != RG_OK is returned.  A failed launch returns
+ *     RG_ERR_CUDA (cudaGetLastError after the launch).
+ *   - Data errors never fail a call: non-finite Gaussians are inactive; hit-buffer
+ *     overflow is truncated deterministically (L7); both are counted
+ *     in the optional device-side rg_stats.
+ *   - Parameters are ACTIVATED values (activations live with the caller):
+ *     unit quaternion (w,x,y,z), scale > 0, density sigma~ > 0, SG axes unit.
+ *     The quaternion/axes are consumed as given (no internal normalisation) and
+ *     gradients are w.r.t. exactly these tensors.
+ *   - Layouts are row-major, caller (original) Gaussian order:
+ *       mean [n,3], quat [n,4], scale [n,3], density [n],
+ *       sh [n,(sh_degree+1)^2,3], sg_amp [n,sg_count,3], sg_sharp [n,sg_count],
+ *       sg_axis [n,sg_count,3]; rays / images [R,3] row-major, R = ray count.
+ *   - Thread safety: calls on different streams with different workspaces are
+ *     independent; there is no global mutable state.
+ */
+#ifndef RAYGAUSS_RG_H
+#define RAYGAUSS_RG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RG_ABI_VERSION 1
+
+typedef enum {
+  RG_OK = 0,
+  RG_ERR_INVALID_ARG = 1,
+  RG_ERR_WORKSPACE_TOO_SMALL = 2,
+  RG_ERR_CUDA = 3,
+  RG_ERR_NOT_IMPLEMENTED = 4
+} rg_status;
+
+/* Scene parameters P = {(sigma~, c~, mu, q, s)}. */
+typedef struct {
+  int32_t n;          /* number of Gaussians, >= 0 */
+  int32_t sh_degree;  /* L1 of Eq. 14, 0..3 */
+  int32_t sg_count;   /* number of SG lobes (Eq. 15), 0..7 */
+  int32_t pad_;
+  const float *mean, *quat, *scale, *density;
+  const float *sh, *sg_amp, *sg_sharp, *sg_axis;   /* sg_* may be NULL if sg_count == 0 */
+} rg_gaussians;
+
+/* Gradients w.r.t. the same tensors, same layouts.  ACCUMULATED (+=): the
+   caller zeroes them.  Any pointer may be NULL to skip that group. */
+typedef struct {
+  float *mean, *quat, *scale, *density, *sh, *sg_amp, *sg_sharp, *sg_axis;
+} rg_gaussian_grads;
+
+typedef struct {
+  float dt;              /* Delta t, world units along unit d > 0 */
+  int32_t slab_samples;  /* B, samples per slab, 1..32 */
+  float sigma_eps;       /* truncation threshold (Eq. 16) > 0 */
+  float t_eps;           /* early-termination threshold, [0,1) */
+  int32_t hit_capacity;  /* K = n_max of Alg. 1, 1..4096 */
+  int32_t radius_mode;   /* 0: r = phi^-1(sigma_eps/sigma~); 1: r = k_sigma */
+  float k_sigma;         /* support radius in radius_mode 1 (north star "3-sigma") */
+  float t_near;          /* t0 = max(bbox entry, t_near) (L13), usually 0 */
+  float background[3];   /* pixel = C + T_end * background (L12) */
+  int32_t pad_;
+} rg_config;
+
+/* Explicit, possibly uncorrelated rays: device [n,3] origins and
+   unit directions. */
+typedef struct {
+  int32_t n, pad_;
+  const float *origin, *dir;
+} rg_rays;
+
+/* Pinhole camera: one ray through each pixel centre of the
+   rectangle [x0,x1) x [y0,y1); rays are numbered row-major inside the
+   rectangle.  c2w is HOST data (passed by value to the kernel): 3x4 row-major
+   [right | down | forward | eye]. */
+typedef struct {
+  int32_t width, height, x0, y0, x1, y1;
+  float fx, fy, cx, cy;
+  float c2w[12];
+} rg_camera;
+
+/* BVH handle filled by rg_build_bvh: device pointers into the caller's
+   workspace.  Valid until the workspace is reused or the parameters change
+   (the paper rebuilds after every optimiser step). Read-only for callers. */
+typedef struct {
+  int32_t n, sh_degree, sg_count, app_stride;
+  const void* geom;        /* [n] 64-B records, Morton order */
+  const float* app;        /* [n, app_stride] appearance, Morton order */
+  const void* nodes;       /* [n-1] 64-B internal nodes (child boxes + child ids) */
+  const float* leaf_box;   /* [n,6] padded AABBs, Morton order */
+  const float* root_box;   /* [6] scene bbox = union of active AABBs */
+  const uint32_t* codes;   /* [n] Morton codes, caller order */
+  const uint32_t* sorted_codes; /* [n] */
+  const uint32_t* order;   /* [n] order[pos] = caller index */
+} rg_bvh;
+
+/* Device-side counters, ACCUMULATED with atomics (caller zeroes). */
+typedef struct {
+  unsigned long long rays;           /* rays launched */
+  unsigned long long rays_hit;       /* rays with t0 < t1 */
+  unsigned long long slabs;          /* non-empty slabs integrated */
+  unsigned long long pairs;          /* (ray, Gaussian) pair set-ups */
+  unsigned long long evals;          /* (sample, Gaussian) contributions */
+  unsigned long long samples;        /* composited samples (sigma > 0) */
+  unsigned long long overflows;      /* slabs truncated to K */
+  unsigned long long fetches;        /* BVH traversals */
+  unsigned long long node_visits;    /* internal nodes visited */
+  unsigned long long stack_overflows;
+  unsigned long long nonfinite_grads;
+  unsigned long long pad_[5];
+} rg_stats;
+
+/* static string for a status code (host) */
+const char* rg_status_string(rg_status s);
+/* library build string (host) */
+const char* rg_version(void);
+
+/* ---- BVH build -------------------------------- */
+/* Workspace bytes for rg_build_bvh on n Gaussians with the given appearance
+   sizes.  The workspace must be 256-B aligned. */
+size_t rg_bvh_workspace_bytes(int32_t n, int32_t sh_degree, int32_t sg_count);
+
+/* Preprocess (R(q), M = S^-1 R^T, support radius, padded tight AABB: P:176-183,
+   P:529-558), 30-bit Morton codes of the means, stable CUB-free LSD radix sort,
+   Karras hierarchy, bottom-up refit.  Errors: RG_ERR_INVALID_ARG for NULL
+   pointers, n < 0, sh_degree not in 0..3, sg_count not in 0..7, bad config;
+   RG_ERR_WORKSPACE_TOO_SMALL. */
+rg_status rg_build_bvh(const rg_gaussians* g, const rg_config* cfg, void* ws, size_t ws_bytes,
+                       rg_bvh* out, void* stream);
+
+/* ---- rays -------------------------------------------------------------- */
+/* Writes the camera's rays (ARITH-7) to device o/d [R,3]. */
+rg_status rg_camera_rays(const rg_camera* cam, float* origin, float* dir, void* stream);
+
+/* ---- forward (a6-a10) ---------------------------------------------------- */
+/* Renders either `rays` or `cam` (exactly one non-NULL).  Outputs (device):
+     rgb [R,3]  = C + T_end * background,
+     T   [R]    = final transmittance,
+     replay [R] = index of the slab after which the ray terminated early
+                  (T <= t_eps), or -1; consumed by rg_render_backward.
+   stats: optional device rg_stats.  debug: if debug_records != NULL, the first
+   debug_rays rays append up to debug_cap (slab, caller index) pairs per ray of
+   their integrated per-slab hit sets (in order) to debug_records
+   [debug_rays, debug_cap, 2] and their record count to debug_counts. */
+rg_status rg_render_forward(const rg_gaussians* g, const rg_bvh* bvh, const rg_config* cfg,
+                            const rg_rays* rays, const rg_camera* cam, float* rgb, float* T,
+                            int32_t* replay, rg_stats* stats, int32_t debug_rays,
+                            int32_t debug_cap, int32_t* debug_counts, int32_t* debug_records,
+                            void* stream);
+
+/* ---- backward (a11-a12) ------------------------------------------------- */
+/* Workspace for rg_render_backward: the Morton-ordered gradient accumulator. */
+size_t rg_backward_workspace_bytes(int32_t n, int32_t sh_degree, int32_t sg_count);
+
+/* Exact gradient (a.e., decisions held fixed) of sum_r <d_rgb_r, rgb_r> w.r.t.
+   the activated parameters, by replaying the forward (same rays/camera, same
+   bvh and cfg, forward outputs rgb/T/replay).  Gradients are ACCUMULATED into
+   `grads` (caller order).  Non-finite gradient values are counted in stats. */
+rg_status rg_render_backward(const rg_gaussians* g, const rg_bvh* bvh, const rg_config* cfg,
+                             const rg_rays* rays, const rg_camera* cam, const float* rgb,
+                             const float* T, const int32_t* replay, const float* d_rgb,
+                             const rg_gaussian_grads* grads, rg_stats* stats, void* ws,
+                             size_t ws_bytes, void* stream);
+
+/* ---- loss helper (for benchmarks; loss itself is outside the paper's path) -- */
+/* L1 loss: loss += scale * sum |rgb - target|, d_rgb = scale * sign(rgb - target)
+   over n_values floats (device; loss is one device float, accumulated). */
+rg_status rg_l1_loss_grad(const float* rgb, const float* target, int64_t n_values, float scale,
+                          float* d_rgb, float* loss, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAYGAUSS_RG_H */

@@ -1,0 +1,162 @@
+// rg_api.cu -- the C-ABI entry points of include/rg.h: argument validation
+// (before anything is enqueued), workspace layout, launch, error mapping.
+#include <cstring>
+
+#include "rg_internal.cuh"
+
+using namespace rg;
+
+namespace {
+
+bool config_ok(const rg_config* c) {
+  if (!c) return false;
+  if (!(c->dt > 0.0f) || !isfinite(c->dt)) return false;
+  if (c->slab_samples < 1 || c->slab_samples > 32) return false;
+  if (!(c->sigma_eps > 0.0f) || !isfinite(c->sigma_eps)) return false;
+  if (!(c->t_eps >= 0.0f && c->t_eps < 1.0f)) return false;
+  if (c->hit_capacity < 1 || c->hit_capacity > 4096) return false;
+  if (c->radius_mode != 0 && c->radius_mode != 1) return false;
+  if (c->radius_mode == 1 && !(c->k_sigma > 0.0f)) return false;
+  if (!isfinite(c->t_near)) return false;
+  return true;
+}
+
+bool gaussians_ok(const rg_gaussians* g) {
+  if (!g || g->n < 0) return false;
+  if (g->sh_degree < 0 || g->sh_degree > kMaxDeg) return false;
+  if (g->sg_count < 0 || g->sg_count > kMaxLobes) return false;
+  if (g->n == 0) return true;
+  if (!g->mean || !g->quat || !g->scale || !g->density || !g->sh) return false;
+  if (g->sg_count > 0 && (!g->sg_amp || !g->sg_sharp || !g->sg_axis)) return false;
+  return true;
+}
+
+bool bvh_ok(const rg_bvh* b, const rg_gaussians* g) {
+  if (!b || !b->root_box) return false;
+  if (b->n != g->n || b->sh_degree != g->sh_degree || b->sg_count != g->sg_count) return false;
+  if (b->n > 0 && (!b->geom || !b->app || !b->order || (b->n > 1 && !b->nodes))) return false;
+  return true;
+}
+
+bool rays_ok(const rg_rays* r, const rg_camera* cam) {
+  if ((r == nullptr) == (cam == nullptr)) return false;
+  if (r) return r->n >= 0 && (r->n == 0 || (r->origin && r->dir));
+  if (cam->x0 < 0 || cam->y0 < 0 || cam->x1 < cam->x0 || cam->y1 < cam->y0) return false;
+  if (!(cam->fx != 0.0f) || !(cam->fy != 0.0f)) return false;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rg_status_string(rg_status s) {
+  switch (s) {
+    case RG_OK: return "ok";
+    case RG_ERR_INVALID_ARG: return "invalid argument";
+    case RG_ERR_WORKSPACE_TOO_SMALL: return "workspace too small";
+    case RG_ERR_CUDA: return "CUDA error";
+    case RG_ERR_NOT_IMPLEMENTED: return "not implemented";
+  }
+  return "unknown status";
+}
+
+const char* rg_version(void) {
+  return "libraygauss abi=1 sm_100a (LBVH + slab ray casting, fwd+bwd)";
+}
+
+size_t rg_bvh_workspace_bytes(int32_t n, int32_t sh_degree, int32_t sg_count) {
+  if (n < 0 || sh_degree < 0 || sh_degree > kMaxDeg || sg_count < 0 || sg_count > kMaxLobes)
+    return 0;
+  return bvh_layout(n, sh_degree, sg_count).total;
+}
+
+rg_status rg_build_bvh(const rg_gaussians* g, const rg_config* cfg, void* ws, size_t ws_bytes,
+                       rg_bvh* out, void* stream) {
+  if (!gaussians_ok(g) || !config_ok(cfg) || !ws || !out) return RG_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return RG_ERR_INVALID_ARG;
+  const BvhLayout L = bvh_layout(g->n, g->sh_degree, g->sg_count);
+  if (ws_bytes < L.total) return RG_ERR_WORKSPACE_TOO_SMALL;
+  char* w = static_cast<char*>(ws);
+  cudaGetLastError();   // clear sticky-free previous errors
+  const cudaError_t e = launch_build(*g, *cfg, w, L, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return RG_ERR_CUDA;
+  rg_bvh b;
+  std::memset(&b, 0, sizeof(b));
+  b.n = g->n;
+  b.sh_degree = g->sh_degree;
+  b.sg_count = g->sg_count;
+  b.app_stride = app_stride(g->sh_degree, g->sg_count);
+  b.geom = w + L.geom;
+  b.app = reinterpret_cast<const float*>(w + L.app);
+  b.nodes = w + L.nodes;
+  b.leaf_box = reinterpret_cast<const float*>(w + L.leaf_box);
+  b.root_box = reinterpret_cast<const float*>(w + L.root_box);
+  b.codes = reinterpret_cast<const uint32_t*>(w + L.codes);
+  b.sorted_codes = reinterpret_cast<const uint32_t*>(w + L.keys_a);
+  b.order = reinterpret_cast<const uint32_t*>(w + L.vals_a);
+  *out = b;
+  return RG_OK;
+}
+
+rg_status rg_camera_rays(const rg_camera* cam, float* origin, float* dir, void* stream) {
+  if (!cam || !rays_ok(nullptr, cam)) return RG_ERR_INVALID_ARG;
+  const int n = (cam->x1 - cam->x0) * (cam->y1 - cam->y0);
+  if (n > 0 && (!origin || !dir)) return RG_ERR_INVALID_ARG;
+  return launch_camera_rays(*cam, origin, dir, static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? RG_OK
+             : RG_ERR_CUDA;
+}
+
+rg_status rg_render_forward(const rg_gaussians* g, const rg_bvh* bvh, const rg_config* cfg,
+                            const rg_rays* rays, const rg_camera* cam, float* rgb, float* T,
+                            int32_t* replay, rg_stats* stats, int32_t debug_rays,
+                            int32_t debug_cap, int32_t* debug_counts, int32_t* debug_records,
+                            void* stream) {
+  if (!gaussians_ok(g) || !config_ok(cfg) || !bvh_ok(bvh, g) || !rays_ok(rays, cam))
+    return RG_ERR_INVALID_ARG;
+  const int64_t n = rays ? rays->n : (int64_t)(cam->x1 - cam->x0) * (cam->y1 - cam->y0);
+  if (n > 0 && (!rgb || !T || !replay)) return RG_ERR_INVALID_ARG;
+  if (debug_records && (debug_rays < 0 || debug_cap < 1 || !debug_counts))
+    return RG_ERR_INVALID_ARG;
+  const cudaError_t e = launch_forward(*g, *bvh, *cfg, rays, cam, rgb, T, replay, stats,
+                                       debug_rays, debug_cap, debug_counts, debug_records,
+                                       static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? RG_OK : RG_ERR_CUDA;
+}
+
+size_t rg_backward_workspace_bytes(int32_t n, int32_t sh_degree, int32_t sg_count) {
+  if (n < 0 || sh_degree < 0 || sh_degree > kMaxDeg || sg_count < 0 || sg_count > kMaxLobes)
+    return 0;
+  return sizeof(float) * (size_t)grad_stride(sh_degree, sg_count) * (size_t)(n > 0 ? n : 1);
+}
+
+rg_status rg_render_backward(const rg_gaussians* g, const rg_bvh* bvh, const rg_config* cfg,
+                             const rg_rays* rays, const rg_camera* cam, const float* rgb,
+                             const float* T, const int32_t* replay, const float* d_rgb,
+                             const rg_gaussian_grads* grads, rg_stats* stats, void* ws,
+                             size_t ws_bytes, void* stream) {
+  if (!gaussians_ok(g) || !config_ok(cfg) || !bvh_ok(bvh, g) || !rays_ok(rays, cam) || !grads)
+    return RG_ERR_INVALID_ARG;
+  const int64_t n = rays ? rays->n : (int64_t)(cam->x1 - cam->x0) * (cam->y1 - cam->y0);
+  if (n > 0 && (!rgb || !replay || !d_rgb)) return RG_ERR_INVALID_ARG;
+  if (!ws || (reinterpret_cast<uintptr_t>(ws) & 15) != 0) return RG_ERR_INVALID_ARG;
+  if (ws_bytes < rg_backward_workspace_bytes(g->n, g->sh_degree, g->sg_count))
+    return RG_ERR_WORKSPACE_TOO_SMALL;
+  const cudaError_t e = launch_backward(*g, *bvh, *cfg, rays, cam, rgb, T, replay, d_rgb, *grads,
+                                        stats, static_cast<float*>(ws),
+                                        static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? RG_OK : RG_ERR_CUDA;
+}
+
+rg_status rg_l1_loss_grad(const float* rgb, const float* target, int64_t n_values, float scale,
+                          float* d_rgb, float* loss, void* stream) {
+  if (n_values < 0 || (n_values > 0 && (!rgb || !target || !d_rgb || !loss)))
+    return RG_ERR_INVALID_ARG;
+  return launch_l1(rgb, target, n_values, scale, d_rgb, loss, static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess
+             ? RG_OK
+             : RG_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,428 @@
+// rg_build.cu -- LBVH build over the padded support AABBs of the Gaussians
+// (PAPER.md P:239):
+//   k_preprocess : validity, support radius, padded tight AABB (ARITH-1..4),
+//                  block-reduced bbox of valid means (ordered-int atomics)
+//   k_morton     : 30-bit Morton codes of the means (ARITH-6)
+//   k_radix_*    : stable LSD radix sort, 4 x 8-bit passes, CUB-free
+//                  (tile histogram -> single-block scan -> stable tile scatter
+//                  ranked with __match_any_sync)
+//   k_pack       : Morton-ordered 64-B geometry records + appearance records
+//   k_karras     : Karras 2012 hierarchy (one thread per internal node)
+//   k_refit      : bottom-up AABB union with per-node arrival counters
+#include "rg_internal.cuh"
+
+namespace rg {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kItems = 16;
+constexpr int kTile = kThreads * kItems;   // keys per radix tile
+
+__device__ __forceinline__ int ord_enc(float f) {
+  int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float ord_dec(int i) {
+  return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF);
+}
+
+__global__ void k_init(int* bounds, float* root_box) {
+  if (threadIdx.x < 3) {
+    bounds[threadIdx.x] = ord_enc(INFINITY);
+    bounds[3 + threadIdx.x] = ord_enc(-INFINITY);
+    root_box[threadIdx.x] = INFINITY;
+    root_box[3 + threadIdx.x] = -INFINITY;
+  }
+}
+
+__device__ __forceinline__ bool finite_(float x) { return isfinite(x); }
+
+// validity of every parameter of Gaussian i (non-finite -> inactive)
+__device__ bool gaussian_valid(const rg_gaussians& g, int i) {
+  bool ok = true;
+  for (int k = 0; k < 3; ++k) {
+    const float m = g.mean[3 * (size_t)i + k], s = g.scale[3 * (size_t)i + k];
+    ok &= finite_(m) && finite_(s) && s > 0.0f;
+  }
+  for (int k = 0; k < 4; ++k) ok &= finite_(g.quat[4 * (size_t)i + k]);
+  ok &= finite_(g.density[i]);
+  const int nc = (g.sh_degree + 1) * (g.sh_degree + 1);
+  for (int k = 0; k < 3 * nc; ++k) ok &= finite_(g.sh[(size_t)i * 3 * nc + k]);
+  const int G = g.sg_count;
+  for (int k = 0; k < 3 * G; ++k) ok &= finite_(g.sg_amp[(size_t)i * 3 * G + k]);
+  for (int k = 0; k < G; ++k) ok &= finite_(g.sg_sharp[(size_t)i * G + k]);
+  for (int k = 0; k < 3 * G; ++k) ok &= finite_(g.sg_axis[(size_t)i * 3 * G + k]);
+  return ok;
+}
+
+// ARITH-2/3: M and r^2 (r2 < 0 marks inactive)
+__device__ void support_exact(const rg_gaussians& g, const rg_config& c, int i, bool active,
+                              float R[9], float M[9], float& r2) {
+  const float* q = g.quat + 4 * (size_t)i;
+  const float* s = g.scale + 3 * (size_t)i;
+  rot_exact(q[0], q[1], q[2], q[3], R);
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) M[3 * a + b] = div_(R[3 * b + a], s[a]);
+  if (!active) { r2 = -1.0f; return; }
+  if (c.radius_mode == 0)
+    r2 = (float)(2.0 * (log((double)g.density[i]) - log((double)c.sigma_eps)));
+  else
+    r2 = mul_(c.k_sigma, c.k_sigma);
+}
+
+__global__ void __launch_bounds__(kThreads) k_preprocess(rg_gaussians g, rg_config c,
+                                                         float* box_orig, int* flags,
+                                                         int* bounds) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  if (i < g.n) {
+    const bool valid = gaussian_valid(g, i);
+    const bool active = valid && (g.density[i] > c.sigma_eps);
+    flags[i] = (valid ? 1 : 0) | (active ? 2 : 0);
+    float bx[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    if (active) {
+      float R[9], M[9], r2;
+      support_exact(g, c, i, true, R, M, r2);
+      const float* s = g.scale + 3 * (size_t)i;
+      for (int a = 0; a < 3; ++a) {                             // ARITH-4
+        const float a0 = mul_(s[0], R[3 * a + 0]);
+        const float a1 = mul_(s[1], R[3 * a + 1]);
+        const float a2 = mul_(s[2], R[3 * a + 2]);
+        const float ss = dot3_(a0, a1, a2, a0, a1, a2);
+        const float e = sqrt_(mul_(r2, ss));
+        const float mu = g.mean[3 * (size_t)i + a];
+        const float e1 = mul_(e, 0x1p-8f);
+        const float m1 = mul_(add_(fabsf(mu), e), 0x1p-18f);
+        const float ep = add_(add_(e, e1), m1);
+        bx[a] = sub_(mu, ep);
+        bx[3 + a] = add_(mu, ep);
+      }
+    }
+    for (int k = 0; k < 6; ++k) box_orig[6 * (size_t)i + k] = bx[k];
+    if (valid)
+      for (int a = 0; a < 3; ++a) lo[a] = hi[a] = g.mean[3 * (size_t)i + a];
+  }
+  // block reduction of the bbox of valid means (exact min/max)
+  for (int a = 0; a < 3; ++a) {
+    for (int off = 16; off > 0; off >>= 1) {
+      lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], off));
+      hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], off));
+    }
+  }
+  if ((threadIdx.x & 31) == 0 && lo[0] <= hi[0]) {
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(bounds + a, ord_enc(lo[a]));
+      atomicMax(bounds + 3 + a, ord_enc(hi[a]));
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t spread10(uint32_t x) {
+  x = (x * 0x00010001u) & 0xFF0000FFu;
+  x = (x * 0x00000101u) & 0x0F00F00Fu;
+  x = (x * 0x00000011u) & 0xC30C30C3u;
+  x = (x * 0x00000005u) & 0x49249249u;
+  return x;
+}
+
+__global__ void __launch_bounds__(kThreads) k_morton(rg_gaussians g, const int* flags,
+                                                     const int* bounds, uint32_t* codes,
+                                                     uint32_t* keys, uint32_t* vals) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  uint32_t code = 0xFFFFFFFFu;
+  if (flags[i] & 1) {
+    uint32_t q[3];
+    for (int a = 0; a < 3; ++a) {                               // ARITH-6
+      const float lo = ord_dec(bounds[a]), hi = ord_dec(bounds[3 + a]);
+      const float ext = sub_(hi, lo);
+      float u = 0.0f;
+      if (ext > 0.0f) u = div_(sub_(g.mean[3 * (size_t)i + a], lo), ext);
+      const float v = mul_(u, 1024.0f);
+      int qi = (int)floorf(v);
+      qi = qi < 0 ? 0 : (qi > 1023 ? 1023 : qi);
+      q[a] = (uint32_t)qi;
+    }
+    code = (spread10(q[0]) << 2) | (spread10(q[1]) << 1) | spread10(q[2]);
+  }
+  codes[i] = code;
+  keys[i] = code;
+  vals[i] = (uint32_t)i;
+}
+
+// --- radix sort -----------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_radix_hist(const uint32_t* keys, int n, int shift,
+                                                         uint32_t* hist, int tiles) {
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int base = blockIdx.x * kTile;
+  for (int r = 0; r < kItems; ++r) {
+    const int i = base + r * kThreads + threadIdx.x;
+    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xFF], 1u);
+  }
+  __syncthreads();
+  hist[threadIdx.x * tiles + blockIdx.x] = h[threadIdx.x];   // digit-major
+}
+
+// exclusive scan of hist[256*tiles] in place, one block of 1024 threads
+__global__ void __launch_bounds__(1024) k_radix_scan(uint32_t* hist, int total) {
+  __shared__ uint32_t part[1024];
+  const int t = threadIdx.x;
+  const int per = (total + 1023) / 1024;
+  const int b = t * per, e = min(total, b + per);
+  uint32_t s = 0;
+  for (int i = b; i < e; ++i) s += hist[i];
+  part[t] = s;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    const uint32_t v = t >= off ? part[t - off] : 0u;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  uint32_t run = part[t] - s;
+  for (int i = b; i < e; ++i) {
+    const uint32_t v = hist[i];
+    hist[i] = run;
+    run += v;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_radix_scatter(const uint32_t* kin, const uint32_t* vin,
+                                                            uint32_t* kout, uint32_t* vout, int n,
+                                                            int shift, const uint32_t* hist,
+                                                            int tiles) {
+  constexpr int kWarps = kThreads / 32;
+  __shared__ uint32_t base_off[256];
+  __shared__ uint32_t run[256];
+  __shared__ uint32_t wcnt[kWarps][256];   // (round << 16) | count
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  base_off[t] = hist[t * tiles + blockIdx.x];
+  run[t] = 0;
+  for (int w = 0; w < kWarps; ++w) wcnt[w][t] = 0xFFFF0000u;
+  __syncthreads();
+  const int tbase = blockIdx.x * kTile;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int r = 0; r < kItems; ++r) {
+    const int i = tbase + r * kThreads + t;
+    const bool valid = i < n;
+    const uint32_t key = valid ? kin[i] : 0u;
+    const uint32_t val = valid ? vin[i] : 0u;
+    const uint32_t dig = valid ? ((key >> shift) & 0xFF) : 256u;   // 256: invalid
+    const uint32_t peers = __match_any_sync(0xffffffffu, dig);
+    const uint32_t rank = __popc(peers & lt);
+    if (valid && rank == 0) wcnt[warp][dig] = ((uint32_t)r << 16) | (uint32_t)__popc(peers);
+    __syncthreads();
+    if (valid) {
+      uint32_t pre = 0;
+      for (int w = 0; w < warp; ++w) {
+        const uint32_t e = wcnt[w][dig];
+        if ((e >> 16) == (uint32_t)r) pre += e & 0xFFFFu;
+      }
+      const uint32_t pos = base_off[dig] + run[dig] + pre + rank;
+      kout[pos] = key;
+      vout[pos] = val;
+    }
+    __syncthreads();
+    {
+      uint32_t add = 0;
+      for (int w = 0; w < kWarps; ++w) {
+        const uint32_t e = wcnt[w][t];
+        if ((e >> 16) == (uint32_t)r) add += e & 0xFFFFu;
+      }
+      run[t] += add;
+    }
+    __syncthreads();
+  }
+}
+
+// --- pack records in Morton order -------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_pack(rg_gaussians g, rg_config c,
+                                                   const uint32_t* order, const float* box_orig,
+                                                   const int* flags, float4* geom, float* app,
+                                                   int stride, float* leaf_box) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= g.n) return;
+  const int i = (int)order[p];
+  const bool active = (flags[i] & 2) != 0;
+  float R[9], M[9], r2;
+  support_exact(g, c, i, active, R, M, r2);
+  const float* mu = g.mean + 3 * (size_t)i;
+  float4* gp = geom + 4 * (size_t)p;
+  gp[0] = make_float4(mu[0], mu[1], mu[2], g.density[i]);
+  gp[1] = make_float4(M[0], M[1], M[2], M[3]);
+  gp[2] = make_float4(M[4], M[5], M[6], M[7]);
+  gp[3] = make_float4(M[8], r2, __int_as_float(i), 0.0f);
+  for (int k = 0; k < 6; ++k) leaf_box[6 * (size_t)p + k] = box_orig[6 * (size_t)i + k];
+  // appearance: SH [(deg+1)^2 x 3], then per lobe (k0,k1,k2, lambda, p0,p1,p2)
+  const int nc = (g.sh_degree + 1) * (g.sh_degree + 1);
+  float* ap = app + (size_t)p * stride;
+  for (int k = 0; k < 3 * nc; ++k) ap[k] = g.sh[(size_t)i * 3 * nc + k];
+  for (int j = 0; j < g.sg_count; ++j) {
+    const size_t ij = (size_t)i * g.sg_count + j;
+    float* dst = ap + 3 * nc + 7 * j;
+    dst[0] = g.sg_amp[3 * ij]; dst[1] = g.sg_amp[3 * ij + 1]; dst[2] = g.sg_amp[3 * ij + 2];
+    dst[3] = g.sg_sharp[ij];
+    dst[4] = g.sg_axis[3 * ij]; dst[5] = g.sg_axis[3 * ij + 1]; dst[6] = g.sg_axis[3 * ij + 2];
+  }
+  for (int k = 3 * nc + 7 * g.sg_count; k < stride; ++k) ap[k] = 0.0f;
+}
+
+// --- Karras 2012 ---------------------------------------------------------------
+__device__ __forceinline__ int delta(const uint32_t* k, int n, int i, int j) {
+  if (j < 0 || j >= n) return -1;
+  const uint32_t a = k[i], b = k[j];
+  return a == b ? 32 + __clz(i ^ j) : __clz(a ^ b);
+}
+
+__global__ void __launch_bounds__(kThreads) k_karras(const uint32_t* k, int n, float4* nodes,
+                                                     int* parent_int, int* parent_leaf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n - 1) return;
+  const int d = (delta(k, n, i, i + 1) - delta(k, n, i, i - 1)) > 0 ? 1 : -1;
+  const int dmin = delta(k, n, i, i - d);
+  int lmax = 2;
+  while (delta(k, n, i, i + lmax * d) > dmin) lmax <<= 1;
+  int l = 0;
+  for (int t = lmax >> 1; t >= 1; t >>= 1)
+    if (delta(k, n, i, i + (l + t) * d) > dmin) l += t;
+  const int j = i + l * d;
+  const int dnode = delta(k, n, i, j);
+  int s = 0;
+  for (int div = 2;; div <<= 1) {
+    const int t = (l + div - 1) / div;
+    if (delta(k, n, i, i + (s + t) * d) > dnode) s += t;
+    if (t <= 1) break;
+  }
+  const int gamma = i + s * d + min(d, 0);
+  const int left = (min(i, j) == gamma) ? ~gamma : gamma;
+  const int right = (max(i, j) == gamma + 1) ? ~(gamma + 1) : gamma + 1;
+  nodes[4 * (size_t)i + 3] = make_float4(__int_as_float(left), __int_as_float(right), 0.f, 0.f);
+  if (left < 0) parent_leaf[~left] = i; else parent_int[left] = i;
+  if (right < 0) parent_leaf[~right] = i; else parent_int[right] = i;
+  if (i == 0) parent_int[0] = -1;
+}
+
+// --- refit ------------------------------------------------------------------------
+__device__ __forceinline__ void store_child_box(float4* nodes, int parent, bool is_left,
+                                                const float b[6]) {
+  float* w = reinterpret_cast<float*>(nodes + 4 * (size_t)parent);
+  const int o = is_left ? 0 : 6;
+  for (int k = 0; k < 6; ++k) __stcg(w + o + k, b[k]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_refit(const float* leaf_box, float4* nodes,
+                                                    const int* parent_int, const int* parent_leaf,
+                                                    int* cnt, float* root_box, int n) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  float b[6];
+  for (int k = 0; k < 6; ++k) b[k] = leaf_box[6 * (size_t)p + k];
+  if (n == 1) {
+    for (int k = 0; k < 6; ++k) root_box[k] = b[k];
+    return;
+  }
+  int child = ~p;
+  int node = parent_leaf[p];
+  while (true) {
+    const int4 ids = __ldcg(reinterpret_cast<const int4*>(nodes + 4 * (size_t)node + 3));
+    store_child_box(nodes, node, ids.x == child, b);
+    __threadfence();
+    if (atomicAdd(cnt + node, 1) == 0) return;     // first arrival: sibling finishes
+    __threadfence();
+    const float* w = reinterpret_cast<const float*>(nodes + 4 * (size_t)node);
+    float l[6], r[6];
+    for (int k = 0; k < 6; ++k) { l[k] = __ldcg(w + k); r[k] = __ldcg(w + 6 + k); }
+    for (int k = 0; k < 3; ++k) {
+      b[k] = fminf(l[k], r[k]);
+      b[3 + k] = fmaxf(l[3 + k], r[3 + k]);
+    }
+    if (node == 0) {
+      for (int k = 0; k < 6; ++k) root_box[k] = b[k];
+      return;
+    }
+    child = node;
+    node = parent_int[node];
+  }
+}
+
+inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace
+
+BvhLayout bvh_layout(int n, int deg, int lobes) {
+  BvhLayout L{};
+  const size_t nn = n > 0 ? (size_t)n : 1;
+  const size_t ni = n > 1 ? (size_t)(n - 1) : 1;
+  L.tiles = (int)((nn + kTile - 1) / kTile);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o += al(bytes); return r; };
+  L.geom = take(64 * nn);
+  L.app = take(sizeof(float) * (size_t)app_stride(deg, lobes) * nn);
+  L.nodes = take(64 * ni);
+  L.leaf_box = take(24 * nn);
+  L.root_box = take(32);
+  L.codes = take(4 * nn);
+  L.keys_a = take(4 * nn);
+  L.keys_b = take(4 * nn);
+  L.vals_a = take(4 * nn);
+  L.vals_b = take(4 * nn);
+  L.box_orig = take(24 * nn);
+  L.flags = take(4 * nn);
+  L.parent_int = take(4 * ni);
+  L.parent_leaf = take(4 * nn);
+  L.refit_cnt = take(4 * ni);
+  L.bounds = take(32);
+  L.hist = take(4 * 256 * (size_t)L.tiles);
+  L.total = o;
+  return L;
+}
+
+cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, const BvhLayout& L,
+                         cudaStream_t st) {
+  const int n = g.n;
+  float* root_box = reinterpret_cast<float*>(ws + L.root_box);
+  int* bounds = reinterpret_cast<int*>(ws + L.bounds);
+  k_init<<<1, 32, 0, st>>>(bounds, root_box);
+  if (n == 0) return cudaGetLastError();
+  const int blocks = (n + kThreads - 1) / kThreads;
+  float* box_orig = reinterpret_cast<float*>(ws + L.box_orig);
+  int* flags = reinterpret_cast<int*>(ws + L.flags);
+  k_preprocess<<<blocks, kThreads, 0, st>>>(g, c, box_orig, flags, bounds);
+  uint32_t* ka = reinterpret_cast<uint32_t*>(ws + L.keys_a);
+  uint32_t* kb = reinterpret_cast<uint32_t*>(ws + L.keys_b);
+  uint32_t* va = reinterpret_cast<uint32_t*>(ws + L.vals_a);
+  uint32_t* vb = reinterpret_cast<uint32_t*>(ws + L.vals_b);
+  k_morton<<<blocks, kThreads, 0, st>>>(g, flags, bounds,
+                                        reinterpret_cast<uint32_t*>(ws + L.codes), ka, va);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 8 * pass;
+    uint32_t *ki = (pass & 1) ? kb : ka, *vi = (pass & 1) ? vb : va;
+    uint32_t *ko = (pass & 1) ? ka : kb, *vo = (pass & 1) ? va : vb;
+    k_radix_hist<<<L.tiles, kThreads, 0, st>>>(ki, n, shift, hist, L.tiles);
+    k_radix_scan<<<1, 1024, 0, st>>>(hist, 256 * L.tiles);
+    k_radix_scatter<<<L.tiles, kThreads, 0, st>>>(ki, vi, ko, vo, n, shift, hist, L.tiles);
+  }
+  // after 4 passes the sorted keys / order are back in ka / va
+  float4* geom = reinterpret_cast<float4*>(ws + L.geom);
+  float* app = reinterpret_cast<float*>(ws + L.app);
+  float* leaf_box = reinterpret_cast<float*>(ws + L.leaf_box);
+  k_pack<<<blocks, kThreads, 0, st>>>(g, c, va, box_orig, flags, geom, app,
+                                      app_stride(g.sh_degree, g.sg_count), leaf_box);
+  float4* nodes = reinterpret_cast<float4*>(ws + L.nodes);
+  int* parent_int = reinterpret_cast<int*>(ws + L.parent_int);
+  int* parent_leaf = reinterpret_cast<int*>(ws + L.parent_leaf);
+  int* cnt = reinterpret_cast<int*>(ws + L.refit_cnt);
+  if (n > 1) {
+    const int bi = (n - 1 + kThreads - 1) / kThreads;
+    k_karras<<<bi, kThreads, 0, st>>>(ka, n, nodes, parent_int, parent_leaf);
+    cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)(n - 1), st);
+  }
+  k_refit<<<blocks, kThreads, 0, st>>>(leaf_box, nodes, parent_int, parent_leaf, cnt, root_box, n);
+  return cudaGetLastError();
+}
+
+}  // namespace rg

@@ -1,0 +1,236 @@
+// rg_internal.cuh -- device-side building blocks of libraygauss (sm_100a).
+//
+// The fp32 "decision" sequences below follow DESIGN.md ARITH-1..9 with every
+// operation explicitly rounded (__f*_rn) so nvcc cannot contract or reorder
+// them; they decide Morton codes, hit sets, sample positions and must agree
+// bit for bit with the oracle, which implements the same contract on its own
+// (oracle/rg_oracle.c; no code is shared).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rg.h"
+
+namespace rg {
+
+// ---------------------------------------------------------------------------
+// constants / layouts
+// ---------------------------------------------------------------------------
+constexpr int kMaxDeg = 3;
+constexpr int kMaxLobes = 7;
+constexpr int kMaxApp = 3 * 16 + 7 * 7;          // 97 floats
+constexpr int kStack = 64;                        // traversal stack entries
+constexpr int kACap = 32;                         // active-list capacity per ray
+constexpr int kGroup = 8;                         // samples per register group
+constexpr float kLog2e = 1.4426950408889634f;
+
+__host__ __device__ inline int app_floats(int deg, int lobes) {
+  return 3 * (deg + 1) * (deg + 1) + 7 * lobes;
+}
+__host__ __device__ inline int app_stride(int deg, int lobes) {
+  return (app_floats(deg, lobes) + 3) & ~3;
+}
+__host__ __device__ inline int grad_stride(int deg, int lobes) {
+  return 16 + app_stride(deg, lobes);
+}
+
+// geometry record, 64 B, Morton order:
+//  g0 = {mu.x, mu.y, mu.z, sigma~}   g1 = {M0, M1, M2, M3}
+//  g2 = {M4, M5, M6, M7}             g3 = {M8, r2 (<0: inactive), idx bits, 0}
+// node record, 64 B: n0 = {L.lo.xyz, L.hi.x} n1 = {L.hi.yz, R.lo.xy}
+//                    n2 = {R.lo.z, R.hi.xyz} n3 = {left, right (int bits), 0, 0}
+// child id >= 0: internal node, < 0: leaf ~pos.
+
+struct SceneView {
+  const float4* geom;
+  const float* app;
+  const float4* nodes;
+  const float* root_box;
+  int n, deg, lobes, app_stride;
+};
+
+// ---------------------------------------------------------------------------
+// exact fp32 helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float add_(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float mul_(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float div_(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float sqrt_(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ float fma_(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+// (a0*b0 + a1*b1) + a2*b2, each op rounded
+__device__ __forceinline__ float dot3_(float a0, float a1, float a2, float b0, float b1, float b2) {
+  return add_(add_(mul_(a0, b0), mul_(a1, b1)), mul_(a2, b2));
+}
+
+__device__ __forceinline__ uint32_t fkey(float f) {
+  uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(uint32_t k) {
+  uint32_t b = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+  return __uint_as_float(b);
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// ARITH-1: R(q), q = (w,x,y,z)
+__device__ __forceinline__ void rot_exact(float w, float x, float y, float z, float R[9]) {
+  const float xx = mul_(x, x), yy = mul_(y, y), zz = mul_(z, z);
+  const float xy = mul_(x, y), xz = mul_(x, z), yz = mul_(y, z);
+  const float wx = mul_(w, x), wy = mul_(w, y), wz = mul_(w, z);
+  R[0] = sub_(1.0f, mul_(2.0f, add_(yy, zz)));
+  R[1] = mul_(2.0f, sub_(xy, wz));
+  R[2] = mul_(2.0f, add_(xz, wy));
+  R[3] = mul_(2.0f, add_(xy, wz));
+  R[4] = sub_(1.0f, mul_(2.0f, add_(xx, zz)));
+  R[5] = mul_(2.0f, sub_(yz, wx));
+  R[6] = mul_(2.0f, sub_(xz, wy));
+  R[7] = mul_(2.0f, add_(yz, wx));
+  R[8] = sub_(1.0f, mul_(2.0f, add_(xx, yy)));
+}
+
+// ARITH-5: support interval of the ray against the ellipsoid of a geometry
+// record.  Returns false on miss.  Also returns d_l = M d and A = |d_l|^2.
+struct PairGeom {
+  float te, tx, tm, A;
+  float dl0, dl1, dl2;
+};
+__device__ __forceinline__ bool isect_exact(const float4& g0, const float4& g1, const float4& g2,
+                                            const float4& g3, const float3& o, const float3& d,
+                                            PairGeom& pg) {
+  const float r2 = g3.y;
+  const float v0 = sub_(o.x, g0.x), v1 = sub_(o.y, g0.y), v2 = sub_(o.z, g0.z);
+  const float ol0 = dot3_(g1.x, g1.y, g1.z, v0, v1, v2);
+  const float ol1 = dot3_(g1.w, g2.x, g2.y, v0, v1, v2);
+  const float ol2 = dot3_(g2.z, g2.w, g3.x, v0, v1, v2);
+  const float dl0 = dot3_(g1.x, g1.y, g1.z, d.x, d.y, d.z);
+  const float dl1 = dot3_(g1.w, g2.x, g2.y, d.x, d.y, d.z);
+  const float dl2 = dot3_(g2.z, g2.w, g3.x, d.x, d.y, d.z);
+  const float A = dot3_(dl0, dl1, dl2, dl0, dl1, dl2);
+  const float B = dot3_(ol0, ol1, ol2, dl0, dl1, dl2);
+  const float tm = -div_(B, A);
+  const float u0 = add_(ol0, mul_(tm, dl0));
+  const float u1 = add_(ol1, mul_(tm, dl1));
+  const float u2 = add_(ol2, mul_(tm, dl2));
+  const float qmin = dot3_(u0, u1, u2, u0, u1, u2);
+  if (!(qmin <= r2)) return false;
+  const float h = sqrt_(div_(sub_(r2, qmin), A));
+  pg.te = sub_(tm, h);
+  pg.tx = add_(tm, h);
+  pg.tm = tm;
+  pg.A = A;
+  pg.dl0 = dl0; pg.dl1 = dl1; pg.dl2 = dl2;
+  return true;
+}
+
+// Compensated x' = (o - mu) + tm * d (TwoSum / fma TwoProduct): the world
+// offset of the ray point at t_mid from the Gaussian centre, accurate to a few
+// ulp of |x'| although |o - mu| >> |x'|.  Value path only (never a decision).
+__device__ __forceinline__ float two_sum_err(float a, float b, float s) {
+  const float bb = sub_(s, a);
+  return add_(sub_(a, sub_(s, bb)), sub_(b, bb));
+}
+__device__ __forceinline__ float offset_at(float o, float mu, float tm, float d) {
+  const float v = sub_(o, mu);
+  const float ve = two_sum_err(o, -mu, v);
+  const float p = mul_(tm, d);
+  const float pe = fma_(tm, d, -p);
+  const float s = add_(v, p);
+  const float se = two_sum_err(v, p, s);
+  return add_(s, add_(se, add_(ve, pe)));
+}
+
+// ARITH-8: scene bbox clip
+__device__ __forceinline__ bool clip_exact(const float* box, const float3& o, const float3& d,
+                                           float t_near, float& t0, float& t1) {
+  if (!(box[0] <= box[3]) || !(box[1] <= box[4]) || !(box[2] <= box[5])) return false;
+  const float ix = div_(1.0f, d.x), iy = div_(1.0f, d.y), iz = div_(1.0f, d.z);
+  const float ax = mul_(sub_(box[0], o.x), ix), bx = mul_(sub_(box[3], o.x), ix);
+  const float ay = mul_(sub_(box[1], o.y), iy), by = mul_(sub_(box[4], o.y), iy);
+  const float az = mul_(sub_(box[2], o.z), iz), bz = mul_(sub_(box[5], o.z), iz);
+  t0 = fmaxf(fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fminf(az, bz)), t_near);
+  t1 = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fmaxf(az, bz));
+  return t0 < t1;
+}
+
+// ARITH-7: pinhole ray through pixel centre
+__device__ __forceinline__ void camera_ray(const rg_camera& cam, int px, int py, float3& o,
+                                           float3& d) {
+  const float xc = div_(sub_(add_((float)px, 0.5f), cam.cx), cam.fx);
+  const float yc = div_(sub_(add_((float)py, 0.5f), cam.cy), cam.fy);
+  const float* M = cam.c2w;
+  const float dw0 = add_(add_(mul_(M[0], xc), mul_(M[1], yc)), M[2]);
+  const float dw1 = add_(add_(mul_(M[4], xc), mul_(M[5], yc)), M[6]);
+  const float dw2 = add_(add_(mul_(M[8], xc), mul_(M[9], yc)), M[10]);
+  const float nrm = sqrt_(dot3_(dw0, dw1, dw2, dw0, dw1, dw2));
+  d = make_float3(div_(dw0, nrm), div_(dw1, nrm), div_(dw2, nrm));
+  o = make_float3(M[3], M[7], M[11]);
+}
+
+// ARITH-9
+__device__ __forceinline__ float sample_t(int k, float dt, float t0) {
+  return fma_(add_((float)k, 0.5f), dt, t0);
+}
+
+// ---------------------------------------------------------------------------
+// colour c_l(d) (Eq. 14-15): 3DGS real SH basis (L10) + SG lobes
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void sh_basis(int deg, float x, float y, float z, float Y[16]) {
+  Y[0] = 0.28209479177387814f;
+  if (deg < 1) return;
+  Y[1] = -0.4886025119029199f * y;
+  Y[2] = 0.4886025119029199f * z;
+  Y[3] = -0.4886025119029199f * x;
+  if (deg < 2) return;
+  const float xx = x * x, yy = y * y, zz = z * z;
+  Y[4] = 1.0925484305920792f * x * y;
+  Y[5] = -1.0925484305920792f * y * z;
+  Y[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+  Y[7] = -1.0925484305920792f * x * z;
+  Y[8] = 0.5462742152960396f * (xx - yy);
+  if (deg < 3) return;
+  Y[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
+  Y[10] = 2.890611442640554f * x * y * z;
+  Y[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
+  Y[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+  Y[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
+  Y[14] = 1.445305721320277f * z * (xx - yy);
+  Y[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
+}
+
+// ---------------------------------------------------------------------------
+// host-side launchers (defined in the .cu files)
+// ---------------------------------------------------------------------------
+struct BvhLayout {
+  size_t geom, app, nodes, leaf_box, root_box, codes, keys_a, keys_b, vals_a, vals_b,
+      box_orig, flags, parent_int, parent_leaf, refit_cnt, bounds, hist, total;
+  int tiles;
+};
+BvhLayout bvh_layout(int n, int deg, int lobes);
+cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, const BvhLayout& L,
+                         cudaStream_t st);
+cudaError_t launch_camera_rays(const rg_camera& cam, float* o, float* d, cudaStream_t st);
+cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,
+                           const rg_rays* rays, const rg_camera* cam, float* rgb, float* T,
+                           int32_t* replay, rg_stats* stats, int dbg_rays, int dbg_cap,
+                           int32_t* dbg_counts, int32_t* dbg_rec, cudaStream_t st);
+cudaError_t launch_backward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,
+                            const rg_rays* rays, const rg_camera* cam, const float* rgb,
+                            const float* T, const int32_t* replay, const float* d_rgb,
+                            const rg_gaussian_grads& grads, rg_stats* stats, float* gbuf,
+                            cudaStream_t st);
+cudaError_t launch_l1(const float* rgb, const float* target, int64_t n, float scale, float* d_rgb,
+                      float* loss, cudaStream_t st);
+
+}  // namespace rg

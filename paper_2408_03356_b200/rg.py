@@ -1,0 +1,346 @@
+"""Thin ctypes binding of the C-ABI in include/rg.h (libraygauss.so).
+
+Argument marshalling only: torch tensors provide device memory and the current
+CUDA stream; every step of the path runs in the library's sm_100a kernels.
+There is no CPU fallback: if the library cannot be loaded, or CUDA is not
+available, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+from . import build as _build
+
+__all__ = ["RGError", "Config", "Gaussians", "BVH", "lib", "build_bvh", "camera_rays",
+           "render_forward", "render_backward", "l1_loss_grad", "camera_struct", "STAT_KEYS"]
+
+STAT_KEYS = ("rays", "rays_hit", "slabs", "pairs", "evals", "samples", "overflows", "fetches",
+             "node_visits", "stack_overflows", "nonfinite_grads")
+
+
+class RGError(RuntimeError):
+    pass
+
+
+class _Gaussians(C.Structure):
+    _fields_ = [("n", C.c_int32), ("sh_degree", C.c_int32), ("sg_count", C.c_int32),
+                ("pad_", C.c_int32)] + [(k, C.c_void_p) for k in
+                                        ("mean", "quat", "scale", "density", "sh", "sg_amp",
+                                         "sg_sharp", "sg_axis")]
+
+
+class _Grads(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("mean", "quat", "scale", "density", "sh", "sg_amp",
+                                          "sg_sharp", "sg_axis")]
+
+
+class _Config(C.Structure):
+    _fields_ = [("dt", C.c_float), ("slab_samples", C.c_int32), ("sigma_eps", C.c_float),
+                ("t_eps", C.c_float), ("hit_capacity", C.c_int32), ("radius_mode", C.c_int32),
+                ("k_sigma", C.c_float), ("t_near", C.c_float), ("background", C.c_float * 3),
+                ("pad_", C.c_int32)]
+
+
+class _Rays(C.Structure):
+    _fields_ = [("n", C.c_int32), ("pad_", C.c_int32), ("origin", C.c_void_p), ("dir", C.c_void_p)]
+
+
+class _Camera(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("x0", C.c_int32), ("y0", C.c_int32),
+                ("x1", C.c_int32), ("y1", C.c_int32), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("c2w", C.c_float * 12)]
+
+
+class _BVH(C.Structure):
+    _fields_ = [("n", C.c_int32), ("sh_degree", C.c_int32), ("sg_count", C.c_int32),
+                ("app_stride", C.c_int32)] + [(k, C.c_void_p) for k in
+                                              ("geom", "app", "nodes", "leaf_box", "root_box",
+                                               "codes", "sorted_codes", "order")]
+
+
+EXPORTS = ("rg_status_string", "rg_version", "rg_bvh_workspace_bytes", "rg_build_bvh",
+           "rg_camera_rays", "rg_render_forward", "rg_backward_workspace_bytes",
+           "rg_render_backward", "rg_l1_loss_grad")
+
+_lib = None
+
+
+def lib(load_only: bool = False):
+    """Load libraygauss.so (building it in-tree with nvcc if missing/stale)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    if _build.stale():
+        try:
+            _build.build()
+        except Exception as e:  # noqa: BLE001
+            if not os.path.exists(path):
+                raise RGError(f"libraygauss.so missing and build failed: {e}") from e
+    try:
+        L = C.CDLL(path)
+    except OSError as e:
+        raise RGError(f"cannot load {path}: {e}") from e
+    P, I32, SZ = C.c_void_p, C.c_int32, C.c_size_t
+    L.rg_status_string.restype = C.c_char_p
+    L.rg_status_string.argtypes = [C.c_int]
+    L.rg_version.restype = C.c_char_p
+    L.rg_bvh_workspace_bytes.restype = SZ
+    L.rg_bvh_workspace_bytes.argtypes = [I32, I32, I32]
+    L.rg_build_bvh.restype = C.c_int
+    L.rg_build_bvh.argtypes = [P, P, P, SZ, P, P]
+    L.rg_camera_rays.restype = C.c_int
+    L.rg_camera_rays.argtypes = [P, P, P, P]
+    L.rg_render_forward.restype = C.c_int
+    L.rg_render_forward.argtypes = [P, P, P, P, P, P, P, P, P, I32, I32, P, P, P]
+    L.rg_backward_workspace_bytes.restype = SZ
+    L.rg_backward_workspace_bytes.argtypes = [I32, I32, I32]
+    L.rg_render_backward.restype = C.c_int
+    L.rg_render_backward.argtypes = [P, P, P, P, P, P, P, P, P, P, P, P, SZ, P]
+    L.rg_l1_loss_grad.restype = C.c_int
+    L.rg_l1_loss_grad.argtypes = [P, P, C.c_int64, C.c_float, P, P, P]
+    _lib = L
+    return L
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        msg = lib().rg_status_string(status).decode()
+        raise RGError(f"{what}: {msg} ({status})")
+
+
+def _require_cuda():
+    if not torch.cuda.is_available():
+        raise RGError("CUDA device required: libraygauss has no CPU path")
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return C.c_void_p(t.data_ptr()) if t.numel() > 0 else None
+
+
+@dataclass
+class Config:
+    dt: float = 2.5e-4
+    slab_samples: int = 8
+    sigma_eps: float = 0.1
+    t_eps: float = 1e-4
+    hit_capacity: int = 512
+    radius_mode: int = 0
+    k_sigma: float = 3.0
+    t_near: float = 0.0
+    background: tuple = (1.0, 1.0, 1.0)
+
+    @classmethod
+    def of(cls, p) -> "Config":
+        return cls(p.dt, p.slab_samples, p.sigma_eps, p.t_eps, p.hit_capacity, p.radius_mode,
+                   p.k_sigma, p.t_near, tuple(p.background))
+
+    def struct(self) -> _Config:
+        c = _Config()
+        c.dt, c.slab_samples, c.sigma_eps, c.t_eps = self.dt, self.slab_samples, self.sigma_eps, self.t_eps
+        c.hit_capacity, c.radius_mode, c.k_sigma, c.t_near = (self.hit_capacity, self.radius_mode,
+                                                              self.k_sigma, self.t_near)
+        for i in range(3):
+            c.background[i] = self.background[i]
+        return c
+
+
+GROUPS = ("mean", "quat", "scale", "density", "sh", "sg_amp", "sg_sharp", "sg_axis")
+
+
+class Gaussians:
+    """Activated parameters as contiguous fp32 CUDA tensors (caller layout of rg.h)."""
+
+    def __init__(self, mean, quat, scale, density, sh, sg_amp=None, sg_sharp=None, sg_axis=None,
+                 *, sh_degree=None, sg_count=None):
+        n = mean.shape[0]
+        self.sh_degree = int(sh_degree if sh_degree is not None else round(sh.shape[1] ** 0.5) - 1)
+        self.sg_count = int(sg_count if sg_count is not None else
+                            (0 if sg_amp is None else sg_amp.shape[1]))
+        dev = mean.device
+        z = lambda *s: torch.zeros(*s, dtype=torch.float32, device=dev)  # noqa: E731
+        self.mean, self.quat, self.scale, self.density, self.sh = [
+            t.contiguous().float() for t in (mean, quat, scale, density, sh)]
+        self.sg_amp = (sg_amp if sg_amp is not None else z(n, 0, 3)).contiguous().float()
+        self.sg_sharp = (sg_sharp if sg_sharp is not None else z(n, 0)).contiguous().float()
+        self.sg_axis = (sg_axis if sg_axis is not None else z(n, 0, 3)).contiguous().float()
+
+    @classmethod
+    def from_scene(cls, sc, device="cuda"):
+        t = lambda a: torch.from_numpy(a).to(device)  # noqa: E731
+        return cls(*[t(a) for a in sc.arrays()], sh_degree=sc.sh_degree, sg_count=sc.sg_count)
+
+    @property
+    def n(self):
+        return int(self.mean.shape[0])
+
+    def tensors(self):
+        return [getattr(self, k) for k in GROUPS]
+
+    def struct(self) -> _Gaussians:
+        s = _Gaussians()
+        s.n, s.sh_degree, s.sg_count = self.n, self.sh_degree, self.sg_count
+        for k in GROUPS:
+            setattr(s, k, _ptr(getattr(self, k)))
+        return s
+
+    def zeros_like_grads(self):
+        return {k: torch.zeros_like(getattr(self, k)) for k in GROUPS}
+
+
+class BVH:
+    def __init__(self, ws, handle: _BVH, scene: Gaussians):
+        self.ws = ws
+        self.h = handle
+        self.scene = scene   # keep parameters alive
+
+    def debug_views(self):
+        """Device arrays of the build for parity tests."""
+        n = self.h.n
+        dev = self.ws.device
+
+        def view(addr, count, dtype, itemsize):
+            if count <= 0:
+                return torch.zeros(0, dtype=dtype, device=dev)
+            base = self.ws.data_ptr()
+            off = addr - base
+            assert off % itemsize == 0
+            flat = self.ws.view(torch.uint8)[off:off + count * itemsize]
+            return flat.view(dtype)
+        return dict(
+            codes=view(self.h.codes, n, torch.int32, 4),
+            sorted_codes=view(self.h.sorted_codes, n, torch.int32, 4),
+            order=view(self.h.order, n, torch.int32, 4),
+            nodes=view(self.h.nodes, 16 * max(n - 1, 0), torch.float32, 4).reshape(-1, 16),
+            leaf_box=view(self.h.leaf_box, 6 * n, torch.float32, 4).reshape(-1, 6),
+            root_box=view(self.h.root_box, 6, torch.float32, 4),
+            geom=view(self.h.geom, 16 * n, torch.float32, 4).reshape(-1, 16),
+        )
+
+
+def build_bvh(scene: Gaussians, cfg: Config) -> BVH:
+    _require_cuda()
+    L = lib()
+    nbytes = int(L.rg_bvh_workspace_bytes(scene.n, scene.sh_degree, scene.sg_count))
+    ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=scene.mean.device)
+    h = _BVH()
+    gs, cs = scene.struct(), cfg.struct()
+    _check(L.rg_build_bvh(C.byref(gs), C.byref(cs), _ptr(ws), nbytes, C.byref(h), _stream()),
+           "rg_build_bvh")
+    return BVH(ws, h, scene)
+
+
+def camera_struct(cam) -> _Camera:
+    s = _Camera()
+    x0, y0, x1, y1 = cam.x0y0x1y1
+    s.width, s.height, s.x0, s.y0, s.x1, s.y1 = cam.width, cam.height, x0, y0, x1, y1
+    s.fx, s.fy, s.cx, s.cy = cam.fx, cam.fy, cam.cx, cam.cy
+    flat = [float(v) for v in cam.c2w.reshape(-1)]
+    for i in range(12):
+        s.c2w[i] = flat[i]
+    return s
+
+
+def camera_rays(cam, device="cuda"):
+    _require_cuda()
+    n = cam.n_rays
+    o = torch.empty(n, 3, dtype=torch.float32, device=device)
+    d = torch.empty(n, 3, dtype=torch.float32, device=device)
+    cs = camera_struct(cam)
+    _check(lib().rg_camera_rays(C.byref(cs), _ptr(o), _ptr(d), _stream()), "rg_camera_rays")
+    return o, d
+
+
+def _ray_args(rays, camera):
+    if (rays is None) == (camera is None):
+        raise RGError("pass exactly one of rays=(origin, dir) or camera=")
+    if rays is not None:
+        o, d = rays
+        r = _Rays()
+        r.n = int(o.shape[0])
+        r.origin, r.dir = _ptr(o.contiguous()), _ptr(d.contiguous())
+        return C.byref(r), None, r.n, (r, o, d)
+    cs = camera_struct(camera)
+    return None, C.byref(cs), camera.n_rays, (cs,)
+
+
+def render_forward(scene: Gaussians, bvh: BVH, cfg: Config, *, rays=None, camera=None,
+                   stats=None, debug=None, out=None):
+    """Returns dict(rgb [R,3], T [R], replay [R]) (+ debug counts/records)."""
+    _require_cuda()
+    rp, cp, n, keep = _ray_args(rays, camera)
+    dev = scene.mean.device
+    if out is None:
+        out = dict(rgb=torch.empty(n, 3, dtype=torch.float32, device=dev),
+                   T=torch.empty(n, dtype=torch.float32, device=dev),
+                   replay=torch.empty(n, dtype=torch.int32, device=dev))
+    dbg_n, dbg_cap, dc, dr = 0, 0, None, None
+    if debug is not None:
+        dbg_n, dbg_cap = debug
+        dc = torch.zeros(dbg_n, dtype=torch.int32, device=dev)
+        dr = torch.full((dbg_n, dbg_cap, 2), -1, dtype=torch.int32, device=dev)
+        out["debug_counts"], out["debug_records"] = dc, dr
+    gs, cs = scene.struct(), cfg.struct()
+    _check(lib().rg_render_forward(C.byref(gs), C.byref(bvh.h), C.byref(cs), rp, cp,
+                                   _ptr(out["rgb"]), _ptr(out["T"]), _ptr(out["replay"]),
+                                   _ptr(stats), dbg_n, dbg_cap, _ptr(dc), _ptr(dr), _stream()),
+           "rg_render_forward")
+    del keep
+    return out
+
+
+def backward_workspace(scene: Gaussians):
+    nbytes = int(lib().rg_backward_workspace_bytes(scene.n, scene.sh_degree, scene.sg_count))
+    return torch.empty(max(nbytes // 4, 4), dtype=torch.float32, device=scene.mean.device)
+
+
+def render_backward(scene: Gaussians, bvh: BVH, cfg: Config, fwd: dict, d_rgb, *, rays=None,
+                    camera=None, grads=None, stats=None, ws=None):
+    """Accumulates dL/dparams for L = sum <d_rgb, rgb> into `grads` (dict of tensors)."""
+    _require_cuda()
+    rp, cp, n, keep = _ray_args(rays, camera)
+    if grads is None:
+        grads = scene.zeros_like_grads()
+    if ws is None:
+        ws = backward_workspace(scene)
+    g = _Grads()
+    for k in GROUPS:
+        setattr(g, k, _ptr(grads[k]))
+    gs, cs = scene.struct(), cfg.struct()
+    d_rgb = d_rgb.contiguous()
+    _check(lib().rg_render_backward(C.byref(gs), C.byref(bvh.h), C.byref(cs), rp, cp,
+                                    _ptr(fwd["rgb"]), _ptr(fwd["T"]), _ptr(fwd["replay"]),
+                                    _ptr(d_rgb), C.byref(g), _ptr(stats), _ptr(ws),
+                                    ws.numel() * 4, _stream()), "rg_render_backward")
+    del keep
+    return grads
+
+
+def l1_loss_grad(rgb, target, scale, d_rgb=None, loss=None):
+    _require_cuda()
+    if d_rgb is None:
+        d_rgb = torch.empty_like(rgb)
+    if loss is None:
+        loss = torch.zeros(1, dtype=torch.float32, device=rgb.device)
+    _check(lib().rg_l1_loss_grad(_ptr(rgb), _ptr(target), rgb.numel(), float(scale), _ptr(d_rgb),
+                                 _ptr(loss), _stream()), "rg_l1_loss_grad")
+    return d_rgb, loss
+
+
+def new_stats(device="cuda"):
+    return torch.zeros(16, dtype=torch.int64, device=device)
+
+
+def stats_dict(t):
+    v = t.cpu().tolist()
+    return {k: int(v[i]) for i, k in enumerate(STAT_KEYS)}
