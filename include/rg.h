@@ -25,7 +25,7 @@
  *       sh [n,(sh_degree+1)^2,3], sg_amp [n,sg_count,3], sg_sharp [n,sg_count],
  *       sg_axis [n,sg_count,3]; rays / images [R,3] row-major, R = ray count.
  *   - Thread safety: calls on different streams with different workspaces are
- *     independent; there is no global mutable state.
+ *     independent; the only global state is the diagnostic launch counter.
  */
 #ifndef RAYGAUSS_RG_H
 #define RAYGAUSS_RG_H
@@ -128,6 +128,9 @@ typedef struct {
 const char* rg_status_string(rg_status s);
 /* library build string (host) */
 const char* rg_version(void);
+/* diagnostic: kernels enqueued by this library since load (host; the only
+   process-wide state, a relaxed atomic counter) */
+unsigned long long rg_kernel_launches(void);
 
 /* ---- BVH build -------------------------------- */
 /* Workspace bytes for rg_build_bvh on n Gaussians with the given appearance

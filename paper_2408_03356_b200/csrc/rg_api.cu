@@ -4,7 +4,15 @@
 
 #include "rg_internal.cuh"
 
+#include <atomic>
+
 using namespace rg;
+
+namespace rg {
+// diagnostic: number of kernels this library enqueued (process-wide)
+static std::atomic<unsigned long long> g_launches{0};
+void count_launches(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace rg
 
 namespace {
 
@@ -60,6 +68,8 @@ const char* rg_status_string(rg_status s) {
   }
   return "unknown status";
 }
+
+unsigned long long rg_kernel_launches(void) { return g_launches.load(); }
 
 const char* rg_version(void) {
   return "libraygauss abi=1 sm_100a (LBVH + slab ray casting, fwd+bwd)";

@@ -386,7 +386,9 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
   float* root_box = reinterpret_cast<float*>(ws + L.root_box);
   int* bounds = reinterpret_cast<int*>(ws + L.bounds);
   k_init<<<1, 32, 0, st>>>(bounds, root_box);
+  count_launches(1);
   if (n == 0) return cudaGetLastError();
+  count_launches(n > 1 ? 17 : 16);
   const int blocks = (n + kThreads - 1) / kThreads;
   float* box_orig = reinterpret_cast<float*>(ws + L.box_orig);
   int* flags = reinterpret_cast<int*>(ws + L.flags);

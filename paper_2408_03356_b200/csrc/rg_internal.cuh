@@ -230,6 +230,7 @@ cudaError_t launch_backward(const rg_gaussians& g, const rg_bvh& b, const rg_con
                             const float* T, const int32_t* replay, const float* d_rgb,
                             const rg_gaussian_grads& grads, rg_stats* stats, float* gbuf,
                             cudaStream_t st);
+void count_launches(unsigned n);
 cudaError_t launch_l1(const float* rgb, const float* target, int64_t n, float scale, float* d_rgb,
                       float* loss, cudaStream_t st);
 

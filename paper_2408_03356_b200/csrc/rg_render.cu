@@ -435,7 +435,12 @@ __global__ void __launch_bounds__(kBlock) k_render(const RenderArgs P) {
       while (n_in < count && act[n_in].te <= thi) ++n_in;
       const int n_use = min(n_in, K);
       const bool more = (n_in == kACap) && !exhausted && (K > kACap);
-      if (n_in > K) cnt.overflows++;
+      if (n_in > K) {
+        cnt.overflows++;
+      } else if (!BWD && n_in == K && n_in == kACap && !exhausted &&
+                 fetch(P.S, o, d, inv, oinv, tlo, thi, cursor, 1, hk, hp, cnt) > 0) {
+        cnt.overflows++;   // exactly K held, at least one more member beyond the cursor
+      }
       if (dbg)
         for (int e = 0; e < n_use; ++e)
           if (dbg_n < P.dbg_cap) {
@@ -664,7 +669,7 @@ void ray_grid(RenderArgs& A, const rg_rays* rays, const rg_camera* cam, dim3& gr
 
 cudaError_t launch_camera_rays(const rg_camera& cam, float* o, float* d, cudaStream_t st) {
   const int n = (cam.x1 - cam.x0) * (cam.y1 - cam.y0);
-  if (n > 0) k_camera_rays<<<(n + 255) / 256, 256, 0, st>>>(cam, o, d);
+  if (n > 0) { k_camera_rays<<<(n + 255) / 256, 256, 0, st>>>(cam, o, d); count_launches(1); }
   return cudaGetLastError();
 }
 
@@ -683,6 +688,7 @@ cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_conf
   A.dbg_rays = dbg_rec ? dbg_rays : 0;
   A.dbg_cap = dbg_cap; A.dbg_counts = dbg_counts; A.dbg_rec = dbg_rec;
   k_render<false><<<grid, kBlock, 0, st>>>(A);
+  count_launches(1);
   return cudaGetLastError();
 }
 
@@ -701,9 +707,11 @@ cudaError_t launch_backward(const rg_gaussians& g, const rg_bvh& b, const rg_con
   if (b.n > 0) cudaMemsetAsync(gbuf, 0, sizeof(float) * (size_t)gs * b.n, st);
   A.stats = stats;
   A.rgb_in = rgb; A.replay_in = replay; A.d_rgb = d_rgb; A.gbuf = gbuf; A.gstride = gs;
-  if (A.n_rays > 0) k_render<true><<<grid, kBlock, 0, st>>>(A);
-  if (b.n > 0)
+  if (A.n_rays > 0) { k_render<true><<<grid, kBlock, 0, st>>>(A); count_launches(1); }
+  if (b.n > 0) {
     k_finalize<<<(b.n + 255) / 256, 256, 0, st>>>(gbuf, gs, b.order, g, grads, stats);
+    count_launches(1);
+  }
   return cudaGetLastError();
 }
 
@@ -712,6 +720,7 @@ cudaError_t launch_l1(const float* rgb, const float* target, int64_t n, float sc
   if (n > 0) {
     const int64_t nb = (n + 255) / 256; const int blocks = (int)(nb < 148 * 8 ? nb : 148 * 8);
     k_l1<<<blocks, 256, 0, st>>>(rgb, target, n, scale, d_rgb, loss);
+    count_launches(1);
   }
   return cudaGetLastError();
 }

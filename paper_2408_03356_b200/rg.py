@@ -62,7 +62,7 @@ class _BVH(C.Structure):
                                                "codes", "sorted_codes", "order")]
 
 
-EXPORTS = ("rg_status_string", "rg_version", "rg_bvh_workspace_bytes", "rg_build_bvh",
+EXPORTS = ("rg_status_string", "rg_version", "rg_kernel_launches", "rg_bvh_workspace_bytes", "rg_build_bvh",
            "rg_camera_rays", "rg_render_forward", "rg_backward_workspace_bytes",
            "rg_render_backward", "rg_l1_loss_grad")
 
@@ -89,6 +89,7 @@ def lib(load_only: bool = False):
     L.rg_status_string.restype = C.c_char_p
     L.rg_status_string.argtypes = [C.c_int]
     L.rg_version.restype = C.c_char_p
+    L.rg_kernel_launches.restype = C.c_ulonglong
     L.rg_bvh_workspace_bytes.restype = SZ
     L.rg_bvh_workspace_bytes.argtypes = [I32, I32, I32]
     L.rg_build_bvh.restype = C.c_int
@@ -228,11 +229,21 @@ class BVH:
         )
 
 
-def build_bvh(scene: Gaussians, cfg: Config) -> BVH:
+def bvh_workspace(scene: Gaussians):
+    nbytes = int(lib().rg_bvh_workspace_bytes(scene.n, scene.sh_degree, scene.sg_count))
+    return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=scene.mean.device)
+
+
+def build_bvh(scene: Gaussians, cfg: Config, ws=None) -> BVH:
+    """Full LBVH rebuild (UpdateBVH).  `ws` (from bvh_workspace) may be
+    reused across calls; the returned BVH is valid until ws is rebuilt."""
     _require_cuda()
     L = lib()
     nbytes = int(L.rg_bvh_workspace_bytes(scene.n, scene.sh_degree, scene.sg_count))
-    ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=scene.mean.device)
+    if ws is None:
+        ws = bvh_workspace(scene)
+    if ws.numel() < nbytes:
+        raise RGError("bvh workspace too small")
     h = _BVH()
     gs, cs = scene.struct(), cfg.struct()
     _check(L.rg_build_bvh(C.byref(gs), C.byref(cs), _ptr(ws), nbytes, C.byref(h), _stream()),
@@ -335,6 +346,10 @@ def l1_loss_grad(rgb, target, scale, d_rgb=None, loss=None):
     _check(lib().rg_l1_loss_grad(_ptr(rgb), _ptr(target), rgb.numel(), float(scale), _ptr(d_rgb),
                                  _ptr(loss), _stream()), "rg_l1_loss_grad")
     return d_rgb, loss
+
+
+def kernel_launches() -> int:
+    return int(lib().rg_kernel_launches())
 
 
 def new_stats(device="cuda"):
