@@ -101,6 +101,8 @@ typedef struct {
   const void* geom;        /* [n] 64-B records, Morton order */
   const float* app;        /* [n, app_stride] appearance, Morton order */
   const void* nodes;       /* [n-1] 64-B internal nodes (child boxes + child ids) */
+  const void* wide;        /* 32-wide collapse of the Karras tree (traversal structure) */
+  const int32_t* wide_info;/* device [4]: wide node count, -, -, rounds left unfinished */
   const float* leaf_box;   /* [n,6] padded AABBs, Morton order */
   const float* root_box;   /* [6] scene bbox = union of active AABBs */
   const uint32_t* codes;   /* [n] Morton codes, caller order */

@@ -42,7 +42,8 @@ bool gaussians_ok(const rg_gaussians* g) {
 bool bvh_ok(const rg_bvh* b, const rg_gaussians* g) {
   if (!b || !b->root_box) return false;
   if (b->n != g->n || b->sh_degree != g->sh_degree || b->sg_count != g->sg_count) return false;
-  if (b->n > 0 && (!b->geom || !b->app || !b->order || (b->n > 1 && !b->nodes))) return false;
+  if (b->n > 0 && (!b->geom || !b->app || !b->order || !b->wide || (b->n > 1 && !b->nodes)))
+    return false;
   return true;
 }
 
@@ -100,6 +101,8 @@ rg_status rg_build_bvh(const rg_gaussians* g, const rg_config* cfg, void* ws, si
   b.geom = w + L.geom;
   b.app = reinterpret_cast<const float*>(w + L.app);
   b.nodes = w + L.nodes;
+  b.wide = w + L.wide;
+  b.wide_info = reinterpret_cast<const int32_t*>(w + L.wcounts);
   b.leaf_box = reinterpret_cast<const float*>(w + L.leaf_box);
   b.root_box = reinterpret_cast<const float*>(w + L.root_box);
   b.codes = reinterpret_cast<const uint32_t*>(w + L.codes);

@@ -348,6 +348,98 @@ __global__ void __launch_bounds__(kThreads) k_refit(const float* leaf_box, float
   }
 }
 
+// --- collapse of the binary tree into 32-wide nodes (traversal structure) --------
+// Greedy top-down: a wide node's children are a cut of the binary subtree,
+// grown by repeatedly opening the internal entry with the largest box surface
+// area until 32 entries (or only leaves) remain.  Level-synchronous rounds with
+// device-side work queues (binary id, wide id).
+__device__ __forceinline__ float box_area(const float* b) {
+  const float dx = b[3] - b[0], dy = b[4] - b[1], dz = b[5] - b[2];
+  return (dx < 0.f || dy < 0.f || dz < 0.f) ? -1.f : dx * dy + dy * dz + dz * dx;
+}
+
+__global__ void k_collapse_init(int n, const float* leaf_box, WideNode* wide, int2* wq,
+                                int* counts) {
+  const int l = threadIdx.x;
+  if (l < 4) counts[l] = 0;
+  if (n == 1) {
+    wide[0].lox[l] = l == 0 ? leaf_box[0] : INFINITY;
+    wide[0].loy[l] = l == 0 ? leaf_box[1] : INFINITY;
+    wide[0].loz[l] = l == 0 ? leaf_box[2] : INFINITY;
+    wide[0].hix[l] = l == 0 ? leaf_box[3] : -INFINITY;
+    wide[0].hiy[l] = l == 0 ? leaf_box[4] : -INFINITY;
+    wide[0].hiz[l] = l == 0 ? leaf_box[5] : -INFINITY;
+    wide[0].child[l] = l == 0 ? ~0 : kWideEmpty;
+    if (l == 0) counts[0] = 1;
+  } else if (l == 0) {
+    wq[0] = make_int2(0, 0);   // binary root -> wide node 0
+    counts[0] = 1;             // wide nodes allocated
+    counts[1] = 1;             // items in the current queue
+  }
+}
+
+__global__ void __launch_bounds__(128) k_collapse(const float4* nodes, const float* leaf_box,
+                                                  WideNode* wide, const int2* qin, int2* qout,
+                                                  int* counts, int in_slot, int out_slot) {
+  const int nin = counts[in_slot];
+  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < nin; it += gridDim.x * blockDim.x) {
+    const int2 job = qin[it];
+    int ids[kWide];
+    float bx[kWide][6];
+    int m = 0;
+    {
+      const float* w = reinterpret_cast<const float*>(nodes + 4 * (size_t)job.x);
+      const int4 c = *reinterpret_cast<const int4*>(nodes + 4 * (size_t)job.x + 3);
+      ids[0] = c.x; ids[1] = c.y;
+      for (int k = 0; k < 6; ++k) { bx[0][k] = w[k]; bx[1][k] = w[6 + k]; }
+      m = 2;
+    }
+    while (m < kWide) {
+      int best = -1;
+      float ba = -2.f;
+      for (int k = 0; k < m; ++k)
+        if (ids[k] >= 0) {
+          const float a = box_area(bx[k]);
+          if (a > ba) { ba = a; best = k; }
+        }
+      if (best < 0) break;
+      const int b = ids[best];
+      const float* w = reinterpret_cast<const float*>(nodes + 4 * (size_t)b);
+      const int4 c = *reinterpret_cast<const int4*>(nodes + 4 * (size_t)b + 3);
+      ids[best] = c.x;
+      for (int k = 0; k < 6; ++k) bx[best][k] = w[k];
+      ids[m] = c.y;
+      for (int k = 0; k < 6; ++k) bx[m][k] = w[6 + k];
+      ++m;
+    }
+    WideNode& W = wide[job.y];
+    for (int k = 0; k < kWide; ++k) {
+      if (k < m) {
+        int child = ids[k];
+        if (child >= 0) {
+          const int wid = atomicAdd(counts + 0, 1);
+          const int slot = atomicAdd(counts + out_slot, 1);
+          qout[slot] = make_int2(child, wid);
+          child = wid;
+        }
+        W.lox[k] = bx[k][0]; W.loy[k] = bx[k][1]; W.loz[k] = bx[k][2];
+        W.hix[k] = bx[k][3]; W.hiy[k] = bx[k][4]; W.hiz[k] = bx[k][5];
+        W.child[k] = child;
+      } else {
+        W.lox[k] = W.loy[k] = W.loz[k] = INFINITY;
+        W.hix[k] = W.hiy[k] = W.hiz[k] = -INFINITY;
+        W.child[k] = kWideEmpty;
+      }
+    }
+  }
+}
+
+__global__ void k_collapse_next(int* counts, int in_slot) {
+  counts[in_slot] = 0;   // the consumed queue becomes the next output queue
+}
+
+__global__ void k_collapse_check(int* counts, int last_out) { counts[3] = counts[last_out]; }
+
 inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace
@@ -376,6 +468,10 @@ BvhLayout bvh_layout(int n, int deg, int lobes) {
   L.refit_cnt = take(4 * ni);
   L.bounds = take(32);
   L.hist = take(4 * 256 * (size_t)L.tiles);
+  L.wide = take(sizeof(WideNode) * wide_capacity(n));
+  L.wq_a = take(8 * nn);
+  L.wq_b = take(8 * nn);
+  L.wcounts = take(16);
   L.total = o;
   return L;
 }
@@ -424,6 +520,24 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
     cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)(n - 1), st);
   }
   k_refit<<<blocks, kThreads, 0, st>>>(leaf_box, nodes, parent_int, parent_leaf, cnt, root_box, n);
+  // 32-wide collapse (level-synchronous; queue slots 1/2 alternate)
+  WideNode* wide = reinterpret_cast<WideNode*>(ws + L.wide);
+  int2* qa = reinterpret_cast<int2*>(ws + L.wq_a);
+  int2* qb = reinterpret_cast<int2*>(ws + L.wq_b);
+  int* wc = reinterpret_cast<int*>(ws + L.wcounts);
+  k_collapse_init<<<1, 32, 0, st>>>(n, leaf_box, wide, qa, wc);
+  count_launches(1);
+  if (n > 1) {
+    const int grid = 148 * 4;
+    for (int r = 0; r < kCollapseRounds; ++r) {
+      const int in_slot = 1 + (r & 1), out_slot = 2 - (r & 1);
+      k_collapse<<<grid, 128, 0, st>>>(nodes, leaf_box, wide, (r & 1) ? qb : qa,
+                                       (r & 1) ? qa : qb, wc, in_slot, out_slot);
+      k_collapse_next<<<1, 1, 0, st>>>(wc, in_slot);
+    }
+    k_collapse_check<<<1, 1, 0, st>>>(wc, 2 - ((kCollapseRounds - 1) & 1));
+    count_launches(2 * kCollapseRounds + 1);
+  }
   return cudaGetLastError();
 }
 

@@ -42,10 +42,22 @@ __host__ __device__ inline int grad_stride(int deg, int lobes) {
 //                    n2 = {R.lo.z, R.hi.xyz} n3 = {left, right (int bits), 0, 0}
 // child id >= 0: internal node, < 0: leaf ~pos.
 
+// 32-wide BVH node (collapse of the Karras tree, one child per warp lane):
+// SoA child boxes and child ids; child >= 0: wide node, < 0: leaf ~pos,
+// kWideEmpty: unused slot (its box is empty).
+constexpr int kWide = 32;
+constexpr int kWideEmpty = 0x7FFFFFFF;
+struct WideNode {
+  float lox[kWide], loy[kWide], loz[kWide], hix[kWide], hiy[kWide], hiz[kWide];
+  int child[kWide];
+};
+__host__ __device__ inline size_t wide_capacity(int n) { return (size_t)(n / 2 + 2); }
+
 struct SceneView {
   const float4* geom;
   const float* app;
   const float4* nodes;
+  const WideNode* wide;
   const float* root_box;
   int n, deg, lobes, app_stride;
 };
@@ -214,9 +226,11 @@ __device__ __forceinline__ void sh_basis(int deg, float x, float y, float z, flo
 // ---------------------------------------------------------------------------
 struct BvhLayout {
   size_t geom, app, nodes, leaf_box, root_box, codes, keys_a, keys_b, vals_a, vals_b,
-      box_orig, flags, parent_int, parent_leaf, refit_cnt, bounds, hist, total;
+      box_orig, flags, parent_int, parent_leaf, refit_cnt, bounds, hist, wide, wq_a, wq_b,
+      wcounts, total;
   int tiles;
 };
+constexpr int kCollapseRounds = 40;
 BvhLayout bvh_layout(int n, int deg, int lobes);
 cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, const BvhLayout& L,
                          cudaStream_t st);

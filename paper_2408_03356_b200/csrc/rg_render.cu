@@ -1,5 +1,5 @@
 // rg_render.cu -- slab-by-slab volume ray casting of the Gaussians through the
-// LBVH, forward and backward:
+// BVH, forward and backward:
 //
 //   PAPER.md Alg. 2: per ray, bbox clip, then slabs of B samples
 //   of length dt*B; per slab the set of Gaussians whose support overlaps the
@@ -9,26 +9,35 @@
 //   samples (Eq. 10-16) and composite front to back (Eq. 4); early
 //   termination at slab granularity when T <= T_eps.
 //
-// B200 design: one thread per ray, 8x4-pixel warps; instead of
-// a BVH traversal per slab, each ray keeps a sorted ACTIVE LIST (local memory,
-// capacity kACap) of its upcoming/overlapping Gaussians, refilled by a
-// k-nearest-by-t_entry traversal ("fetch the next k after a cursor") with a
-// short stack; empty slabs are skipped exactly (jump to the slab holding the
-// next t_entry).  Per-slab hit sets are reproduced bit for bit from the exact
-// fp32 intervals.  Per-pair work (interval, colour, exponent coefficients) is
-// done once per (ray, Gaussian) and reused across the slabs it spans.
-// Backward replays the same march, recomputes each slab's samples, walks them
-// front to back with suffix = P - prefix (L16), accumulates four per-pair
-// moments and scatters 16 + app_stride floats per pair with float4 atomics
-// into a Morton-ordered buffer; k_finalize converts (mu, M) -> (mu, q, s) and
-// un-permutes to caller order.
+// B200 design: ONE WARP PER RAY.  The ray keeps a sorted
+// ACTIVE LIST (shared memory, capacity kA) of its upcoming/overlapping
+// Gaussians with their per-pair data (exact interval, weight-exponent
+// polynomial, colour), refilled by a warp-cooperative k-nearest-by-t_entry
+// traversal of the 32-wide BVH ("next k keys after a cursor"): one node visit
+// = 32 lanes testing the node's 32 child boxes, leaf children tested exactly
+// by their lane, the k-buffer held one key per lane (rank/ballot merge),
+// internal children pushed nearest-last on a shared stack.  Empty slabs are
+// skipped exactly (jump to the slab holding the next t_entry).  Integration
+// maps lanes to (entry-subset x sample) and reduces with shuffles;
+// compositing is a segmented scan over the slab's samples with the optical
+// depth accumulated (Kahan) so T does not drift over thousands of samples.
+// Backward replays the same march, walks each sample group front to back with
+// suffix = P - prefix (L16), accumulates per-pair moments in shared memory
+// and scatters each pair's 16 + app_stride gradient floats as one coalesced
+// burst of float4 atomics (one per lane) into a Morton-ordered buffer;
+// k_finalize converts (mu, M) -> (mu, q, s) and un-permutes.
 #include "rg_internal.cuh"
 
 namespace rg {
 
 namespace {
 
-constexpr int kBlock = 128;
+constexpr int kWarps = 4;              // rays (warps) per block
+constexpr int kBlock = 32 * kWarps;
+constexpr int kA = 64;                 // persistent active-list capacity
+constexpr int kSlots = kA + 32;        // + one transient chunk (slab sets > kA)
+constexpr int kStk = 256;              // traversal stack (wide nodes)
+constexpr unsigned kFull = 0xffffffffu;
 
 struct Counters {
   uint32_t slabs, pairs, evals, samples, overflows, fetches, nodes, stackov;
@@ -39,7 +48,7 @@ struct RenderArgs {
   rg_config c;
   int cam_mode;
   rg_camera cam;
-  int rw, rh;              // camera rect size
+  int rw, rh, tiles_x;
   const float* ro;
   const float* rd;
   int n_rays;
@@ -58,13 +67,27 @@ struct RenderArgs {
   int gstride;
 };
 
-struct Entry {
-  float te, tx, tm, c0, c1, c2, cr, cg, cb;
-  int pos;
-  uint32_t idx;
+struct WarpMem {
+  float te[kSlots], tx[kSlots], tm[kSlots], c0[kSlots], c1[kSlots], c2[kSlots];
+  float cr[kSlots], cg[kSlots], cb[kSlots];
+  int pos[kSlots];
+  uint32_t idx[kSlots];
+  int stk[kStk];
+  unsigned long long kscr[32];
+  uint32_t pscr[32];
+  float Y[16];
+};
+struct WarpAcc {
+  float a[6][kSlots];   // Sw, Sw1, Sw2, dc_r, dc_g, dc_b per slot
 };
 
-__device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ unsigned long long shfl64(unsigned long long v, int src) {
+  const unsigned lo = __shfl_sync(kFull, (unsigned)v, src);
+  const unsigned hi = __shfl_sync(kFull, (unsigned)(v >> 32), src);
+  return ((unsigned long long)hi << 32) | lo;
+}
 
 // conservative ray/AABB overlap (sign-selected slabs: empty boxes never hit)
 __device__ __forceinline__ void box_t(float lx, float ly, float lz, float hx, float hy, float hz,
@@ -79,65 +102,105 @@ __device__ __forceinline__ void box_t(float lx, float ly, float lz, float hx, fl
   tf = fminf(fminf(fx, fy), fz);
 }
 
-// Collect, in ascending (t_entry, index) key order, the `kmax` smallest keys
-// > cursor among Gaussians whose exact support interval satisfies
-// t_exit >= seg_lo and t_entry <= seg_hi.  Node pruning: segment overlap and,
-// once kmax keys are held, box entry > current kmax-th t_entry.
-__device__ int fetch(const SceneView& S, const float3& o, const float3& d, const float3& inv,
-                     const float3& oinv, float seg_lo, float seg_hi, uint64_t cursor, int kmax,
-                     uint64_t* hk, uint32_t* hp, Counters& cnt) {
-  cnt.fetches++;
-  int nb = 0;
+struct Ray {
+  float3 o, d, inv, oinv;
+};
+
+// Warp-cooperative k-nearest query on the 32-wide BVH: the kmax (<= 32)
+// smallest keys (t_entry bits, index) > cursor among Gaussians whose exact
+// support interval satisfies t_exit >= seg_lo and t_entry <= seg_hi.
+// Result: lane l < return value holds the l-th smallest key and its position.
+__device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo, float seg_hi,
+                     unsigned long long cursor, int kmax, unsigned long long& key, uint32_t& pos,
+                     Counters& cnt) {
+  const unsigned lane = lane_id();
+  const unsigned lt_mask = (1u << lane) - 1u;
+  if (lane == 0) cnt.fetches++;
+  key = ~0ull;
+  pos = 0;
+  int nk = 0;
   float te_lim = INFINITY;
+  unsigned long long kth = ~0ull;
   const float slack = 1e-5f * (fabsf(seg_lo) + fabsf(seg_hi)) + 1e-6f;
   const float lo_s = seg_lo - slack, hi_s = seg_hi + slack;
-  int stk[kStack];
-  int sp = 0;
-  stk[sp++] = (S.n == 1) ? ~0 : 0;
+  int sp = 1;
+  if (lane == 0) M.stk[0] = 0;
+  __syncwarp();
   while (sp > 0) {
-    const int id = stk[--sp];
-    if (id >= 0) {
-      cnt.nodes++;
-      const float4* np = S.nodes + 4 * (size_t)id;
-      const float4 a = ldg4(np), b = ldg4(np + 1), c = ldg4(np + 2), e = ldg4(np + 3);
-      float ln, lf, rn, rf;
-      box_t(a.x, a.y, a.z, a.w, b.x, b.y, inv, oinv, ln, lf);
-      box_t(b.z, b.w, c.x, c.y, c.z, c.w, inv, oinv, rn, rf);
-      const float lim = te_lim + slack;
-      const bool hl = ln <= lf && lf >= lo_s && ln <= hi_s && ln <= lim;
-      const bool hr = rn <= rf && rf >= lo_s && rn <= hi_s && rn <= lim;
-      const int cl = __float_as_int(e.x), cr = __float_as_int(e.y);
-      if (hl && hr) {
-        if (sp + 2 > kStack) { cnt.stackov++; continue; }
-        const bool lfirst = ln <= rn;
-        stk[sp++] = lfirst ? cr : cl;
-        stk[sp++] = lfirst ? cl : cr;
-      } else if (hl || hr) {
-        if (sp + 1 > kStack) { cnt.stackov++; continue; }
-        stk[sp++] = hl ? cl : cr;
-      }
-    } else {
-      const int p = ~id;
-      const float4* gp = S.geom + 4 * (size_t)p;
-      const float4 g0 = ldg4(gp), g1 = ldg4(gp + 1), g2 = ldg4(gp + 2), g3 = ldg4(gp + 3);
+    const int node = M.stk[sp - 1];
+    --sp;
+    if (lane == 0) cnt.nodes++;
+    const WideNode& W = S.wide[node];
+    const int child = __ldg(&W.child[lane]);
+    float tn, tf;
+    box_t(__ldg(&W.lox[lane]), __ldg(&W.loy[lane]), __ldg(&W.loz[lane]), __ldg(&W.hix[lane]),
+          __ldg(&W.hiy[lane]), __ldg(&W.hiz[lane]), R.inv, R.oinv, tn, tf);
+    const bool hit = child != kWideEmpty && tn <= tf && tf >= lo_s && tn <= hi_s &&
+                     tn <= te_lim + slack;
+    bool cand = false;
+    unsigned long long ck = ~0ull;
+    uint32_t cp = 0;
+    if (hit && child < 0) {
+      cp = (uint32_t)(~child);
+      const float4* gp = S.geom + 4 * (size_t)cp;
+      const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2), g3 = __ldg(gp + 3);
       PairGeom pg;
-      if (!isect_exact(g0, g1, g2, g3, o, d, pg)) continue;
-      if (!(pg.tx >= seg_lo && pg.te <= seg_hi)) continue;
-      const uint64_t key = ((uint64_t)fkey(pg.te) << 32) | (uint32_t)__float_as_int(g3.z);
-      if (key <= cursor) continue;
-      if (nb == kmax && key >= hk[kmax - 1]) continue;
-      int i = nb < kmax ? nb++ : kmax - 1;
-      while (i > 0 && hk[i - 1] > key) {
-        hk[i] = hk[i - 1];
-        hp[i] = hp[i - 1];
-        --i;
+      if (isect_exact(g0, g1, g2, g3, R.o, R.d, pg) && pg.tx >= seg_lo && pg.te <= seg_hi) {
+        ck = ((unsigned long long)fkey(pg.te) << 32) | (uint32_t)__float_as_int(g3.z);
+        cand = ck > cursor && ck < kth;
       }
-      hk[i] = key;
-      hp[i] = (uint32_t)p;
-      if (nb == kmax) te_lim = fkey_inv((uint32_t)(hk[kmax - 1] >> 32));
     }
+    // internal children: push sorted so that the nearest is on top
+    const unsigned im = __ballot_sync(kFull, hit && child >= 0);
+    if (im) {
+      int rank = 0;
+      unsigned mm = im;
+      while (mm) {
+        const int b = __ffs(mm) - 1;
+        mm &= mm - 1;
+        const float tb = __shfl_sync(kFull, tn, b);
+        rank += (tb > tn) || (tb == tn && b < (int)lane);
+      }
+      const int np = __popc(im);
+      __syncwarp();
+      if (sp + np <= kStk) {
+        if (hit && child >= 0) M.stk[sp + rank] = child;
+        sp += np;
+      } else if (lane == 0) {
+        cnt.stackov++;
+      }
+      __syncwarp();
+    }
+    // leaf candidates: rank-merge into the per-lane sorted k-buffer
+    const unsigned cm = __ballot_sync(kFull, cand);
+    if (cm) {
+      int crank = 0, shift = 0, krank = 0;
+      unsigned mm = cm;
+      while (mm) {
+        const int b = __ffs(mm) - 1;
+        mm &= mm - 1;
+        const unsigned long long kb = shfl64(ck, b);
+        crank += (cand && kb < ck) ? 1 : 0;
+        shift += (kb < key) ? 1 : 0;
+        const unsigned ltm = __ballot_sync(kFull, key < kb);
+        if ((int)lane == b) krank = __popc(ltm);
+      }
+      const int newk = (int)lane + shift, newc = krank + crank;
+      if ((int)lane < nk && newk < kmax) { M.kscr[newk] = key; M.pscr[newk] = pos; }
+      if (cand && newc < kmax) { M.kscr[newc] = ck; M.pscr[newc] = cp; }
+      __syncwarp();
+      nk = min(kmax, nk + __popc(cm));
+      key = ((int)lane < nk) ? M.kscr[lane] : ~0ull;
+      pos = ((int)lane < nk) ? M.pscr[lane] : 0u;
+      __syncwarp();
+      if (nk == kmax) {
+        kth = shfl64(key, kmax - 1);
+        te_lim = fkey_inv((uint32_t)(kth >> 32));
+      }
+    }
+    (void)lt_mask;
   }
-  return nb;
+  return nk;
 }
 
 __device__ __forceinline__ float3 pair_color(const SceneView& S, int pos, const float3& d) {
@@ -169,33 +232,35 @@ __device__ __forceinline__ float3 pair_color(const SceneView& S, int pos, const 
   return make_float3(r, g, b);
 }
 
-// Per-(ray, Gaussian) set-up: exact interval, exponent polynomial of the
-// weight w(tau) = sigma~ exp(-|u + tau d_l|^2 / 2) = 2^(c0 + tau (c1 + c2 tau)),
-// tau = t - t_mid, with u = M x' from the compensated offset x' (value path).
-__device__ void setup_pair(const SceneView& S, const float3& o, const float3& d, uint64_t key,
-                           uint32_t pos, Entry& E) {
+// Per-(ray, Gaussian) set-up into slot `sl`: exact interval and the exponent
+// polynomial of w(tau) = sigma~ exp(-|u + tau d_l|^2 / 2) = 2^(c0 + tau (c1 + c2 tau)),
+// tau = t - t_mid, u = M x' from the compensated offset x' (value path).
+__device__ void setup_pair(const SceneView& S, WarpMem& M, int sl, const Ray& R,
+                           unsigned long long key, uint32_t pos) {
   const float4* gp = S.geom + 4 * (size_t)pos;
-  const float4 g0 = ldg4(gp), g1 = ldg4(gp + 1), g2 = ldg4(gp + 2), g3 = ldg4(gp + 3);
+  const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2), g3 = __ldg(gp + 3);
   PairGeom pg;
-  isect_exact(g0, g1, g2, g3, o, d, pg);
-  const float x0 = offset_at(o.x, g0.x, pg.tm, d.x);
-  const float x1 = offset_at(o.y, g0.y, pg.tm, d.y);
-  const float x2 = offset_at(o.z, g0.z, pg.tm, d.z);
+  isect_exact(g0, g1, g2, g3, R.o, R.d, pg);
+  const float x0 = offset_at(R.o.x, g0.x, pg.tm, R.d.x);
+  const float x1 = offset_at(R.o.y, g0.y, pg.tm, R.d.y);
+  const float x2 = offset_at(R.o.z, g0.z, pg.tm, R.d.z);
   const float u0 = g1.x * x0 + g1.y * x1 + g1.z * x2;
   const float u1 = g1.w * x0 + g2.x * x1 + g2.y * x2;
   const float u2 = g2.z * x0 + g2.w * x1 + g3.x * x2;
   const float qm = u0 * u0 + u1 * u1 + u2 * u2;
   const float b1 = u0 * pg.dl0 + u1 * pg.dl1 + u2 * pg.dl2;
-  E.te = pg.te;
-  E.tx = pg.tx;
-  E.tm = pg.tm;
-  E.c0 = lg2_approx(g0.w) - 0.5f * kLog2e * qm;
-  E.c1 = -kLog2e * b1;
-  E.c2 = -0.5f * kLog2e * pg.A;
-  const float3 col = pair_color(S, (int)pos, d);
-  E.cr = col.x; E.cg = col.y; E.cb = col.z;
-  E.pos = (int)pos;
-  E.idx = (uint32_t)(key & 0xFFFFFFFFu);
+  const float3 col = pair_color(S, (int)pos, R.d);
+  M.te[sl] = pg.te;
+  M.tx[sl] = pg.tx;
+  M.tm[sl] = pg.tm;
+  M.c0[sl] = lg2_approx(g0.w) - 0.5f * kLog2e * qm;
+  M.c1[sl] = -kLog2e * b1;
+  M.c2[sl] = -0.5f * kLog2e * pg.A;
+  M.cr[sl] = col.x;
+  M.cg[sl] = col.y;
+  M.cb[sl] = col.z;
+  M.pos[sl] = (int)pos;
+  M.idx[sl] = (uint32_t)(key & 0xFFFFFFFFu);
 }
 
 // 1 - exp(-x) without cancellation for small x
@@ -204,125 +269,144 @@ __device__ __forceinline__ float alpha_of(float x, float e) {
   return 1.0f - e;
 }
 
-struct Group {
-  float tk[kGroup];
-  bool val[kGroup];
-  float sg[kGroup], sr[kGroup], sgg[kGroup], sb[kGroup];
+struct Lanes {   // lane -> (entry subset, sample) mapping for one sample group
+  int GW, ER, j, esub;
 };
 
-__device__ __forceinline__ void accum_entry(const Entry& E, Group& G, Counters& cnt) {
-#pragma unroll
-  for (int j = 0; j < kGroup; ++j) {
-    if (G.val[j] && E.te <= G.tk[j] && G.tk[j] <= E.tx) {
-      const float tau = G.tk[j] - E.tm;
-      const float w = ex2_approx(fmaf(tau, fmaf(E.c2, tau, E.c1), E.c0));
-      G.sg[j] += w;
-      G.sr[j] = fmaf(w, E.cr, G.sr[j]);
-      G.sgg[j] = fmaf(w, E.cg, G.sgg[j]);
-      G.sb[j] = fmaf(w, E.cb, G.sb[j]);
-      cnt.evals++;
+// sigma and sigma*c at this lane's sample from slots [e0, e1)
+__device__ __forceinline__ void eval_range(const WarpMem& M, int e0, int e1, const Lanes& L, float tk,
+                                           bool val, float& s, float& r, float& g, float& b,
+                                           uint32_t& evals) {
+  for (int e = e0 + L.esub; e < e1; e += L.ER) {
+    const float te = M.te[e], tx = M.tx[e];
+    if (val && te <= tk && tk <= tx) {
+      const float tau = tk - M.tm[e];
+      const float w = ex2_approx(fmaf(tau, fmaf(M.c2[e], tau, M.c1[e]), M.c0[e]));
+      s += w;
+      r = fmaf(w, M.cr[e], r);
+      g = fmaf(w, M.cg[e], g);
+      b = fmaf(w, M.cb[e], b);
+      ++evals;
     }
   }
 }
 
-struct BwdGroup {
-  float dls[kGroup], dc0[kGroup], dc1[kGroup], dc2[kGroup], gc[kGroup], inv[kGroup];
+struct SampleGrad {   // per-sample backward quantities (lane j of the group)
+  float dls, dc0, dc1, dc2, gc, inv;
 };
 
-__device__ __forceinline__ void grad_entry(const Entry& E, const Group& G, const BwdGroup& H,
-                                           float* a) {
-#pragma unroll
-  for (int j = 0; j < kGroup; ++j) {
-    if (G.val[j] && G.sg[j] > 0.f && E.te <= G.tk[j] && G.tk[j] <= E.tx) {
-      const float tau = G.tk[j] - E.tm;
-      const float w = ex2_approx(fmaf(tau, fmaf(E.c2, tau, E.c1), E.c0));
-      const float dldw =
-          H.dls[j] + (H.dc0[j] * E.cr + H.dc1[j] * E.cg + H.dc2[j] * E.cb - H.gc[j]) * H.inv[j];
-      const float wd = w * dldw;
-      const float wi = w * H.inv[j];
-      a[0] += wd;
-      a[1] = fmaf(wd, tau, a[1]);
-      a[2] = fmaf(wd * tau, tau, a[2]);
-      a[3] = fmaf(wi, H.dc0[j], a[3]);
-      a[4] = fmaf(wi, H.dc1[j], a[4]);
-      a[5] = fmaf(wi, H.dc2[j], a[5]);
+// accumulate the per-pair moments of slots [e0, e1) for this group's samples
+__device__ __forceinline__ void grad_range(const WarpMem& M, WarpAcc& A, int e0, int e1,
+                                           const Lanes& L, float tk, bool live,
+                                           const SampleGrad& H) {
+  const int rounds = (e1 - e0 + L.ER - 1) / L.ER;
+  for (int r = 0; r < rounds; ++r) {
+    const int e = e0 + L.esub + r * L.ER;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
+    if (e < e1 && live && M.te[e] <= tk && tk <= M.tx[e]) {
+      const float tau = tk - M.tm[e];
+      const float w = ex2_approx(fmaf(tau, fmaf(M.c2[e], tau, M.c1[e]), M.c0[e]));
+      const float dldw = H.dls + (H.dc0 * M.cr[e] + H.dc1 * M.cg[e] + H.dc2 * M.cb[e] - H.gc) * H.inv;
+      const float wd = w * dldw, wi = w * H.inv;
+      a0 = wd;
+      a1 = wd * tau;
+      a2 = wd * tau * tau;
+      a3 = wi * H.dc0;
+      a4 = wi * H.dc1;
+      a5 = wi * H.dc2;
+    }
+    for (int off = 1; off < L.GW; off <<= 1) {
+      a0 += __shfl_xor_sync(kFull, a0, off);
+      a1 += __shfl_xor_sync(kFull, a1, off);
+      a2 += __shfl_xor_sync(kFull, a2, off);
+      a3 += __shfl_xor_sync(kFull, a3, off);
+      a4 += __shfl_xor_sync(kFull, a4, off);
+      a5 += __shfl_xor_sync(kFull, a5, off);
+    }
+    if (L.j == 0 && e < e1) {
+      A.a[0][e] += a0; A.a[1][e] += a1; A.a[2][e] += a2;
+      A.a[3][e] += a3; A.a[4][e] += a4; A.a[5][e] += a5;
     }
   }
+  __syncwarp();
 }
 
-// Per-pair gradient scatter into the Morton-ordered buffer:
-//  [0..2] dL/dmu, [3] dL/dsigma~, [4..12] dL/dM, [16..] appearance grads.
-//  With w = sigma~ exp(-|M x|^2/2), x = x' + tau d, u = M x', d_l = M d and
-//  moments Sw = sum w dL/dw, Sw1 = sum w dL/dw tau, Sw2 = sum w dL/dw tau^2:
-//    dL/dmu = M^T (Sw u + Sw1 d_l)
-//    dL/dM  = -(Sw u x'^T + Sw1 (u d^T + d_l x'^T) + Sw2 d_l d^T)
-//    dL/dsigma~ = Sw / sigma~
-__device__ void scatter_pair(const SceneView& S, const Entry& E, const float* a, const float3& o,
-                             const float3& d, float* gbuf, int gstride) {
-  if (a[0] == 0.f && a[1] == 0.f && a[2] == 0.f && a[3] == 0.f && a[4] == 0.f && a[5] == 0.f)
-    return;
-  const float4* gp = S.geom + 4 * (size_t)E.pos;
-  const float4 g0 = ldg4(gp), g1 = ldg4(gp + 1), g2 = ldg4(gp + 2), g3 = ldg4(gp + 3);
-  const float M[9] = {g1.x, g1.y, g1.z, g1.w, g2.x, g2.y, g2.z, g2.w, g3.x};
-  const float xp[3] = {offset_at(o.x, g0.x, E.tm, d.x), offset_at(o.y, g0.y, E.tm, d.y),
-                       offset_at(o.z, g0.z, E.tm, d.z)};
-  const float dv[3] = {d.x, d.y, d.z};
-  float u[3], dl[3];
+// Warp-cooperative gradient scatter of slot `e` (lane c writes float4 chunk c):
+//  chunk 0 = (dL/dmu, dL/dsigma~), chunks 1-3 = dL/dM (9 + pad), chunks 4.. = appearance.
+//  With x = x' + tau d, u = M x', d_l = M d and Sw = sum w dL/dw, Sw1 = sum w dL/dw tau,
+//  Sw2 = sum w dL/dw tau^2:  dL/dmu = M^T (Sw u + Sw1 d_l),
+//  dL/dM = -(Sw u x'^T + Sw1 (u d^T + d_l x'^T) + Sw2 d_l d^T),  dL/dsigma~ = Sw / sigma~.
+__device__ void scatter_slot(const SceneView& S, const WarpMem& M, const WarpAcc& A, int e,
+                             const Ray& R, float* gbuf, int gstride) {
+  const float Sw = A.a[0][e], Sw1 = A.a[1][e], Sw2 = A.a[2][e];
+  const float d0 = A.a[3][e], d1 = A.a[4][e], d2 = A.a[5][e];
+  if (Sw == 0.f && Sw1 == 0.f && Sw2 == 0.f && d0 == 0.f && d1 == 0.f && d2 == 0.f) return;
+  const int c = (int)lane_id();
+  const int pos = M.pos[e];
+  const int nchunks = 4 + S.app_stride / 4;
+  float v[4] = {0.f, 0.f, 0.f, 0.f};
+  if (c < 4) {
+    const float4* gp = S.geom + 4 * (size_t)pos;
+    const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2), g3 = __ldg(gp + 3);
+    const float Mm[9] = {g1.x, g1.y, g1.z, g1.w, g2.x, g2.y, g2.z, g2.w, g3.x};
+    const float tm = M.tm[e];
+    const float xp[3] = {offset_at(R.o.x, g0.x, tm, R.d.x), offset_at(R.o.y, g0.y, tm, R.d.y),
+                         offset_at(R.o.z, g0.z, tm, R.d.z)};
+    const float dv[3] = {R.d.x, R.d.y, R.d.z};
+    float u[3], dl[3];
 #pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    u[r] = M[3 * r] * xp[0] + M[3 * r + 1] * xp[1] + M[3 * r + 2] * xp[2];
-    dl[r] = M[3 * r] * dv[0] + M[3 * r + 1] * dv[1] + M[3 * r + 2] * dv[2];
-  }
-  const float Sw = a[0], Sw1 = a[1], Sw2 = a[2];
-  float* row = gbuf + (size_t)E.pos * gstride;
-  float gm[3];
-#pragma unroll
-  for (int b = 0; b < 3; ++b) {
-    gm[b] = 0.f;
-#pragma unroll
-    for (int r = 0; r < 3; ++r) gm[b] += M[3 * r + b] * (Sw * u[r] + Sw1 * dl[r]);
-  }
-  float dM[9];
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-#pragma unroll
-    for (int b = 0; b < 3; ++b)
-      dM[3 * r + b] = -(Sw * u[r] * xp[b] + Sw1 * (u[r] * dv[b] + dl[r] * xp[b]) +
-                        Sw2 * dl[r] * dv[b]);
-  float4* r4 = reinterpret_cast<float4*>(row);
-  atomicAdd(r4 + 0, make_float4(gm[0], gm[1], gm[2], Sw / g0.w));
-  atomicAdd(r4 + 1, make_float4(dM[0], dM[1], dM[2], dM[3]));
-  atomicAdd(r4 + 2, make_float4(dM[4], dM[5], dM[6], dM[7]));
-  atomicAdd(r4 + 3, make_float4(dM[8], 0.f, 0.f, 0.f));
-  // appearance
-  float Y[16];
-  sh_basis(S.deg, d.x, d.y, d.z, Y);
-  const int nc = (S.deg + 1) * (S.deg + 1);
-  float v[kMaxApp + 3];
-#pragma unroll
-  for (int m = 0; m < 16; ++m)
-    if (m < nc) {
-      v[3 * m] = a[3] * Y[m];
-      v[3 * m + 1] = a[4] * Y[m];
-      v[3 * m + 2] = a[5] * Y[m];
+    for (int r = 0; r < 3; ++r) {
+      u[r] = Mm[3 * r] * xp[0] + Mm[3 * r + 1] * xp[1] + Mm[3 * r + 2] * xp[2];
+      dl[r] = Mm[3 * r] * dv[0] + Mm[3 * r + 1] * dv[1] + Mm[3 * r + 2] * dv[2];
     }
-  const float* ap = S.app + (size_t)E.pos * S.app_stride + 3 * nc;
-  for (int j = 0; j < S.lobes; ++j) {
-    const float* q = ap + 7 * j;
-    const float k0 = __ldg(q), k1 = __ldg(q + 1), k2 = __ldg(q + 2), lam = __ldg(q + 3);
-    const float dp = d.x * __ldg(q + 4) + d.y * __ldg(q + 5) + d.z * __ldg(q + 6);
-    const float e = ex2_approx(lam * (dp - 1.0f) * kLog2e);
-    const float kd = (a[3] * k0 + a[4] * k1 + a[5] * k2) * e;
-    float* dst = v + 3 * nc + 7 * j;
-    dst[0] = a[3] * e; dst[1] = a[4] * e; dst[2] = a[5] * e;
-    dst[3] = kd * (dp - 1.0f);
-    dst[4] = kd * lam * d.x; dst[5] = kd * lam * d.y; dst[6] = kd * lam * d.z;
+    float out[16];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      float acc = 0.f;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) acc += Mm[3 * r + b] * (Sw * u[r] + Sw1 * dl[r]);
+      out[b] = acc;
+    }
+    out[3] = Sw / g0.w;
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        out[4 + 3 * r + b] = -(Sw * u[r] * xp[b] + Sw1 * (u[r] * dv[b] + dl[r] * xp[b]) +
+                               Sw2 * dl[r] * dv[b]);
+    out[13] = out[14] = out[15] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = out[4 * c + k];
+  } else if (c < nchunks) {
+    const int nc = (S.deg + 1) * (S.deg + 1);
+    const float dc[3] = {d0, d1, d2};
+    const float* ap = S.app + (size_t)pos * S.app_stride + 3 * nc;
+    int lobe_cached = -1;
+    float e_j = 0.f, kd = 0.f, dp = 0.f, lam = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int f = 4 * (c - 4) + k;
+      if (f < 3 * nc) {
+        v[k] = dc[f % 3] * M.Y[f / 3];
+      } else if (f < 3 * nc + 7 * S.lobes) {
+        const int j = (f - 3 * nc) / 7, rr = (f - 3 * nc) % 7;
+        if (j != lobe_cached) {
+          const float* q = ap + 7 * j;
+          lam = __ldg(q + 3);
+          dp = R.d.x * __ldg(q + 4) + R.d.y * __ldg(q + 5) + R.d.z * __ldg(q + 6);
+          e_j = ex2_approx(lam * (dp - 1.0f) * kLog2e);
+          kd = (d0 * __ldg(q) + d1 * __ldg(q + 1) + d2 * __ldg(q + 2)) * e_j;
+          lobe_cached = j;
+        }
+        if (rr < 3) v[k] = dc[rr] * e_j;
+        else if (rr == 3) v[k] = kd * (dp - 1.0f);
+        else v[k] = kd * lam * (rr == 4 ? R.d.x : (rr == 5 ? R.d.y : R.d.z));
+      }
+    }
   }
-  const int nv = 3 * nc + 7 * S.lobes;
-  for (int k = nv; k < S.app_stride; ++k) v[k] = 0.f;
-  float4* a4 = r4 + 4;
-  for (int k = 0; k < S.app_stride / 4; ++k)
-    atomicAdd(a4 + k, make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
+  if (c < nchunks)
+    atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + c,
+              make_float4(v[0], v[1], v[2], v[3]));
 }
 
 __device__ __forceinline__ int skip_to(float te, int s, int B, float dt, float t0, float t1) {
@@ -334,40 +418,52 @@ __device__ __forceinline__ int skip_to(float te, int s, int B, float dt, float t
 }
 
 __device__ __forceinline__ void flush_stats(rg_stats* st, const Counters& c, bool hit) {
-  const unsigned m = __activemask();
-  const unsigned lane = threadIdx.x & 31;
-  const unsigned leader = __ffs(m) - 1;
-  const uint32_t v[10] = {1u, hit ? 1u : 0u, c.slabs, c.pairs, c.evals, c.samples, c.overflows,
-                          c.fetches, c.nodes, c.stackov};
+  const unsigned lane = lane_id();
+  const uint32_t v[10] = {lane == 0 ? 1u : 0u, (lane == 0 && hit) ? 1u : 0u, c.slabs, c.pairs,
+                          c.evals, c.samples, c.overflows, c.fetches, c.nodes, c.stackov};
   unsigned long long* dst = reinterpret_cast<unsigned long long*>(st);
 #pragma unroll
   for (int k = 0; k < 10; ++k) {
-    const uint32_t s = __reduce_add_sync(m, v[k]);
-    if (lane == leader && s) atomicAdd(dst + k, (unsigned long long)s);
+    const uint32_t s = __reduce_add_sync(kFull, v[k]);
+    if (lane == 0 && s) atomicAdd(dst + k, (unsigned long long)s);
   }
 }
 
+// Kahan accumulation
+__device__ __forceinline__ void kadd(float& s, float& comp, float x) {
+  const float y = x - comp;
+  const float t = s + y;
+  comp = (t - s) - y;
+  s = t;
+}
+
 template <bool BWD>
-__global__ void __launch_bounds__(kBlock) k_render(const RenderArgs P) {
+__global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const unsigned lane = lane_id();
+  const int wid = threadIdx.x >> 5;
+  WarpMem& M = reinterpret_cast<WarpMem*>(smem_raw)[wid];
+  WarpAcc& A = reinterpret_cast<WarpAcc*>(smem_raw + sizeof(WarpMem) * kWarps)[BWD ? wid : 0];
   int ray;
-  float3 o, d;
+  Ray R;
   if (P.cam_mode) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int px = blockIdx.x * 16 + (w & 1) * 8 + (lane & 7);
-    const int py = blockIdx.y * 8 + (w >> 1) * 4 + (lane >> 3);
+    const int tile = blockIdx.x;
+    const int px = 2 * (tile % P.tiles_x) + (wid & 1);
+    const int py = 2 * (tile / P.tiles_x) + (wid >> 1);
     if (px >= P.rw || py >= P.rh) return;
     ray = py * P.rw + px;
-    camera_ray(P.cam, P.cam.x0 + px, P.cam.y0 + py, o, d);
+    camera_ray(P.cam, P.cam.x0 + px, P.cam.y0 + py, R.o, R.d);
   } else {
-    ray = blockIdx.x * kBlock + threadIdx.x;
+    ray = blockIdx.x * kWarps + wid;
     if (ray >= P.n_rays) return;
-    o = make_float3(P.ro[3 * ray], P.ro[3 * ray + 1], P.ro[3 * ray + 2]);
-    d = make_float3(P.rd[3 * ray], P.rd[3 * ray + 1], P.rd[3 * ray + 2]);
+    R.o = make_float3(P.ro[3 * ray], P.ro[3 * ray + 1], P.ro[3 * ray + 2]);
+    R.d = make_float3(P.rd[3 * ray], P.rd[3 * ray + 1], P.rd[3 * ray + 2]);
   }
   const rg_config& c = P.c;
   const int B = c.slab_samples;
   const int K = c.hit_capacity;
-  float C0 = 0.f, C1 = 0.f, C2 = 0.f, T = 1.f;
+  float C0 = 0.f, C1 = 0.f, C2 = 0.f, k0c = 0.f, k1c = 0.f, k2c = 0.f;
+  float tau = 0.f, tauc = 0.f, T = 1.f;
   int replay = -1;
   Counters cnt = {};
   const bool dbg = (!BWD) && P.dbg_rec != nullptr && ray < P.dbg_rays;
@@ -379,17 +475,31 @@ __global__ void __launch_bounds__(kBlock) k_render(const RenderArgs P) {
     Pp0 = P.rgb_in[3 * ray]; Pp1 = P.rgb_in[3 * ray + 1]; Pp2 = P.rgb_in[3 * ray + 2];
     replay_in = P.replay_in[ray];
   }
-  float t0, t1;
-  const bool hit = P.S.n > 0 && clip_exact(P.S.root_box, o, d, c.t_near, t0, t1);
+  float t0 = 0.f, t1 = 0.f;
+  const bool hit = P.S.n > 0 && clip_exact(P.S.root_box, R.o, R.d, c.t_near, t0, t1);
   if (hit && !(BWD && gr0 == 0.f && gr1 == 0.f && gr2 == 0.f)) {
-    const float3 inv = make_float3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
-    const float3 oinv = make_float3(o.x * inv.x, o.y * inv.y, o.z * inv.z);
-    Entry act[kACap];
-    float acc[BWD ? kACap : 1][6];
-    uint64_t hk[kACap];
-    uint32_t hp[kACap];
+    R.inv = make_float3(1.0f / R.d.x, 1.0f / R.d.y, 1.0f / R.d.z);
+    R.oinv = make_float3(R.o.x * R.inv.x, R.o.y * R.inv.y, R.o.z * R.inv.z);
+    if (BWD) {
+      float Y[16];
+      sh_basis(P.S.deg, R.d.x, R.d.y, R.d.z, Y);
+      if (lane < 16) {
+#pragma unroll
+        for (int m = 0; m < 16; ++m)
+          if ((int)lane == m) M.Y[m] = Y[m];
+      }
+      __syncwarp();
+    }
+    // lane mapping for sample groups
+    Lanes L;
+    L.GW = B >= 8 ? 8 : (B >= 4 ? 4 : (B >= 2 ? 2 : 1));
+    if (B == 3) L.GW = 4;
+    if (B > 4 && B < 8) L.GW = 8;
+    L.ER = 32 / L.GW;
+    L.j = (int)lane % L.GW;
+    L.esub = (int)lane / L.GW;
     int count = 0;
-    uint64_t cursor = 0;
+    unsigned long long cursor = 0;
     bool exhausted = false;
     int s = 0;
     while (true) {
@@ -397,143 +507,212 @@ __global__ void __launch_bounds__(kBlock) k_render(const RenderArgs P) {
       if (!(sample_t(k0, c.dt, t0) < t1)) break;
       const float tlo = fma_((float)k0, c.dt, t0);
       const float thi = fminf(t1, fma_((float)(k0 + B), c.dt, t0));
-      // expire Gaussians whose support ended before this slab
-      int wr = 0;
-      for (int e = 0; e < count; ++e) {
-        if (act[e].tx >= tlo) {
-          if (wr != e) {
-            act[wr] = act[e];
-            if (BWD)
-              for (int k = 0; k < 6; ++k) acc[wr][k] = acc[e][k];
+      // ---- expire Gaussians whose support ended before this slab
+      {
+        int nc = 0;
+        for (int base = 0; base < count; base += 32) {
+          const int e = base + (int)lane;
+          const bool valid = e < count;
+          const bool keep = valid && M.tx[e] >= tlo;
+          if (BWD) {
+            unsigned xm = __ballot_sync(kFull, valid && !keep);
+            while (xm) {
+              const int b = __ffs(xm) - 1;
+              xm &= xm - 1;
+              scatter_slot(P.S, M, A, base + b, R, P.gbuf, P.gstride);
+            }
           }
-          ++wr;
-        } else if (BWD) {
-          scatter_pair(P.S, act[e], acc[e], o, d, P.gbuf, P.gstride);
+          float f[9];
+          int ps = 0;
+          uint32_t ix = 0;
+          float ac[6];
+          if (keep) {
+            f[0] = M.te[e]; f[1] = M.tx[e]; f[2] = M.tm[e]; f[3] = M.c0[e]; f[4] = M.c1[e];
+            f[5] = M.c2[e]; f[6] = M.cr[e]; f[7] = M.cg[e]; f[8] = M.cb[e];
+            ps = M.pos[e]; ix = M.idx[e];
+            if (BWD)
+              for (int k = 0; k < 6; ++k) ac[k] = A.a[k][e];
+          }
+          const unsigned km = __ballot_sync(kFull, keep);
+          const int dst = nc + __popc(km & ((1u << lane) - 1u));
+          __syncwarp();
+          if (keep) {
+            M.te[dst] = f[0]; M.tx[dst] = f[1]; M.tm[dst] = f[2]; M.c0[dst] = f[3];
+            M.c1[dst] = f[4]; M.c2[dst] = f[5]; M.cr[dst] = f[6]; M.cg[dst] = f[7];
+            M.cb[dst] = f[8]; M.pos[dst] = ps; M.idx[dst] = ix;
+            if (BWD)
+              for (int k = 0; k < 6; ++k) A.a[k][dst] = ac[k];
+          }
+          nc += __popc(km);
+          __syncwarp();
         }
+        count = nc;
       }
-      count = wr;
-      // refill in key order until every Gaussian entering by t_hi is held
-      while (!exhausted && count < kACap && (count == 0 || act[count - 1].te <= thi)) {
-        const int want = kACap - count;
-        const int got = fetch(P.S, o, d, inv, oinv, tlo, t1, cursor, want, hk, hp, cnt);
-        for (int i = 0; i < got; ++i) {
-          setup_pair(P.S, o, d, hk[i], hp[i], act[count]);
+      // ---- refill in key order until every Gaussian entering by t_hi is held
+      while (!exhausted && count < kA && (count == 0 || M.te[count - 1] <= thi)) {
+        const int want = min(32, kA - count);
+        unsigned long long key;
+        uint32_t pos;
+        const int got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
+        if ((int)lane < got) {
+          setup_pair(P.S, M, count + (int)lane, R, key, pos);
           if (BWD)
-            for (int k = 0; k < 6; ++k) acc[count][k] = 0.f;
-          ++count;
+            for (int k = 0; k < 6; ++k) A.a[k][count + lane] = 0.f;
         }
-        cnt.pairs += got;
-        if (got > 0) cursor = hk[got - 1];
+        if (lane == 0) cnt.pairs += got;
+        if (got > 0) cursor = shfl64(key, got - 1);
+        count += got;
         if (got < want) exhausted = true;
+        __syncwarp();
       }
       if (count == 0) break;
-      if (act[0].te > thi) {   // empty slab(s): jump to the slab holding the next entry
-        s = skip_to(act[0].te, s, B, c.dt, t0, t1);
+      if (M.te[0] > thi) {   // empty slab(s): jump to the slab holding the next entry
+        s = skip_to(M.te[0], s, B, c.dt, t0, t1);
         continue;
       }
       int n_in = 0;
-      while (n_in < count && act[n_in].te <= thi) ++n_in;
-      const int n_use = min(n_in, K);
-      const bool more = (n_in == kACap) && !exhausted && (K > kACap);
-      if (n_in > K) {
-        cnt.overflows++;
-      } else if (!BWD && n_in == K && n_in == kACap && !exhausted &&
-                 fetch(P.S, o, d, inv, oinv, tlo, thi, cursor, 1, hk, hp, cnt) > 0) {
-        cnt.overflows++;   // exactly K held, at least one more member beyond the cursor
+      for (int base = 0; base < count; base += 32) {
+        const int e = base + (int)lane;
+        const unsigned m = __ballot_sync(kFull, e < count && M.te[e] <= thi);
+        n_in += __popc(m);
+        if (m != kFull) break;
       }
-      if (dbg)
-        for (int e = 0; e < n_use; ++e)
-          if (dbg_n < P.dbg_cap) {
-            int32_t* r = P.dbg_rec + 2 * ((size_t)ray * P.dbg_cap + dbg_n++);
+      const int n_use = min(n_in, K);
+      const bool more = (n_in == kA) && !exhausted && (K > kA);
+      if (n_in > K) {
+        if (lane == 0) cnt.overflows++;
+      } else if (!BWD && n_in == K && n_in == kA && !exhausted) {
+        unsigned long long pk;
+        uint32_t pp;
+        if (fetch(P.S, M, R, tlo, thi, cursor, 1, pk, pp, cnt) > 0 && lane == 0) cnt.overflows++;
+      }
+      if (dbg) {
+        for (int e = (int)lane; e < n_use; e += 32)
+          if (dbg_n + e < P.dbg_cap) {
+            int32_t* r = P.dbg_rec + 2 * ((size_t)ray * P.dbg_cap + dbg_n + e);
             r[0] = s;
-            r[1] = (int32_t)act[e].idx;
+            r[1] = (int32_t)M.idx[e];
           }
-      for (int g0 = 0; g0 < B; g0 += kGroup) {
-        Group G;
-#pragma unroll
-        for (int j = 0; j < kGroup; ++j) {
-          G.tk[j] = sample_t(k0 + g0 + j, c.dt, t0);
-          G.val[j] = (g0 + j < B) && (G.tk[j] < t1);
-          G.sg[j] = G.sr[j] = G.sgg[j] = G.sb[j] = 0.f;
-        }
-        for (int e = 0; e < n_use; ++e) accum_entry(act[e], G, cnt);
+        dbg_n = min(P.dbg_cap, dbg_n + n_use);
+      }
+      for (int g0 = 0; g0 < B; g0 += L.GW) {
+        const float tk = sample_t(k0 + g0 + L.j, c.dt, t0);
+        const bool val = (g0 + L.j < B) && (tk < t1);
+        float sg = 0.f, sr = 0.f, sgg = 0.f, sb = 0.f;
+        uint32_t ev = 0;
+        eval_range(M, 0, n_use, L, tk, val, sg, sr, sgg, sb, ev);
         if (more) {   // slab set larger than the active list: stream the rest
-          uint64_t cur2 = cursor;
+          unsigned long long cur2 = cursor;
           int remaining = K - n_use;
           bool full_last = true;
           while (remaining > 0) {
-            const int want = min(kACap, remaining);
-            const int got = fetch(P.S, o, d, inv, oinv, tlo, thi, cur2, want, hk, hp, cnt);
-            for (int i = 0; i < got; ++i) {
-              Entry E;
-              setup_pair(P.S, o, d, hk[i], hp[i], E);
-              accum_entry(E, G, cnt);
-              if (dbg && g0 == 0 && dbg_n < P.dbg_cap) {
-                int32_t* r = P.dbg_rec + 2 * ((size_t)ray * P.dbg_cap + dbg_n++);
+            const int want = min(32, remaining);
+            unsigned long long key;
+            uint32_t pos;
+            const int got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
+            if ((int)lane < got) setup_pair(P.S, M, kA + (int)lane, R, key, pos);
+            __syncwarp();
+            eval_range(M, kA, kA + got, L, tk, val, sg, sr, sgg, sb, ev);
+            if (dbg && g0 == 0) {
+              if ((int)lane < got && dbg_n + (int)lane < P.dbg_cap) {
+                int32_t* r = P.dbg_rec + 2 * ((size_t)ray * P.dbg_cap + dbg_n + lane);
                 r[0] = s;
-                r[1] = (int32_t)E.idx;
+                r[1] = (int32_t)M.idx[kA + lane];
               }
+              dbg_n = min(P.dbg_cap, dbg_n + got);
             }
-            if (g0 == 0) cnt.pairs += got;
+            if (g0 == 0 && lane == 0) cnt.pairs += got;
             remaining -= got;
-            if (got > 0) cur2 = hk[got - 1];
+            if (got > 0) cur2 = shfl64(key, got - 1);
+            __syncwarp();
             if (got < want) { full_last = false; break; }
           }
-          if (g0 == 0 && remaining == 0 && full_last &&
-              fetch(P.S, o, d, inv, oinv, tlo, thi, cur2, 1, hk, hp, cnt) > 0)
-            cnt.overflows++;
-        }
-        // composite front to back (Eq. 4)
-        BwdGroup H;
-#pragma unroll
-        for (int j = 0; j < kGroup; ++j) {
-          if (BWD) { H.dls[j] = H.dc0[j] = H.dc1[j] = H.dc2[j] = H.gc[j] = H.inv[j] = 0.f; }
-          if (G.val[j] && G.sg[j] > 0.f) {
-            const float inv_s = 1.0f / G.sg[j];
-            const float cr = G.sr[j] * inv_s, cg = G.sgg[j] * inv_s, cb = G.sb[j] * inv_s;
-            const float x = G.sg[j] * c.dt;
-            const float e = ex2_approx(-x * kLog2e);
-            const float al = alpha_of(x, e);
-            const float ta = T * al;
-            C0 = fmaf(ta, cr, C0);
-            C1 = fmaf(ta, cg, C1);
-            C2 = fmaf(ta, cb, C2);
-            if (BWD) {
-              const float Tn = T * e;
-              H.dc0[j] = gr0 * ta; H.dc1[j] = gr1 * ta; H.dc2[j] = gr2 * ta;
-              const float gcj = gr0 * cr + gr1 * cg + gr2 * cb;
-              const float gS = gr0 * (Pp0 - C0) + gr1 * (Pp1 - C1) + gr2 * (Pp2 - C2);
-              H.dls[j] = c.dt * (Tn * gcj - gS);
-              H.gc[j] = H.dc0[j] * cr + H.dc1[j] * cg + H.dc2[j] * cb;
-              H.inv[j] = inv_s;
-            }
-            T *= e;
-            cnt.samples++;
+          if (g0 == 0 && remaining == 0 && full_last) {
+            unsigned long long pk;
+            uint32_t pp;
+            if (fetch(P.S, M, R, tlo, thi, cur2, 1, pk, pp, cnt) > 0 && lane == 0) cnt.overflows++;
           }
         }
+        cnt.evals += ev;
+        // reduce over the entry subsets: every lane of sample j holds the totals
+        for (int off = L.GW; off < 32; off <<= 1) {
+          sg += __shfl_xor_sync(kFull, sg, off);
+          sr += __shfl_xor_sync(kFull, sr, off);
+          sgg += __shfl_xor_sync(kFull, sgg, off);
+          sb += __shfl_xor_sync(kFull, sb, off);
+        }
+        // ---- composite the group front to back (Eq. 4): segmented scans over GW lanes
+        const bool live = val && sg > 0.f;
+        const float x = live ? sg * c.dt : 0.f;
+        float incl = x;
+        for (int dd = 1; dd < L.GW; dd <<= 1) {
+          const float v = __shfl_up_sync(kFull, incl, dd, L.GW);
+          if (L.j >= dd) incl += v;
+        }
+        const float excl = incl - x;
+        const float Tb = ex2_approx(-(tau + excl) * kLog2e);   // T before this sample
+        const float e_s = ex2_approx(-x * kLog2e);
+        const float al = alpha_of(x, e_s);
+        const float inv_s = live ? 1.0f / sg : 0.f;
+        const float cr = sr * inv_s, cg = sgg * inv_s, cb = sb * inv_s;
+        const float wgt = live ? Tb * al : 0.f;
+        float q0 = wgt * cr, q1 = wgt * cg, q2 = wgt * cb;
+        // inclusive prefix of the contributions (backward needs C after each sample)
+        float p0 = q0, p1 = q1, p2 = q2;
+        for (int dd = 1; dd < L.GW; dd <<= 1) {
+          const float v0 = __shfl_up_sync(kFull, p0, dd, L.GW);
+          const float v1 = __shfl_up_sync(kFull, p1, dd, L.GW);
+          const float v2 = __shfl_up_sync(kFull, p2, dd, L.GW);
+          if (L.j >= dd) { p0 += v0; p1 += v1; p2 += v2; }
+        }
+        SampleGrad H = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (BWD && live) {
+          const float Ta = Tb * e_s;
+          H.dc0 = gr0 * wgt; H.dc1 = gr1 * wgt; H.dc2 = gr2 * wgt;
+          const float gcj = gr0 * cr + gr1 * cg + gr2 * cb;
+          const float gS = gr0 * (Pp0 - (C0 + p0)) + gr1 * (Pp1 - (C1 + p1)) + gr2 * (Pp2 - (C2 + p2));
+          H.dls = c.dt * (Ta * gcj - gS);
+          H.gc = H.dc0 * cr + H.dc1 * cg + H.dc2 * cb;
+          H.inv = inv_s;
+        }
+        const int last = L.GW - 1;
+        const float tot_x = __shfl_sync(kFull, incl, last, L.GW);
+        const float t0c = __shfl_sync(kFull, p0, last, L.GW);
+        const float t1c = __shfl_sync(kFull, p1, last, L.GW);
+        const float t2c = __shfl_sync(kFull, p2, last, L.GW);
+        kadd(tau, tauc, tot_x);
+        kadd(C0, k0c, t0c);
+        kadd(C1, k1c, t1c);
+        kadd(C2, k2c, t2c);
+        T = ex2_approx(-tau * kLog2e);
+        const unsigned smask = __ballot_sync(kFull, live && L.esub == 0);
+        if (lane == 0) cnt.samples += __popc(smask);
         if (BWD) {
-          for (int e = 0; e < n_use; ++e) grad_entry(act[e], G, H, acc[e]);
+          grad_range(M, A, 0, n_use, L, tk, live, H);
           if (more) {
-            uint64_t cur2 = cursor;
+            unsigned long long cur2 = cursor;
             int remaining = K - n_use;
             while (remaining > 0) {
-              const int want = min(kACap, remaining);
-              const int got = fetch(P.S, o, d, inv, oinv, tlo, thi, cur2, want, hk, hp, cnt);
-              for (int i = 0; i < got; ++i) {
-                Entry E;
-                setup_pair(P.S, o, d, hk[i], hp[i], E);
-                float a[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                grad_entry(E, G, H, a);
-                scatter_pair(P.S, E, a, o, d, P.gbuf, P.gstride);
+              const int want = min(32, remaining);
+              unsigned long long key;
+              uint32_t pos;
+              const int got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
+              if ((int)lane < got) {
+                setup_pair(P.S, M, kA + (int)lane, R, key, pos);
+                for (int k = 0; k < 6; ++k) A.a[k][kA + lane] = 0.f;
               }
+              __syncwarp();
+              grad_range(M, A, kA, kA + got, L, tk, live, H);
+              for (int e = kA; e < kA + got; ++e) scatter_slot(P.S, M, A, e, R, P.gbuf, P.gstride);
               remaining -= got;
-              if (got > 0) cur2 = hk[got - 1];
+              if (got > 0) cur2 = shfl64(key, got - 1);
+              __syncwarp();
               if (got < want) break;
             }
           }
         }
       }
-      cnt.slabs++;
+      if (lane == 0) cnt.slabs++;
       if (BWD) {
         if (s == replay_in) break;
       } else if (T <= c.t_eps) {
@@ -543,9 +722,9 @@ __global__ void __launch_bounds__(kBlock) k_render(const RenderArgs P) {
       ++s;
     }
     if (BWD)
-      for (int e = 0; e < count; ++e) scatter_pair(P.S, act[e], acc[e], o, d, P.gbuf, P.gstride);
+      for (int e = 0; e < count; ++e) scatter_slot(P.S, M, A, e, R, P.gbuf, P.gstride);
   }
-  if (!BWD) {
+  if (!BWD && lane == 0) {
     P.rgb[3 * ray] = C0 + T * c.background[0];
     P.rgb[3 * ray + 1] = C1 + T * c.background[1];
     P.rgb[3 * ray + 2] = C2 + T * c.background[2];
@@ -640,6 +819,7 @@ SceneView view_of(const rg_bvh& b) {
   S.geom = reinterpret_cast<const float4*>(b.geom);
   S.app = b.app;
   S.nodes = reinterpret_cast<const float4*>(b.nodes);
+  S.wide = reinterpret_cast<const WideNode*>(b.wide);
   S.root_box = b.root_box;
   S.n = b.n;
   S.deg = b.sh_degree;
@@ -655,15 +835,19 @@ void ray_grid(RenderArgs& A, const rg_rays* rays, const rg_camera* cam, dim3& gr
     A.rw = cam->x1 - cam->x0;
     A.rh = cam->y1 - cam->y0;
     A.n_rays = A.rw * A.rh;
-    grid = dim3((A.rw + 15) / 16, (A.rh + 7) / 8);
+    A.tiles_x = (A.rw + 1) / 2;
+    grid = dim3((unsigned)(A.tiles_x * ((A.rh + 1) / 2)));
   } else {
     A.cam_mode = 0;
     A.ro = rays->origin;
     A.rd = rays->dir;
     A.n_rays = rays->n;
-    grid = dim3((rays->n + kBlock - 1) / kBlock);
+    grid = dim3((unsigned)((rays->n + kWarps - 1) / kWarps));
   }
 }
+
+constexpr size_t kSmemFwd = sizeof(WarpMem) * kWarps;
+constexpr size_t kSmemBwd = (sizeof(WarpMem) + sizeof(WarpAcc)) * kWarps;
 
 }  // namespace
 
@@ -687,7 +871,7 @@ cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_conf
   A.rgb = rgb; A.T = T; A.replay = replay; A.stats = stats;
   A.dbg_rays = dbg_rec ? dbg_rays : 0;
   A.dbg_cap = dbg_cap; A.dbg_counts = dbg_counts; A.dbg_rec = dbg_rec;
-  k_render<false><<<grid, kBlock, 0, st>>>(A);
+  k_render<false><<<grid, kBlock, kSmemFwd, st>>>(A);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -707,7 +891,7 @@ cudaError_t launch_backward(const rg_gaussians& g, const rg_bvh& b, const rg_con
   if (b.n > 0) cudaMemsetAsync(gbuf, 0, sizeof(float) * (size_t)gs * b.n, st);
   A.stats = stats;
   A.rgb_in = rgb; A.replay_in = replay; A.d_rgb = d_rgb; A.gbuf = gbuf; A.gstride = gs;
-  if (A.n_rays > 0) { k_render<true><<<grid, kBlock, 0, st>>>(A); count_launches(1); }
+  if (A.n_rays > 0) { k_render<true><<<grid, kBlock, kSmemBwd, st>>>(A); count_launches(1); }
   if (b.n > 0) {
     k_finalize<<<(b.n + 255) / 256, 256, 0, st>>>(gbuf, gs, b.order, g, grads, stats);
     count_launches(1);

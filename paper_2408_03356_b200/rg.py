@@ -58,8 +58,9 @@ class _Camera(C.Structure):
 class _BVH(C.Structure):
     _fields_ = [("n", C.c_int32), ("sh_degree", C.c_int32), ("sg_count", C.c_int32),
                 ("app_stride", C.c_int32)] + [(k, C.c_void_p) for k in
-                                              ("geom", "app", "nodes", "leaf_box", "root_box",
-                                               "codes", "sorted_codes", "order")]
+                                              ("geom", "app", "nodes", "wide", "wide_info",
+                                               "leaf_box", "root_box", "codes", "sorted_codes",
+                                               "order")]
 
 
 EXPORTS = ("rg_status_string", "rg_version", "rg_kernel_launches", "rg_bvh_workspace_bytes", "rg_build_bvh",
@@ -226,7 +227,16 @@ class BVH:
             leaf_box=view(self.h.leaf_box, 6 * n, torch.float32, 4).reshape(-1, 6),
             root_box=view(self.h.root_box, 6, torch.float32, 4),
             geom=view(self.h.geom, 16 * n, torch.float32, 4).reshape(-1, 16),
+            wide_info=view(self.h.wide_info, 4, torch.int32, 4),
         )
+
+    def wide_nodes(self):
+        """[count, 7, 32] view of the 32-wide nodes (6 box planes + child ids)."""
+        info = self.debug_views()["wide_info"].cpu()
+        cnt = int(info[0])
+        base = self.h.wide - self.ws.data_ptr()
+        raw = self.ws.view(torch.uint8)[base:base + cnt * 896]
+        return raw.view(torch.float32).reshape(cnt, 7, 32), raw.view(torch.int32).reshape(cnt, 7, 32)
 
 
 def bvh_workspace(scene: Gaussians):

@@ -67,7 +67,7 @@ def test_struct_sizes_match_header():
     assert C.sizeof(rg._Gaussians) == 16 + 8 * 8
     assert C.sizeof(rg._Config) == 48
     assert C.sizeof(rg._Camera) == 24 + 16 + 48
-    assert C.sizeof(rg._BVH) == 16 + 8 * 8
+    assert C.sizeof(rg._BVH) == 16 + 10 * 8
 
 
 def test_product_package_does_not_import_oracle():

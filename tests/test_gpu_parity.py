@@ -98,6 +98,39 @@ def test_build_bitexact(oracle, kind, n):
             return ref.leaf_boxes[~cid] if cid < 0 else ref.node_boxes[cid]
         lb = np.stack([box(c) for c in ref.left]); rb = np.stack([box(c) for c in ref.right])
         assert np.array_equal(nodes[:, 0:6], lb) and np.array_equal(nodes[:, 6:12], rb)
+    check_wide_tree(b, ref, n)
+
+
+def check_wide_tree(b, ref, n):
+    """32-wide collapse: every leaf exactly once, every wide child box equals
+    the exact union of the leaf boxes below it, no unfinished collapse round."""
+    info = b.debug_views()["wide_info"].cpu().numpy()
+    assert info[3] == 0
+    wf, wi = b.wide_nodes()
+    wf, wi = wf.cpu().numpy(), wi.cpu().numpy()
+    seen = np.zeros(n, int)
+
+    def walk(w):
+        lo = np.full(3, np.inf, np.float32); hi = np.full(3, -np.inf, np.float32)
+        for k in range(32):
+            ch = wi[w, 6, k]
+            if ch == 0x7FFFFFFF:
+                continue
+            cb = wf[w, :6, k]
+            if ch < 0:
+                seen[~ch] += 1
+                sub = ref.leaf_boxes[~ch]
+            else:
+                sub = walk(ch)
+            assert np.array_equal(cb, sub)
+            lo = np.minimum(lo, sub[:3]); hi = np.maximum(hi, sub[3:])
+        return np.concatenate([lo, hi])
+    if n >= 1 and n <= 300_000:
+        import sys
+        sys.setrecursionlimit(10000)
+        root = walk(0)
+        assert np.array_equal(root, ref.root)
+        assert np.all(seen == 1)
 
 
 def test_camera_rays_bitexact(oracle):
