@@ -206,6 +206,7 @@ def run_ours(args):
     fo = dict(rgb=torch.empty(R, 3, device=dev), T=torch.empty(R, device=dev),
               replay=torch.empty(R, dtype=torch.int32, device=dev))
     drgb = torch.empty(R, 3, device=dev)
+    flog = rg.new_log(R, device=dev)
     loss = torch.zeros(1, device=dev)
     # target image: the same view of a seeded perturbation of the scene (setup)
     gp = rg.Gaussians.from_scene(perturbed(sc), device=dev)
@@ -225,7 +226,7 @@ def run_ours(args):
         bvh = rg.build_bvh(g, cfg, ws=bws)
         if marks is not None:
             marks[1].record(stream)
-        f = rg.render_forward(g, bvh, cfg, camera=cam, out=fo)
+        f = rg.render_forward(g, bvh, cfg, camera=cam, out=fo, log=flog)
         if marks is not None:
             marks[2].record(stream)
         loss.zero_()
@@ -258,7 +259,7 @@ def run_ours(args):
     # counters for the roofline's algorithmic work (one instrumented step, untimed)
     st_f, st_b = rg.new_stats(dev), rg.new_stats(dev)
     bvh = rg.build_bvh(g, cfg, ws=bws)
-    f = rg.render_forward(g, bvh, cfg, camera=cam, out=fo, stats=st_f)
+    f = rg.render_forward(g, bvh, cfg, camera=cam, out=fo, stats=st_f, log=flog)
     rg.l1_loss_grad(f["rgb"], tgt_dev, scale, d_rgb=drgb, loss=loss)
     gb.zero_()
     rg.render_backward(g, bvh, cfg, f, drgb, camera=cam, grads=gb.views, ws=gws, stats=st_b)

@@ -237,11 +237,13 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
 cudaError_t launch_camera_rays(const rg_camera& cam, float* o, float* d, cudaStream_t st);
 cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,
                            const rg_rays* rays, const rg_camera* cam, float* rgb, float* T,
-                           int32_t* replay, rg_stats* stats, int dbg_rays, int dbg_cap,
+                           int32_t* replay, int32_t* log, int log_words, rg_stats* stats,
+                           int dbg_rays, int dbg_cap,
                            int32_t* dbg_counts, int32_t* dbg_rec, cudaStream_t st);
 cudaError_t launch_backward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,
                             const rg_rays* rays, const rg_camera* cam, const float* rgb,
-                            const float* T, const int32_t* replay, const float* d_rgb,
+                            const float* T, const int32_t* replay, const int32_t* log,
+                            int log_words, const float* d_rgb,
                             const rg_gaussian_grads& grads, rg_stats* stats, float* gbuf,
                             cudaStream_t st);
 void count_launches(unsigned n);

@@ -35,7 +35,10 @@ namespace {
 constexpr int kWarps = 4;              // rays (warps) per block
 constexpr int kBlock = 32 * kWarps;
 constexpr int kA = 64;                 // persistent active-list capacity
-constexpr int kSlots = kA + 32;        // + one transient chunk (slab sets > kA)
+constexpr int kTrans = kA;             // transient chunk slots (slab sets > kA)
+constexpr int kRet = kA + 32;          // retired (expired, not yet scattered) slots, backward
+constexpr int kSlots = kA + 64;
+static_assert(kA == 64, "expire/n_in handle two 32-slot chunks");
 constexpr int kStk = 256;              // traversal stack (wide nodes)
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -55,6 +58,8 @@ struct RenderArgs {
   float* rgb;
   float* T;
   int32_t* replay;
+  int32_t* log;            // per-ray fetch log [n_rays, log_words] (forward writes, backward reads)
+  int log_words;
   rg_stats* stats;
   int dbg_rays, dbg_cap;
   int32_t* dbg_counts;
@@ -67,18 +72,18 @@ struct RenderArgs {
   int gstride;
 };
 
+// per-slot entry (AoS, three float4 so a lane reads a slot with LDS.128):
+//   e0 = {t_entry, t_exit, t_mid, c0}   e1 = {c1, c2, r, g}   e2 = {b, pos, idx, -}
 struct WarpMem {
-  float te[kSlots], tx[kSlots], tm[kSlots], c0[kSlots], c1[kSlots], c2[kSlots];
-  float cr[kSlots], cg[kSlots], cb[kSlots];
-  int pos[kSlots];
-  uint32_t idx[kSlots];
+  float4 e0[kSlots], e1[kSlots], e2[kSlots];
   int stk[kStk];
   unsigned long long kscr[32];
   uint32_t pscr[32];
   float Y[16];
 };
 struct WarpAcc {
-  float a[6][kSlots];   // Sw, Sw1, Sw2, dc_r, dc_g, dc_b per slot
+  float4 a[kSlots];    // Sw, Sw1, Sw2, dc_r
+  float2 b[kSlots];    // dc_g, dc_b
 };
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
@@ -235,8 +240,8 @@ __device__ __forceinline__ float3 pair_color(const SceneView& S, int pos, const 
 // Per-(ray, Gaussian) set-up into slot `sl`: exact interval and the exponent
 // polynomial of w(tau) = sigma~ exp(-|u + tau d_l|^2 / 2) = 2^(c0 + tau (c1 + c2 tau)),
 // tau = t - t_mid, u = M x' from the compensated offset x' (value path).
-__device__ void setup_pair(const SceneView& S, WarpMem& M, int sl, const Ray& R,
-                           unsigned long long key, uint32_t pos) {
+__device__ __noinline__ void setup_pair(const SceneView& S, WarpMem& M, int sl, const Ray& R,
+                                        uint32_t pos) {
   const float4* gp = S.geom + 4 * (size_t)pos;
   const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2), g3 = __ldg(gp + 3);
   PairGeom pg;
@@ -250,17 +255,9 @@ __device__ void setup_pair(const SceneView& S, WarpMem& M, int sl, const Ray& R,
   const float qm = u0 * u0 + u1 * u1 + u2 * u2;
   const float b1 = u0 * pg.dl0 + u1 * pg.dl1 + u2 * pg.dl2;
   const float3 col = pair_color(S, (int)pos, R.d);
-  M.te[sl] = pg.te;
-  M.tx[sl] = pg.tx;
-  M.tm[sl] = pg.tm;
-  M.c0[sl] = lg2_approx(g0.w) - 0.5f * kLog2e * qm;
-  M.c1[sl] = -kLog2e * b1;
-  M.c2[sl] = -0.5f * kLog2e * pg.A;
-  M.cr[sl] = col.x;
-  M.cg[sl] = col.y;
-  M.cb[sl] = col.z;
-  M.pos[sl] = (int)pos;
-  M.idx[sl] = (uint32_t)(key & 0xFFFFFFFFu);
+  M.e0[sl] = make_float4(pg.te, pg.tx, pg.tm, lg2_approx(g0.w) - 0.5f * kLog2e * qm);
+  M.e1[sl] = make_float4(-kLog2e * b1, -0.5f * kLog2e * pg.A, col.x, col.y);
+  M.e2[sl] = make_float4(col.z, __int_as_float((int)pos), g3.z, 0.f);
 }
 
 // 1 - exp(-x) without cancellation for small x
@@ -269,53 +266,68 @@ __device__ __forceinline__ float alpha_of(float x, float e) {
   return 1.0f - e;
 }
 
-struct Lanes {   // lane -> (entry subset, sample) mapping for one sample group
-  int GW, ER, j, esub;
+// lane -> (entry subset esub, sample j) for one group of GW samples
+template <int GW>
+struct Lanes {
+  static constexpr int ER = 32 / GW;
+  int j, esub;
 };
 
 // sigma and sigma*c at this lane's sample from slots [e0, e1)
-__device__ __forceinline__ void eval_range(const WarpMem& M, int e0, int e1, const Lanes& L, float tk,
-                                           bool val, float& s, float& r, float& g, float& b,
-                                           uint32_t& evals) {
-  for (int e = e0 + L.esub; e < e1; e += L.ER) {
-    const float te = M.te[e], tx = M.tx[e];
-    if (val && te <= tk && tk <= tx) {
-      const float tau = tk - M.tm[e];
-      const float w = ex2_approx(fmaf(tau, fmaf(M.c2[e], tau, M.c1[e]), M.c0[e]));
+template <int GW>
+__device__ __forceinline__ void eval_range(const WarpMem& M, int e0, int e1, const Lanes<GW>& L,
+                                           float tk, bool val, float& s, float& r, float& g,
+                                           float& b, uint32_t& evals) {
+#pragma unroll 2
+  for (int e = e0 + L.esub; e < e1; e += Lanes<GW>::ER) {
+    const float4 a = M.e0[e];
+    if (val && a.x <= tk && tk <= a.y) {
+      const float4 q = M.e1[e];
+      const float cb = M.e2[e].x;
+      const float tau = tk - a.z;
+      const float w = ex2_approx(fmaf(tau, fmaf(q.y, tau, q.x), a.w));
       s += w;
-      r = fmaf(w, M.cr[e], r);
-      g = fmaf(w, M.cg[e], g);
-      b = fmaf(w, M.cb[e], b);
+      r = fmaf(w, q.z, r);
+      g = fmaf(w, q.w, g);
+      b = fmaf(w, cb, b);
       ++evals;
     }
   }
 }
 
-struct SampleGrad {   // per-sample backward quantities (lane j of the group)
+struct SampleGrad {   // per-sample backward quantities (lanes of sample j)
   float dls, dc0, dc1, dc2, gc, inv;
 };
 
 // accumulate the per-pair moments of slots [e0, e1) for this group's samples
+template <int GW>
 __device__ __forceinline__ void grad_range(const WarpMem& M, WarpAcc& A, int e0, int e1,
-                                           const Lanes& L, float tk, bool live,
+                                           const Lanes<GW>& L, float tk, bool live,
                                            const SampleGrad& H) {
-  const int rounds = (e1 - e0 + L.ER - 1) / L.ER;
-  for (int r = 0; r < rounds; ++r) {
-    const int e = e0 + L.esub + r * L.ER;
+  constexpr int ER = Lanes<GW>::ER;
+  const int rounds = (e1 - e0 + ER - 1) / ER;
+  for (int rr = 0; rr < rounds; ++rr) {
+    const int e = e0 + L.esub + rr * ER;
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
-    if (e < e1 && live && M.te[e] <= tk && tk <= M.tx[e]) {
-      const float tau = tk - M.tm[e];
-      const float w = ex2_approx(fmaf(tau, fmaf(M.c2[e], tau, M.c1[e]), M.c0[e]));
-      const float dldw = H.dls + (H.dc0 * M.cr[e] + H.dc1 * M.cg[e] + H.dc2 * M.cb[e] - H.gc) * H.inv;
-      const float wd = w * dldw, wi = w * H.inv;
-      a0 = wd;
-      a1 = wd * tau;
-      a2 = wd * tau * tau;
-      a3 = wi * H.dc0;
-      a4 = wi * H.dc1;
-      a5 = wi * H.dc2;
+    if (e < e1 && live) {
+      const float4 a = M.e0[e];
+      if (a.x <= tk && tk <= a.y) {
+        const float4 q = M.e1[e];
+        const float cb = M.e2[e].x;
+        const float tau = tk - a.z;
+        const float w = ex2_approx(fmaf(tau, fmaf(q.y, tau, q.x), a.w));
+        const float dldw = H.dls + (H.dc0 * q.z + H.dc1 * q.w + H.dc2 * cb - H.gc) * H.inv;
+        const float wd = w * dldw, wi = w * H.inv;
+        a0 = wd;
+        a1 = wd * tau;
+        a2 = wd * tau * tau;
+        a3 = wi * H.dc0;
+        a4 = wi * H.dc1;
+        a5 = wi * H.dc2;
+      }
     }
-    for (int off = 1; off < L.GW; off <<= 1) {
+#pragma unroll
+    for (int off = 1; off < GW; off <<= 1) {
       a0 += __shfl_xor_sync(kFull, a0, off);
       a1 += __shfl_xor_sync(kFull, a1, off);
       a2 += __shfl_xor_sync(kFull, a2, off);
@@ -324,32 +336,71 @@ __device__ __forceinline__ void grad_range(const WarpMem& M, WarpAcc& A, int e0,
       a5 += __shfl_xor_sync(kFull, a5, off);
     }
     if (L.j == 0 && e < e1) {
-      A.a[0][e] += a0; A.a[1][e] += a1; A.a[2][e] += a2;
-      A.a[3][e] += a3; A.a[4][e] += a4; A.a[5][e] += a5;
+      float4 v = A.a[e];
+      float2 w = A.b[e];
+      v.x += a0; v.y += a1; v.z += a2; v.w += a3;
+      w.x += a4; w.y += a5;
+      A.a[e] = v;
+      A.b[e] = w;
     }
   }
   __syncwarp();
 }
 
-// Warp-cooperative gradient scatter of slot `e` (lane c writes float4 chunk c):
-//  chunk 0 = (dL/dmu, dL/dsigma~), chunks 1-3 = dL/dM (9 + pad), chunks 4.. = appearance.
+// Per-lane map of the appearance part of a gradient row: lane c owns the
+// float4 chunk 4 + c, i.e. appearance floats 4c..4c+3 (SH then SG lobes).
+struct AppMap {
+  int8_t kind[4];   // 0 pad, 1 SH, 2 SG
+  int8_t a[4];      // SH: coefficient m; SG: lobe j
+  int8_t b[4];      // SH: channel; SG: component 0..6
+  int nchunks;
+};
+__device__ __forceinline__ AppMap app_map(const SceneView& S) {
+  AppMap m;
+  const int c = (int)lane_id();
+  const int nc = (S.deg + 1) * (S.deg + 1);
+  for (int k = 0; k < 4; ++k) {
+    const int f = 4 * c + k;
+    if (f < 3 * nc) { m.kind[k] = 1; m.a[k] = (int8_t)(f / 3); m.b[k] = (int8_t)(f % 3); }
+    else if (f < 3 * nc + 7 * S.lobes) {
+      m.kind[k] = 2; m.a[k] = (int8_t)((f - 3 * nc) / 7); m.b[k] = (int8_t)((f - 3 * nc) % 7);
+    } else { m.kind[k] = 0; m.a[k] = 0; m.b[k] = 0; }
+  }
+  m.nchunks = S.app_stride / 4;
+  return m;
+}
+
+// Gradient scatter of the slots in `mask` (relative to `base`), warp-cooperative:
+//  geometry: each lane owning a slot computes its 13 values, 4 float4 atomics;
+//  appearance: per slot, lane c writes chunk 4 + c (one coalesced burst).
 //  With x = x' + tau d, u = M x', d_l = M d and Sw = sum w dL/dw, Sw1 = sum w dL/dw tau,
 //  Sw2 = sum w dL/dw tau^2:  dL/dmu = M^T (Sw u + Sw1 d_l),
 //  dL/dM = -(Sw u x'^T + Sw1 (u d^T + d_l x'^T) + Sw2 d_l d^T),  dL/dsigma~ = Sw / sigma~.
-__device__ void scatter_slot(const SceneView& S, const WarpMem& M, const WarpAcc& A, int e,
-                             const Ray& R, float* gbuf, int gstride) {
-  const float Sw = A.a[0][e], Sw1 = A.a[1][e], Sw2 = A.a[2][e];
-  const float d0 = A.a[3][e], d1 = A.a[4][e], d2 = A.a[5][e];
-  if (Sw == 0.f && Sw1 == 0.f && Sw2 == 0.f && d0 == 0.f && d1 == 0.f && d2 == 0.f) return;
-  const int c = (int)lane_id();
-  const int pos = M.pos[e];
-  const int nchunks = 4 + S.app_stride / 4;
-  float v[4] = {0.f, 0.f, 0.f, 0.f};
-  if (c < 4) {
+__device__ __noinline__ void scatter_batch(const SceneView& S, const WarpMem& M, const WarpAcc& A,
+                                           int base, unsigned mask, const Ray& R, const AppMap& am,
+                                           float* gbuf, int gstride) {
+  const unsigned lane = lane_id();
+  // drop slots with all-zero moments (never contributed)
+  {
+    bool nz = false;
+    if (mask & (1u << lane)) {
+      const float4 v = A.a[base + lane];
+      const float2 w = A.b[base + lane];
+      nz = v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f || w.x != 0.f || w.y != 0.f;
+    }
+    mask = __ballot_sync(kFull, nz);
+  }
+  if (!mask) return;
+  if (mask & (1u << lane)) {
+    const int e = base + (int)lane;
+    const float4 acc = A.a[e];
+    const float Sw = acc.x, Sw1 = acc.y, Sw2 = acc.z;
+    const float4 x0 = M.e0[e];
+    const int pos = __float_as_int(M.e2[e].y);
     const float4* gp = S.geom + 4 * (size_t)pos;
     const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2), g3 = __ldg(gp + 3);
     const float Mm[9] = {g1.x, g1.y, g1.z, g1.w, g2.x, g2.y, g2.z, g2.w, g3.x};
-    const float tm = M.tm[e];
+    const float tm = x0.z;
     const float xp[3] = {offset_at(R.o.x, g0.x, tm, R.d.x), offset_at(R.o.y, g0.y, tm, R.d.y),
                          offset_at(R.o.z, g0.z, tm, R.d.z)};
     const float dv[3] = {R.d.x, R.d.y, R.d.z};
@@ -359,54 +410,66 @@ __device__ void scatter_slot(const SceneView& S, const WarpMem& M, const WarpAcc
       u[r] = Mm[3 * r] * xp[0] + Mm[3 * r + 1] * xp[1] + Mm[3 * r + 2] * xp[2];
       dl[r] = Mm[3 * r] * dv[0] + Mm[3 * r + 1] * dv[1] + Mm[3 * r + 2] * dv[2];
     }
-    float out[16];
+    float gm[3];
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      float acc = 0.f;
+      float t = 0.f;
 #pragma unroll
-      for (int r = 0; r < 3; ++r) acc += Mm[3 * r + b] * (Sw * u[r] + Sw1 * dl[r]);
-      out[b] = acc;
+      for (int r = 0; r < 3; ++r) t += Mm[3 * r + b] * (Sw * u[r] + Sw1 * dl[r]);
+      gm[b] = t;
     }
-    out[3] = Sw / g0.w;
+    float dM[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int b = 0; b < 3; ++b)
-        out[4 + 3 * r + b] = -(Sw * u[r] * xp[b] + Sw1 * (u[r] * dv[b] + dl[r] * xp[b]) +
-                               Sw2 * dl[r] * dv[b]);
-    out[13] = out[14] = out[15] = 0.f;
+        dM[3 * r + b] = -(Sw * u[r] * xp[b] + Sw1 * (u[r] * dv[b] + dl[r] * xp[b]) +
+                          Sw2 * dl[r] * dv[b]);
+    float4* row = reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride);
+    atomicAdd(row + 0, make_float4(gm[0], gm[1], gm[2], Sw / g0.w));
+    atomicAdd(row + 1, make_float4(dM[0], dM[1], dM[2], dM[3]));
+    atomicAdd(row + 2, make_float4(dM[4], dM[5], dM[6], dM[7]));
+    atomicAdd(row + 3, make_float4(dM[8], 0.f, 0.f, 0.f));
+  }
+  const int nc = (S.deg + 1) * (S.deg + 1);
+  while (mask) {
+    const int b = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const int e = base + b;
+    const float4 acc = A.a[e];
+    const float2 acb = A.b[e];
+    const float d0 = acc.w, d1 = acb.x, d2 = acb.y;
+    const int pos = __float_as_int(M.e2[e].y);
+    if ((int)lane < am.nchunks) {
+      const float* ap = S.app + (size_t)pos * S.app_stride + 3 * nc;
+      float v[4];
+      int cached = -1;
+      float e_j = 0.f, kd = 0.f, dp = 0.f, lam = 0.f;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = out[4 * c + k];
-  } else if (c < nchunks) {
-    const int nc = (S.deg + 1) * (S.deg + 1);
-    const float dc[3] = {d0, d1, d2};
-    const float* ap = S.app + (size_t)pos * S.app_stride + 3 * nc;
-    int lobe_cached = -1;
-    float e_j = 0.f, kd = 0.f, dp = 0.f, lam = 0.f;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int f = 4 * (c - 4) + k;
-      if (f < 3 * nc) {
-        v[k] = dc[f % 3] * M.Y[f / 3];
-      } else if (f < 3 * nc + 7 * S.lobes) {
-        const int j = (f - 3 * nc) / 7, rr = (f - 3 * nc) % 7;
-        if (j != lobe_cached) {
-          const float* q = ap + 7 * j;
-          lam = __ldg(q + 3);
-          dp = R.d.x * __ldg(q + 4) + R.d.y * __ldg(q + 5) + R.d.z * __ldg(q + 6);
-          e_j = ex2_approx(lam * (dp - 1.0f) * kLog2e);
-          kd = (d0 * __ldg(q) + d1 * __ldg(q + 1) + d2 * __ldg(q + 2)) * e_j;
-          lobe_cached = j;
+      for (int k = 0; k < 4; ++k) {
+        v[k] = 0.f;
+        if (am.kind[k] == 1) {
+          const int ch = am.b[k];
+          v[k] = (ch == 0 ? d0 : (ch == 1 ? d1 : d2)) * M.Y[am.a[k]];
+        } else if (am.kind[k] == 2) {
+          const int j = am.a[k], r = am.b[k];
+          if (j != cached) {
+            const float* q = ap + 7 * j;
+            lam = __ldg(q + 3);
+            dp = R.d.x * __ldg(q + 4) + R.d.y * __ldg(q + 5) + R.d.z * __ldg(q + 6);
+            e_j = ex2_approx(lam * (dp - 1.0f) * kLog2e);
+            kd = (d0 * __ldg(q) + d1 * __ldg(q + 1) + d2 * __ldg(q + 2)) * e_j;
+            cached = j;
+          }
+          if (r < 3) v[k] = (r == 0 ? d0 : (r == 1 ? d1 : d2)) * e_j;
+          else if (r == 3) v[k] = kd * (dp - 1.0f);
+          else v[k] = kd * lam * (r == 4 ? R.d.x : (r == 5 ? R.d.y : R.d.z));
         }
-        if (rr < 3) v[k] = dc[rr] * e_j;
-        else if (rr == 3) v[k] = kd * (dp - 1.0f);
-        else v[k] = kd * lam * (rr == 4 ? R.d.x : (rr == 5 ? R.d.y : R.d.z));
       }
+      atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + lane,
+                make_float4(v[0], v[1], v[2], v[3]));
     }
   }
-  if (c < nchunks)
-    atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + c,
-              make_float4(v[0], v[1], v[2], v[3]));
 }
 
 __device__ __forceinline__ int skip_to(float te, int s, int B, float dt, float t0, float t1) {
@@ -437,7 +500,18 @@ __device__ __forceinline__ void kadd(float& s, float& comp, float x) {
   s = t;
 }
 
-template <bool BWD>
+__device__ __forceinline__ void dbg_put(const RenderArgs& P, int ray, int& dbg_n, int s, int n,
+                                        const WarpMem& M, int first) {
+  for (int e = (int)lane_id(); e < n; e += 32)
+    if (dbg_n + e < P.dbg_cap) {
+      int32_t* r = P.dbg_rec + 2 * ((size_t)ray * P.dbg_cap + dbg_n + e);
+      r[0] = s;
+      r[1] = (int32_t)__float_as_uint(M.e2[first + e].z);
+    }
+  dbg_n = min(P.dbg_cap, dbg_n + n);
+}
+
+template <bool BWD, int GW>
 __global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const unsigned lane = lane_id();
@@ -480,27 +554,26 @@ __global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
   if (hit && !(BWD && gr0 == 0.f && gr1 == 0.f && gr2 == 0.f)) {
     R.inv = make_float3(1.0f / R.d.x, 1.0f / R.d.y, 1.0f / R.d.z);
     R.oinv = make_float3(R.o.x * R.inv.x, R.o.y * R.inv.y, R.o.z * R.inv.z);
+    AppMap am;
     if (BWD) {
+      am = app_map(P.S);
       float Y[16];
       sh_basis(P.S.deg, R.d.x, R.d.y, R.d.z, Y);
-      if (lane < 16) {
 #pragma unroll
-        for (int m = 0; m < 16; ++m)
-          if ((int)lane == m) M.Y[m] = Y[m];
-      }
+      for (int m = 0; m < 16; ++m)
+        if ((int)lane == m) M.Y[m] = Y[m];
       __syncwarp();
     }
-    // lane mapping for sample groups
-    Lanes L;
-    L.GW = B >= 8 ? 8 : (B >= 4 ? 4 : (B >= 2 ? 2 : 1));
-    if (B == 3) L.GW = 4;
-    if (B > 4 && B < 8) L.GW = 8;
-    L.ER = 32 / L.GW;
-    L.j = (int)lane % L.GW;
-    L.esub = (int)lane / L.GW;
-    int count = 0;
+    Lanes<GW> L;
+    L.j = (int)(lane % GW);
+    L.esub = (int)(lane / GW);
+    int count = 0, nret = 0;
     unsigned long long cursor = 0;
     bool exhausted = false;
+    int32_t* lg = P.log ? P.log + (size_t)ray * P.log_words : nullptr;
+    int lp = 1;
+    bool log_ok = lg != nullptr;
+    const bool replay_log = BWD && lg != nullptr && lg[0] >= 0;
     int s = 0;
     while (true) {
       const int k0 = s * B;
@@ -509,73 +582,106 @@ __global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
       const float thi = fminf(t1, fma_((float)(k0 + B), c.dt, t0));
       // ---- expire Gaussians whose support ended before this slab
       {
-        int nc = 0;
-        for (int base = 0; base < count; base += 32) {
-          const int e = base + (int)lane;
-          const bool valid = e < count;
-          const bool keep = valid && M.tx[e] >= tlo;
-          if (BWD) {
-            unsigned xm = __ballot_sync(kFull, valid && !keep);
-            while (xm) {
-              const int b = __ffs(xm) - 1;
-              xm &= xm - 1;
-              scatter_slot(P.S, M, A, base + b, R, P.gbuf, P.gstride);
+        unsigned gone0 = 0, gone1 = 0;
+        {
+          const int e = (int)lane;
+          gone0 = __ballot_sync(kFull, e < count && M.e0[e].y < tlo);
+          gone1 = __ballot_sync(kFull, e + 32 < count && M.e0[e + 32].y < tlo);
+        }
+        if (gone0 | gone1) {
+          if (BWD) {   // retire expired pairs; scatter them 32 at a time
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const unsigned gm = h ? gone1 : gone0;
+              if (!gm) continue;
+              if (nret + __popc(gm) > 32) {
+                scatter_batch(P.S, M, A, kRet, nret >= 32 ? kFull : ((1u << nret) - 1u), R, am,
+                              P.gbuf, P.gstride);
+                nret = 0;
+                __syncwarp();
+              }
+              if ((gm >> lane) & 1u) {
+                const int e = h * 32 + (int)lane;
+                const int dst = kRet + nret + __popc(gm & ((1u << lane) - 1u));
+                M.e0[dst] = M.e0[e]; M.e1[dst] = M.e1[e]; M.e2[dst] = M.e2[e];
+                A.a[dst] = A.a[e]; A.b[dst] = A.b[e];
+              }
+              nret += __popc(gm);
+              __syncwarp();
             }
           }
-          float f[9];
-          int ps = 0;
-          uint32_t ix = 0;
-          float ac[6];
-          if (keep) {
-            f[0] = M.te[e]; f[1] = M.tx[e]; f[2] = M.tm[e]; f[3] = M.c0[e]; f[4] = M.c1[e];
-            f[5] = M.c2[e]; f[6] = M.cr[e]; f[7] = M.cg[e]; f[8] = M.cb[e];
-            ps = M.pos[e]; ix = M.idx[e];
-            if (BWD)
-              for (int k = 0; k < 6; ++k) ac[k] = A.a[k][e];
+          int nc = 0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int e = h * 32 + (int)lane;
+            const bool keep = e < count && !(((h ? gone1 : gone0) >> lane) & 1u);
+            float4 v0, v1, v2, a0;
+            float2 a1;
+            if (keep) {
+              v0 = M.e0[e]; v1 = M.e1[e]; v2 = M.e2[e];
+              if (BWD) { a0 = A.a[e]; a1 = A.b[e]; }
+            }
+            const unsigned km = __ballot_sync(kFull, keep);
+            const int dst = nc + __popc(km & ((1u << lane) - 1u));
+            __syncwarp();
+            if (keep) {
+              M.e0[dst] = v0; M.e1[dst] = v1; M.e2[dst] = v2;
+              if (BWD) { A.a[dst] = a0; A.b[dst] = a1; }
+            }
+            nc += __popc(km);
+            __syncwarp();
           }
-          const unsigned km = __ballot_sync(kFull, keep);
-          const int dst = nc + __popc(km & ((1u << lane) - 1u));
-          __syncwarp();
-          if (keep) {
-            M.te[dst] = f[0]; M.tx[dst] = f[1]; M.tm[dst] = f[2]; M.c0[dst] = f[3];
-            M.c1[dst] = f[4]; M.c2[dst] = f[5]; M.cr[dst] = f[6]; M.cg[dst] = f[7];
-            M.cb[dst] = f[8]; M.pos[dst] = ps; M.idx[dst] = ix;
-            if (BWD)
-              for (int k = 0; k < 6; ++k) A.a[k][dst] = ac[k];
-          }
-          nc += __popc(km);
-          __syncwarp();
+          count = nc;
         }
-        count = nc;
       }
       // ---- refill in key order until every Gaussian entering by t_hi is held
-      while (!exhausted && count < kA && (count == 0 || M.te[count - 1] <= thi)) {
+      while (!exhausted && count < kA && (count == 0 || M.e0[count - 1].x <= thi)) {
         const int want = min(32, kA - count);
-        unsigned long long key;
-        uint32_t pos;
-        const int got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
+        unsigned long long key = 0;
+        uint32_t pos = 0;
+        int got;
+        if (BWD && replay_log) {      // the forward's query results, no traversal
+          got = lg[lp];
+          if ((int)lane < got) pos = (uint32_t)lg[lp + 1 + lane];
+          lp += 1 + got;
+        } else {
+          got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
+          if (!BWD && log_ok) {
+            if (lp + 1 + got > P.log_words) {
+              log_ok = false;
+            } else {
+              if (lane == 0) lg[lp] = got;
+              if ((int)lane < got) lg[lp + 1 + lane] = (int)pos;
+              lp += 1 + got;
+            }
+          }
+        }
         if ((int)lane < got) {
-          setup_pair(P.S, M, count + (int)lane, R, key, pos);
-          if (BWD)
-            for (int k = 0; k < 6; ++k) A.a[k][count + lane] = 0.f;
+          setup_pair(P.S, M, count + (int)lane, R, pos);
+          if (BWD) {
+            A.a[count + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+            A.b[count + lane] = make_float2(0.f, 0.f);
+          }
         }
         if (lane == 0) cnt.pairs += got;
-        if (got > 0) cursor = shfl64(key, got - 1);
         count += got;
         if (got < want) exhausted = true;
         __syncwarp();
+        if (got > 0) {
+          const int l = count - 1;
+          cursor = ((unsigned long long)fkey(M.e0[l].x) << 32) | __float_as_uint(M.e2[l].z);
+        }
       }
       if (count == 0) break;
-      if (M.te[0] > thi) {   // empty slab(s): jump to the slab holding the next entry
-        s = skip_to(M.te[0], s, B, c.dt, t0, t1);
+      if (M.e0[0].x > thi) {   // empty slab(s): jump to the slab holding the next entry
+        s = skip_to(M.e0[0].x, s, B, c.dt, t0, t1);
         continue;
       }
-      int n_in = 0;
-      for (int base = 0; base < count; base += 32) {
-        const int e = base + (int)lane;
-        const unsigned m = __ballot_sync(kFull, e < count && M.te[e] <= thi);
-        n_in += __popc(m);
-        if (m != kFull) break;
+      int n_in;
+      {
+        const unsigned m0 = __ballot_sync(kFull, (int)lane < count && M.e0[lane].x <= thi);
+        const unsigned m1 = __ballot_sync(kFull, (int)lane + 32 < count && M.e0[lane + 32].x <= thi);
+        n_in = __popc(m0) + __popc(m1);
       }
       const int n_use = min(n_in, K);
       const bool more = (n_in == kA) && !exhausted && (K > kA);
@@ -586,21 +692,13 @@ __global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
         uint32_t pp;
         if (fetch(P.S, M, R, tlo, thi, cursor, 1, pk, pp, cnt) > 0 && lane == 0) cnt.overflows++;
       }
-      if (dbg) {
-        for (int e = (int)lane; e < n_use; e += 32)
-          if (dbg_n + e < P.dbg_cap) {
-            int32_t* r = P.dbg_rec + 2 * ((size_t)ray * P.dbg_cap + dbg_n + e);
-            r[0] = s;
-            r[1] = (int32_t)M.idx[e];
-          }
-        dbg_n = min(P.dbg_cap, dbg_n + n_use);
-      }
-      for (int g0 = 0; g0 < B; g0 += L.GW) {
+      if (dbg) dbg_put(P, ray, dbg_n, s, n_use, M, 0);
+      for (int g0 = 0; g0 < B; g0 += GW) {
         const float tk = sample_t(k0 + g0 + L.j, c.dt, t0);
         const bool val = (g0 + L.j < B) && (tk < t1);
         float sg = 0.f, sr = 0.f, sgg = 0.f, sb = 0.f;
         uint32_t ev = 0;
-        eval_range(M, 0, n_use, L, tk, val, sg, sr, sgg, sb, ev);
+        eval_range<GW>(M, 0, n_use, L, tk, val, sg, sr, sgg, sb, ev);
         if (more) {   // slab set larger than the active list: stream the rest
           unsigned long long cur2 = cursor;
           int remaining = K - n_use;
@@ -610,17 +708,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
             unsigned long long key;
             uint32_t pos;
             const int got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
-            if ((int)lane < got) setup_pair(P.S, M, kA + (int)lane, R, key, pos);
+            if ((int)lane < got) setup_pair(P.S, M, kTrans + (int)lane, R, pos);
             __syncwarp();
-            eval_range(M, kA, kA + got, L, tk, val, sg, sr, sgg, sb, ev);
-            if (dbg && g0 == 0) {
-              if ((int)lane < got && dbg_n + (int)lane < P.dbg_cap) {
-                int32_t* r = P.dbg_rec + 2 * ((size_t)ray * P.dbg_cap + dbg_n + lane);
-                r[0] = s;
-                r[1] = (int32_t)M.idx[kA + lane];
-              }
-              dbg_n = min(P.dbg_cap, dbg_n + got);
-            }
+            eval_range<GW>(M, kA, kA + got, L, tk, val, sg, sr, sgg, sb, ev);
+            if (dbg && g0 == 0) dbg_put(P, ray, dbg_n, s, got, M, kA);
             if (g0 == 0 && lane == 0) cnt.pairs += got;
             remaining -= got;
             if (got > 0) cur2 = shfl64(key, got - 1);
@@ -635,7 +726,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
         }
         cnt.evals += ev;
         // reduce over the entry subsets: every lane of sample j holds the totals
-        for (int off = L.GW; off < 32; off <<= 1) {
+#pragma unroll
+        for (int off = GW; off < 32; off <<= 1) {
           sg += __shfl_xor_sync(kFull, sg, off);
           sr += __shfl_xor_sync(kFull, sr, off);
           sgg += __shfl_xor_sync(kFull, sgg, off);
@@ -645,8 +737,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
         const bool live = val && sg > 0.f;
         const float x = live ? sg * c.dt : 0.f;
         float incl = x;
-        for (int dd = 1; dd < L.GW; dd <<= 1) {
-          const float v = __shfl_up_sync(kFull, incl, dd, L.GW);
+#pragma unroll
+        for (int dd = 1; dd < GW; dd <<= 1) {
+          const float v = __shfl_up_sync(kFull, incl, dd, GW);
           if (L.j >= dd) incl += v;
         }
         const float excl = incl - x;
@@ -656,13 +749,12 @@ __global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
         const float inv_s = live ? 1.0f / sg : 0.f;
         const float cr = sr * inv_s, cg = sgg * inv_s, cb = sb * inv_s;
         const float wgt = live ? Tb * al : 0.f;
-        float q0 = wgt * cr, q1 = wgt * cg, q2 = wgt * cb;
-        // inclusive prefix of the contributions (backward needs C after each sample)
-        float p0 = q0, p1 = q1, p2 = q2;
-        for (int dd = 1; dd < L.GW; dd <<= 1) {
-          const float v0 = __shfl_up_sync(kFull, p0, dd, L.GW);
-          const float v1 = __shfl_up_sync(kFull, p1, dd, L.GW);
-          const float v2 = __shfl_up_sync(kFull, p2, dd, L.GW);
+        float p0 = wgt * cr, p1 = wgt * cg, p2 = wgt * cb;
+#pragma unroll
+        for (int dd = 1; dd < GW; dd <<= 1) {
+          const float v0 = __shfl_up_sync(kFull, p0, dd, GW);
+          const float v1 = __shfl_up_sync(kFull, p1, dd, GW);
+          const float v2 = __shfl_up_sync(kFull, p2, dd, GW);
           if (L.j >= dd) { p0 += v0; p1 += v1; p2 += v2; }
         }
         SampleGrad H = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -675,11 +767,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
           H.gc = H.dc0 * cr + H.dc1 * cg + H.dc2 * cb;
           H.inv = inv_s;
         }
-        const int last = L.GW - 1;
-        const float tot_x = __shfl_sync(kFull, incl, last, L.GW);
-        const float t0c = __shfl_sync(kFull, p0, last, L.GW);
-        const float t1c = __shfl_sync(kFull, p1, last, L.GW);
-        const float t2c = __shfl_sync(kFull, p2, last, L.GW);
+        const float tot_x = __shfl_sync(kFull, incl, GW - 1, GW);
+        const float t0c = __shfl_sync(kFull, p0, GW - 1, GW);
+        const float t1c = __shfl_sync(kFull, p1, GW - 1, GW);
+        const float t2c = __shfl_sync(kFull, p2, GW - 1, GW);
         kadd(tau, tauc, tot_x);
         kadd(C0, k0c, t0c);
         kadd(C1, k1c, t1c);
@@ -688,7 +779,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
         const unsigned smask = __ballot_sync(kFull, live && L.esub == 0);
         if (lane == 0) cnt.samples += __popc(smask);
         if (BWD) {
-          grad_range(M, A, 0, n_use, L, tk, live, H);
+          grad_range<GW>(M, A, 0, n_use, L, tk, live, H);
           if (more) {
             unsigned long long cur2 = cursor;
             int remaining = K - n_use;
@@ -698,12 +789,14 @@ __global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
               uint32_t pos;
               const int got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
               if ((int)lane < got) {
-                setup_pair(P.S, M, kA + (int)lane, R, key, pos);
-                for (int k = 0; k < 6; ++k) A.a[k][kA + lane] = 0.f;
+                setup_pair(P.S, M, kTrans + (int)lane, R, pos);
+                A.a[kA + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+                A.b[kA + lane] = make_float2(0.f, 0.f);
               }
               __syncwarp();
-              grad_range(M, A, kA, kA + got, L, tk, live, H);
-              for (int e = kA; e < kA + got; ++e) scatter_slot(P.S, M, A, e, R, P.gbuf, P.gstride);
+              grad_range<GW>(M, A, kA, kA + got, L, tk, live, H);
+              scatter_batch(P.S, M, A, kA, got >= 32 ? kFull : ((1u << got) - 1u), R, am, P.gbuf,
+                            P.gstride);
               remaining -= got;
               if (got > 0) cur2 = shfl64(key, got - 1);
               __syncwarp();
@@ -721,8 +814,16 @@ __global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
       }
       ++s;
     }
-    if (BWD)
-      for (int e = 0; e < count; ++e) scatter_slot(P.S, M, A, e, R, P.gbuf, P.gstride);
+    if (BWD) {
+      const unsigned m0 = count >= 32 ? kFull : ((1u << count) - 1u);
+      const unsigned m1 = count >= 64 ? kFull : (count > 32 ? ((1u << (count - 32)) - 1u) : 0u);
+      scatter_batch(P.S, M, A, 0, m0, R, am, P.gbuf, P.gstride);
+      scatter_batch(P.S, M, A, 32, m1, R, am, P.gbuf, P.gstride);
+      scatter_batch(P.S, M, A, kRet, nret >= 32 ? kFull : ((1u << nret) - 1u), R, am, P.gbuf,
+                    P.gstride);
+    } else if (lg != nullptr && lane == 0) {
+      lg[0] = log_ok ? lp : -1;
+    }
   }
   if (!BWD && lane == 0) {
     P.rgb[3 * ray] = C0 + T * c.background[0];
@@ -846,6 +947,15 @@ void ray_grid(RenderArgs& A, const rg_rays* rays, const rg_camera* cam, dim3& gr
   }
 }
 
+template <bool BWD>
+void launch_render(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
+  const int B = A.c.slab_samples;
+  if (B >= 5) k_render<BWD, 8><<<grid, kBlock, smem, st>>>(A);
+  else if (B >= 3) k_render<BWD, 4><<<grid, kBlock, smem, st>>>(A);
+  else if (B == 2) k_render<BWD, 2><<<grid, kBlock, smem, st>>>(A);
+  else k_render<BWD, 1><<<grid, kBlock, smem, st>>>(A);
+}
+
 constexpr size_t kSmemFwd = sizeof(WarpMem) * kWarps;
 constexpr size_t kSmemBwd = (sizeof(WarpMem) + sizeof(WarpAcc)) * kWarps;
 
@@ -859,8 +969,9 @@ cudaError_t launch_camera_rays(const rg_camera& cam, float* o, float* d, cudaStr
 
 cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,
                            const rg_rays* rays, const rg_camera* cam, float* rgb, float* T,
-                           int32_t* replay, rg_stats* stats, int dbg_rays, int dbg_cap,
-                           int32_t* dbg_counts, int32_t* dbg_rec, cudaStream_t st) {
+                           int32_t* replay, int32_t* log, int log_words, rg_stats* stats,
+                           int dbg_rays, int dbg_cap, int32_t* dbg_counts, int32_t* dbg_rec,
+                           cudaStream_t st) {
   (void)g;
   RenderArgs A = {};
   A.S = view_of(b);
@@ -869,20 +980,24 @@ cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_conf
   ray_grid(A, rays, cam, grid);
   if (A.n_rays == 0) return cudaSuccess;
   A.rgb = rgb; A.T = T; A.replay = replay; A.stats = stats;
+  A.log = log; A.log_words = log_words;
   A.dbg_rays = dbg_rec ? dbg_rays : 0;
   A.dbg_cap = dbg_cap; A.dbg_counts = dbg_counts; A.dbg_rec = dbg_rec;
-  k_render<false><<<grid, kBlock, kSmemFwd, st>>>(A);
+  launch_render<false>(A, grid, kSmemFwd, st);
   count_launches(1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_backward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,
                             const rg_rays* rays, const rg_camera* cam, const float* rgb,
-                            const float* T, const int32_t* replay, const float* d_rgb,
+                            const float* T, const int32_t* replay, const int32_t* log,
+                            int log_words, const float* d_rgb,
                             const rg_gaussian_grads& grads, rg_stats* stats, float* gbuf,
                             cudaStream_t st) {
   (void)T;
   RenderArgs A = {};
+  A.log = const_cast<int32_t*>(log);
+  A.log_words = log_words;
   A.S = view_of(b);
   A.c = c;
   dim3 grid;
@@ -891,7 +1006,7 @@ cudaError_t launch_backward(const rg_gaussians& g, const rg_bvh& b, const rg_con
   if (b.n > 0) cudaMemsetAsync(gbuf, 0, sizeof(float) * (size_t)gs * b.n, st);
   A.stats = stats;
   A.rgb_in = rgb; A.replay_in = replay; A.d_rgb = d_rgb; A.gbuf = gbuf; A.gstride = gs;
-  if (A.n_rays > 0) { k_render<true><<<grid, kBlock, kSmemBwd, st>>>(A); count_launches(1); }
+  if (A.n_rays > 0) { launch_render<true>(A, grid, kSmemBwd, st); count_launches(1); }
   if (b.n > 0) {
     k_finalize<<<(b.n + 255) / 256, 256, 0, st>>>(gbuf, gs, b.order, g, grads, stats);
     count_launches(1);

@@ -35,7 +35,7 @@ def gpu_forward(g, b, p, o, d, debug=None):
                             rays=(torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()),
                             stats=st, debug=debug)
     torch.cuda.synchronize()
-    res = {k: v.cpu().numpy() for k, v in out.items()}
+    res = {k: v.cpu().numpy() for k, v in out.items() if v is not None}
     res["stats"] = rg.stats_dict(st)
     return res
 
@@ -268,7 +268,7 @@ def test_backward_matches_oracle(oracle, seed, deg, sg, n):
     g, b = gpu_build(sc, p)
     cfg = rg.Config.of(p)
     to, td = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
-    fwd = rg.render_forward(g, b, cfg, rays=(to, td))
+    fwd = rg.render_forward(g, b, cfg, rays=(to, td), log=rg.new_log(len(o)) if seed != 1 else None)
     up = np.random.default_rng(seed).normal(size=(len(o), 3)).astype(np.float32)
     st = rg.new_stats()
     grads = rg.render_backward(g, b, cfg, fwd, torch.from_numpy(up).cuda(), rays=(to, td), stats=st)
@@ -289,7 +289,7 @@ def test_backward_overflow_path(oracle):
     g, b = gpu_build(sc, p)
     cfg = rg.Config.of(p)
     to, td = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
-    fwd = rg.render_forward(g, b, cfg, rays=(to, td))
+    fwd = rg.render_forward(g, b, cfg, rays=(to, td), log=rg.new_log(len(o)))
     up = np.random.default_rng(5).normal(size=(len(o), 3)).astype(np.float32)
     grads = rg.render_backward(g, b, cfg, fwd, torch.from_numpy(up).cuda(), rays=(to, td))
     torch.cuda.synchronize()
@@ -309,7 +309,7 @@ def test_backward_full_size_sampled(oracle):
     g, b = gpu_build(sc, p)
     cfg = rg.Config.of(p)
     to, td = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
-    fwd = rg.render_forward(g, b, cfg, rays=(to, td))
+    fwd = rg.render_forward(g, b, cfg, rays=(to, td), log=rg.new_log(len(o)))
     up = np.random.default_rng(7).normal(size=(len(o), 3)).astype(np.float32)
     grads = rg.render_backward(g, b, cfg, fwd, torch.from_numpy(up).cuda(), rays=(to, td))
     torch.cuda.synchronize()

@@ -1,7 +1,9 @@
 """Aggregate ncu warp-stall samples per CUDA source line (dev tool).
 usage: ncu_lines.py report.ncu-rep [kernel-substring] [topN]"""
 import collections, csv, subprocess, sys
-rep = sys.argv[1]; ksub = sys.argv[2] if len(sys.argv) > 2 else ""; top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+rep = sys.argv[1]; metric = "Instructions Executed" if "--inst" in sys.argv else "Warp Stall Sampling (All Samples)"
+sys.argv=[a for a in sys.argv if a!="--inst"]
+ksub = sys.argv[2] if len(sys.argv) > 2 else ""; top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
 def page(view):
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", view],
                          capture_output=True, text=True).stdout
@@ -26,7 +28,7 @@ for r in page("sass"):
         continue
     d = dict(zip(hdr, r))
     if ksub not in kern: continue
-    s = float(d.get("Warp Stall Sampling (All Samples)") or 0)
+    s = float(d.get(metric) or 0)
     per[kern][amap.get((kern, d["Address"]), "?")] += s
     for k in hdr:
         if k.startswith("stall_") and "Not Issued" not in k:

@@ -9,11 +9,12 @@ sc, cam, p = wl.scene, wl.cameras[0], wl.params
 g = rg.Gaussians.from_scene(sc)
 cfg = rg.Config.of(p)
 def ev(): return torch.cuda.Event(enable_timing=True)
+lg = rg.new_log(cam.n_rays)
 for it in range(3):
     st = rg.new_stats()
     e0, e1, e2, e3 = ev(), ev(), ev(), ev()
     e0.record(); b = rg.build_bvh(g, cfg); e1.record()
-    f = rg.render_forward(g, b, cfg, camera=cam, stats=st); e2.record()
+    f = rg.render_forward(g, b, cfg, camera=cam, stats=st, log=lg); e2.record()
     up = torch.full_like(f["rgb"], 1.0 / f["rgb"].numel())
     gr = rg.render_backward(g, b, cfg, f, up, camera=cam); e3.record()
     torch.cuda.synchronize()
