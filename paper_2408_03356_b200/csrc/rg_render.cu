@@ -347,26 +347,40 @@ __device__ __forceinline__ void grad_range(const WarpMem& M, WarpAcc& A, int e0,
   __syncwarp();
 }
 
-// Per-lane map of the appearance part of a gradient row: lane c owns the
-// float4 chunk 4 + c, i.e. appearance floats 4c..4c+3 (SH then SG lobes).
+// Per-lane map of the appearance part of a gradient row (rg_internal.cuh
+// grad_stride): lane c owns float4 chunk 4 + c.  SH chunks: channel `ch`,
+// coefficients 4q..4q+3 (their Y(d) values precomputed per ray in y);
+// SG chunks: component `comp`, lobes 4h..4h+3.
 struct AppMap {
-  int8_t kind[4];   // 0 pad, 1 SH, 2 SG
-  int8_t a[4];      // SH: coefficient m; SG: lobe j
-  int8_t b[4];      // SH: channel; SG: component 0..6
+  float4 y;          // SH: Y(d) of the lane's 4 coefficients (0 past nc)
+  int ch;            // SH channel, or SG component (0..6); -1: no chunk
+  int sg;            // 1 if an SG chunk
+  int h4;            // SG: first lobe of the chunk
+  float dcomp;       // SG components 4..6: d[comp - 4]
   int nchunks;
 };
-__device__ __forceinline__ AppMap app_map(const SceneView& S) {
+__device__ __forceinline__ AppMap app_map(const SceneView& S, const float3& d, const float* Y) {
   AppMap m;
   const int c = (int)lane_id();
   const int nc = (S.deg + 1) * (S.deg + 1);
-  for (int k = 0; k < 4; ++k) {
-    const int f = 4 * c + k;
-    if (f < 3 * nc) { m.kind[k] = 1; m.a[k] = (int8_t)(f / 3); m.b[k] = (int8_t)(f % 3); }
-    else if (f < 3 * nc + 7 * S.lobes) {
-      m.kind[k] = 2; m.a[k] = (int8_t)((f - 3 * nc) / 7); m.b[k] = (int8_t)((f - 3 * nc) % 7);
-    } else { m.kind[k] = 0; m.a[k] = 0; m.b[k] = 0; }
+  const int qsh = sh_pad(S.deg) / 4, qsg = sg_pad(S.lobes) / 4;
+  m.nchunks = 3 * qsh + 7 * qsg;
+  m.y = make_float4(0.f, 0.f, 0.f, 0.f);
+  m.ch = -1; m.sg = 0; m.h4 = 0; m.dcomp = 0.f;
+  if (c < 3 * qsh) {
+    m.ch = c / qsh;
+    const int q = c % qsh;
+    m.y.x = 4 * q + 0 < nc ? Y[4 * q + 0] : 0.f;
+    m.y.y = 4 * q + 1 < nc ? Y[4 * q + 1] : 0.f;
+    m.y.z = 4 * q + 2 < nc ? Y[4 * q + 2] : 0.f;
+    m.y.w = 4 * q + 3 < nc ? Y[4 * q + 3] : 0.f;
+  } else if (c < m.nchunks) {
+    const int cc = c - 3 * qsh;
+    m.sg = 1;
+    m.ch = cc / qsg;
+    m.h4 = 4 * (cc % qsg);
+    m.dcomp = m.ch == 4 ? d.x : (m.ch == 5 ? d.y : d.z);
   }
-  m.nchunks = S.app_stride / 4;
   return m;
 }
 
@@ -440,35 +454,31 @@ __device__ __noinline__ void scatter_batch(const SceneView& S, const WarpMem& M,
     const float2 acb = A.b[e];
     const float d0 = acc.w, d1 = acb.x, d2 = acb.y;
     const int pos = __float_as_int(M.e2[e].y);
-    if ((int)lane < am.nchunks) {
-      const float* ap = S.app + (size_t)pos * S.app_stride + 3 * nc;
-      float v[4];
-      int cached = -1;
-      float e_j = 0.f, kd = 0.f, dp = 0.f, lam = 0.f;
+    // per-lobe terms, lane j < lobes: e_j = exp(lambda (d.p - 1)), kd = <dc, k> e_j
+    float ej = 0.f, kd = 0.f, dpm = 0.f, lam = 0.f;
+    if ((int)lane < S.lobes) {
+      const float* q = S.app + (size_t)pos * S.app_stride + 3 * nc + 7 * lane;
+      lam = __ldg(q + 3);
+      dpm = R.d.x * __ldg(q + 4) + R.d.y * __ldg(q + 5) + R.d.z * __ldg(q + 6) - 1.0f;
+      ej = ex2_approx(lam * dpm * kLog2e);
+      kd = (d0 * __ldg(q) + d1 * __ldg(q + 1) + d2 * __ldg(q + 2)) * ej;
+    }
+    float v[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        v[k] = 0.f;
-        if (am.kind[k] == 1) {
-          const int ch = am.b[k];
-          v[k] = (ch == 0 ? d0 : (ch == 1 ? d1 : d2)) * M.Y[am.a[k]];
-        } else if (am.kind[k] == 2) {
-          const int j = am.a[k], r = am.b[k];
-          if (j != cached) {
-            const float* q = ap + 7 * j;
-            lam = __ldg(q + 3);
-            dp = R.d.x * __ldg(q + 4) + R.d.y * __ldg(q + 5) + R.d.z * __ldg(q + 6);
-            e_j = ex2_approx(lam * (dp - 1.0f) * kLog2e);
-            kd = (d0 * __ldg(q) + d1 * __ldg(q + 1) + d2 * __ldg(q + 2)) * e_j;
-            cached = j;
-          }
-          if (r < 3) v[k] = (r == 0 ? d0 : (r == 1 ? d1 : d2)) * e_j;
-          else if (r == 3) v[k] = kd * (dp - 1.0f);
-          else v[k] = kd * lam * (r == 4 ? R.d.x : (r == 5 ? R.d.y : R.d.z));
-        }
-      }
+    for (int k = 0; k < 4; ++k) {
+      const int src = (am.h4 + k) & 31;
+      const float e_k = __shfl_sync(kFull, ej, src);
+      const float kd_k = __shfl_sync(kFull, kd, src);
+      const float dpm_k = __shfl_sync(kFull, dpm, src);
+      const float lam_k = __shfl_sync(kFull, lam, src);
+      const float dsel = am.ch == 0 ? d0 : (am.ch == 1 ? d1 : d2);
+      const float yk = k == 0 ? am.y.x : (k == 1 ? am.y.y : (k == 2 ? am.y.z : am.y.w));
+      const float sg_v = am.ch < 3 ? dsel * e_k : (am.ch == 3 ? kd_k * dpm_k : kd_k * lam_k * am.dcomp);
+      v[k] = am.sg ? (am.h4 + k < S.lobes ? sg_v : 0.f) : dsel * yk;
+    }
+    if ((int)lane < am.nchunks)
       atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + lane,
                 make_float4(v[0], v[1], v[2], v[3]));
-    }
   }
 }
 
@@ -556,9 +566,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
     R.oinv = make_float3(R.o.x * R.inv.x, R.o.y * R.inv.y, R.o.z * R.inv.z);
     AppMap am;
     if (BWD) {
-      am = app_map(P.S);
       float Y[16];
       sh_basis(P.S.deg, R.d.x, R.d.y, R.d.z, Y);
+      am = app_map(P.S, R.d, Y);
 #pragma unroll
       for (int m = 0; m < 16; ++m)
         if ((int)lane == m) M.Y[m] = Y[m];
@@ -880,14 +890,17 @@ __global__ void __launch_bounds__(256) k_finalize(const float* gbuf, int gstride
   for (int a = 0; a < 3; ++a) put(out.scale, 3 * (size_t)i + a, ds[a]);
   for (int a = 0; a < 4; ++a) put(out.quat, 4 * (size_t)i + a, dq[a]);
   const int nc = (g.sh_degree + 1) * (g.sh_degree + 1);
+  // appearance: SH channel-major [3][ncp], SG component-major [7][gp] (grad_stride)
   const float* ap = row + 16;
-  for (int k = 0; k < 3 * nc; ++k) put(out.sh, (size_t)i * 3 * nc + k, ap[k]);
+  const int ncp = sh_pad(g.sh_degree), gp = sg_pad(g.sg_count);
+  for (int m = 0; m < nc; ++m)
+    for (int ch = 0; ch < 3; ++ch) put(out.sh, ((size_t)i * nc + m) * 3 + ch, ap[ch * ncp + m]);
+  const float* sp = ap + 3 * ncp;
   for (int j = 0; j < g.sg_count; ++j) {
-    const float* v = ap + 3 * nc + 7 * j;
     const size_t ij = (size_t)i * g.sg_count + j;
-    for (int a = 0; a < 3; ++a) put(out.sg_amp, 3 * ij + a, v[a]);
-    put(out.sg_sharp, ij, v[3]);
-    for (int a = 0; a < 3; ++a) put(out.sg_axis, 3 * ij + a, v[4 + a]);
+    for (int a = 0; a < 3; ++a) put(out.sg_amp, 3 * ij + a, sp[a * gp + j]);
+    put(out.sg_sharp, ij, sp[3 * gp + j]);
+    for (int a = 0; a < 3; ++a) put(out.sg_axis, 3 * ij + a, sp[(4 + a) * gp + j]);
   }
   if (bad && stats) atomicAdd(&stats->nonfinite_grads, (unsigned long long)bad);
 }

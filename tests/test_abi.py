@@ -50,7 +50,7 @@ def test_workspace_sizes_and_validation():
     assert L.rg_bvh_workspace_bytes(1000, 3, 7) > 1000 * (64 + 400)
     assert L.rg_bvh_workspace_bytes(-1, 0, 0) == 0
     assert L.rg_bvh_workspace_bytes(10, 4, 0) == 0
-    assert L.rg_backward_workspace_bytes(10, 3, 7) == 10 * 116 * 4
+    assert L.rg_backward_workspace_bytes(10, 3, 7) == 10 * 120 * 4
     # invalid args are rejected before any CUDA call (safe without a GPU)
     g = rg._Gaussians(); g.n = 5; g.sh_degree = 9
     cfg = rg.Config().struct()
