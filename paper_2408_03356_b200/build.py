@@ -19,6 +19,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include")]
+if os.environ.get("RG_MIN_BLOCKS"):
+    FLAGS += [f"-DRG_MIN_BLOCKS={int(os.environ['RG_MIN_BLOCKS'])}"]
 
 
 def _inputs():

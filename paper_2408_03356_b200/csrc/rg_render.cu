@@ -32,6 +32,9 @@ namespace rg {
 
 namespace {
 
+#ifndef RG_MIN_BLOCKS
+#define RG_MIN_BLOCKS 4                // resident blocks per SM the register budget targets
+#endif
 constexpr int kWarps = 4;              // rays (warps) per block
 constexpr int kBlock = 32 * kWarps;
 constexpr int kA = 64;                 // persistent active-list capacity
@@ -77,8 +80,7 @@ struct RenderArgs {
 struct WarpMem {
   float4 e0[kSlots], e1[kSlots], e2[kSlots];
   int stk[kStk];
-  unsigned long long kscr[32];
-  uint32_t pscr[32];
+  uint32_t lq[64];     // fetch: queued leaves awaiting the exact test
   float Y[16];
 };
 struct WarpAcc {
@@ -91,6 +93,11 @@ __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ unsigned long long shfl64(unsigned long long v, int src) {
   const unsigned lo = __shfl_sync(kFull, (unsigned)v, src);
   const unsigned hi = __shfl_sync(kFull, (unsigned)(v >> 32), src);
+  return ((unsigned long long)hi << 32) | lo;
+}
+__device__ __forceinline__ unsigned long long shfl64x(unsigned long long v, int mask) {
+  const unsigned lo = __shfl_xor_sync(kFull, (unsigned)v, mask);
+  const unsigned hi = __shfl_xor_sync(kFull, (unsigned)(v >> 32), mask);
   return ((unsigned long long)hi << 32) | lo;
 }
 
@@ -128,9 +135,64 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
   unsigned long long kth = ~0ull;
   const float slack = 1e-5f * (fabsf(seg_lo) + fabsf(seg_hi)) + 1e-6f;
   const float lo_s = seg_lo - slack, hi_s = seg_hi + slack;
-  int sp = 1;
+  int sp = 1, qn = 0;
   if (lane == 0) M.stk[0] = 0;
   __syncwarp();
+  // Exact leaf tests are batched: box-passing leaves are queued in shared
+  // memory and tested 32 at a time (all lanes busy), then the candidates are
+  // bitonic-sorted and bitonic-merged into the k-buffer.
+  auto flush = [&](int n) {
+    __syncwarp();
+    const uint32_t cp = (int)lane < n ? M.lq[lane] : 0u;
+    bool cand = false;
+    unsigned long long ck = ~0ull;
+    if ((int)lane < n) {
+      const float4* gp = S.geom + 4 * (size_t)cp;
+      const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2), g3 = __ldg(gp + 3);
+      PairGeom pg;
+      if (isect_exact(g0, g1, g2, g3, R.o, R.d, pg) && pg.tx >= seg_lo && pg.te <= seg_hi) {
+        ck = ((unsigned long long)fkey(pg.te) << 32) | (uint32_t)__float_as_int(g3.z);
+        cand = ck > cursor && ck < kth;
+        if (!cand) ck = ~0ull;
+      }
+    }
+    // drop the consumed queue entries
+    const int rem = qn - n;
+    const uint32_t mv = (int)lane < rem ? M.lq[n + lane] : 0u;
+    __syncwarp();
+    if ((int)lane < rem) M.lq[lane] = mv;
+    qn = rem;
+    if (!__ballot_sync(kFull, cand)) return;
+    uint32_t cpos = cp;
+    // bitonic sort of the candidate keys, ascending across lanes
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const unsigned long long ok = shfl64x(ck, j);
+        const uint32_t op = __shfl_xor_sync(kFull, cpos, j);
+        const bool take_min = (((int)lane & j) == 0) == (((int)lane & k) == 0);
+        if (take_min ? (ok < ck) : (ok > ck)) { ck = ok; cpos = op; }
+      }
+    // the 32 smallest of (k-buffer, candidates) form a bitonic sequence: merge
+    {
+      const unsigned long long rk = shfl64(ck, 31 - (int)lane);
+      const uint32_t rp = __shfl_sync(kFull, cpos, 31 - (int)lane);
+      if (rk < key) { key = rk; pos = rp; }
+    }
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+      const unsigned long long ok = shfl64x(key, j);
+      const uint32_t op = __shfl_xor_sync(kFull, pos, j);
+      if ((((int)lane & j) == 0) ? (ok < key) : (ok > key)) { key = ok; pos = op; }
+    }
+    if ((int)lane >= kmax) { key = ~0ull; pos = 0u; }
+    nk = __popc(__ballot_sync(kFull, key != ~0ull));
+    if (nk == kmax) {
+      kth = shfl64(key, kmax - 1);
+      te_lim = fkey_inv((uint32_t)(kth >> 32));
+    }
+  };
   while (sp > 0) {
     const int node = M.stk[sp - 1];
     --sp;
@@ -142,17 +204,13 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
           __ldg(&W.hiy[lane]), __ldg(&W.hiz[lane]), R.inv, R.oinv, tn, tf);
     const bool hit = child != kWideEmpty && tn <= tf && tf >= lo_s && tn <= hi_s &&
                      tn <= te_lim + slack;
-    bool cand = false;
-    unsigned long long ck = ~0ull;
-    uint32_t cp = 0;
-    if (hit && child < 0) {
-      cp = (uint32_t)(~child);
-      const float4* gp = S.geom + 4 * (size_t)cp;
-      const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2), g3 = __ldg(gp + 3);
-      PairGeom pg;
-      if (isect_exact(g0, g1, g2, g3, R.o, R.d, pg) && pg.tx >= seg_lo && pg.te <= seg_hi) {
-        ck = ((unsigned long long)fkey(pg.te) << 32) | (uint32_t)__float_as_int(g3.z);
-        cand = ck > cursor && ck < kth;
+    // queue box-passing leaves
+    {
+      const unsigned lm = __ballot_sync(kFull, hit && child < 0);
+      if (lm) {
+        __syncwarp();
+        if (hit && child < 0) M.lq[qn + __popc(lm & lt_mask)] = (uint32_t)(~child);
+        qn += __popc(lm);
       }
     }
     // internal children: push sorted so that the nearest is on top
@@ -176,35 +234,9 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
       }
       __syncwarp();
     }
-    // leaf candidates: rank-merge into the per-lane sorted k-buffer
-    const unsigned cm = __ballot_sync(kFull, cand);
-    if (cm) {
-      int crank = 0, shift = 0, krank = 0;
-      unsigned mm = cm;
-      while (mm) {
-        const int b = __ffs(mm) - 1;
-        mm &= mm - 1;
-        const unsigned long long kb = shfl64(ck, b);
-        crank += (cand && kb < ck) ? 1 : 0;
-        shift += (kb < key) ? 1 : 0;
-        const unsigned ltm = __ballot_sync(kFull, key < kb);
-        if ((int)lane == b) krank = __popc(ltm);
-      }
-      const int newk = (int)lane + shift, newc = krank + crank;
-      if ((int)lane < nk && newk < kmax) { M.kscr[newk] = key; M.pscr[newk] = pos; }
-      if (cand && newc < kmax) { M.kscr[newc] = ck; M.pscr[newc] = cp; }
-      __syncwarp();
-      nk = min(kmax, nk + __popc(cm));
-      key = ((int)lane < nk) ? M.kscr[lane] : ~0ull;
-      pos = ((int)lane < nk) ? M.pscr[lane] : 0u;
-      __syncwarp();
-      if (nk == kmax) {
-        kth = shfl64(key, kmax - 1);
-        te_lim = fkey_inv((uint32_t)(kth >> 32));
-      }
-    }
-    (void)lt_mask;
+    if (qn >= 32) flush(32);
   }
+  while (qn > 0) flush(min(qn, 32));
   return nk;
 }
 
@@ -522,7 +554,7 @@ __device__ __forceinline__ void dbg_put(const RenderArgs& P, int ray, int& dbg_n
 }
 
 template <bool BWD, int GW>
-__global__ void __launch_bounds__(kBlock, 4) k_render(const RenderArgs P) {
+__global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderArgs P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const unsigned lane = lane_id();
   const int wid = threadIdx.x >> 5;
