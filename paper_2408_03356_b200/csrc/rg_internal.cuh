@@ -33,13 +33,12 @@ __host__ __device__ inline int app_stride(int deg, int lobes) {
 }
 // Morton-ordered gradient row (floats): [0..2] dL/dmu, [3] dL/dsigma~,
 // [4..12] dL/dM, [13..15] pad, then SH grads channel-major [3][ncp]
-// (ncp = (deg+1)^2 rounded up to 4), then SG grads component-major [7][gp]
-// (components k0,k1,k2,lambda,p0,p1,p2; gp = lobes rounded up to 4), so that
-// every float4 of the appearance part is one channel/component x 4 terms.
+// (ncp = (deg+1)^2 rounded up to 4), then SG grads lobe-major [G][8]
+// (k0,k1,k2,lambda | p0,p1,p2,-), so that every float4 of the appearance part
+// is one SH channel x 4 coefficients or one half of one lobe.
 __host__ __device__ inline int sh_pad(int deg) { return (((deg + 1) * (deg + 1)) + 3) & ~3; }
-__host__ __device__ inline int sg_pad(int lobes) { return (lobes + 3) & ~3; }
 __host__ __device__ inline int grad_stride(int deg, int lobes) {
-  return 16 + 3 * sh_pad(deg) + 7 * sg_pad(lobes);
+  return 16 + 3 * sh_pad(deg) + 8 * lobes;
 }
 
 // geometry record, 64 B, Morton order:

@@ -81,6 +81,8 @@ struct WarpMem {
   float4 e0[kSlots], e1[kSlots], e2[kSlots];
   int stk[kStk];
   uint32_t lq[64];     // fetch: queued leaves awaiting the exact test
+  unsigned long long kscr[32];   // fetch: candidate sort scratch
+  uint32_t pscr[32];
   float Y[16];
 };
 struct WarpAcc {
@@ -162,18 +164,25 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
     __syncwarp();
     if ((int)lane < rem) M.lq[lane] = mv;
     qn = rem;
-    if (!__ballot_sync(kFull, cand)) return;
-    uint32_t cpos = cp;
-    // bitonic sort of the candidate keys, ascending across lanes
-#pragma unroll
-    for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        const unsigned long long ok = shfl64x(ck, j);
-        const uint32_t op = __shfl_xor_sync(kFull, cpos, j);
-        const bool take_min = (((int)lane & j) == 0) == (((int)lane & k) == 0);
-        if (take_min ? (ok < ck) : (ok > ck)) { ck = ok; cpos = op; }
+    const unsigned cmask = __ballot_sync(kFull, cand);
+    if (!cmask) return;
+    // sort the candidates by rank (O(#candidates)): place, then read back in order
+    {
+      int crank = 0;
+      unsigned mm = cmask;
+      while (mm) {
+        const int b = __ffs(mm) - 1;
+        mm &= mm - 1;
+        const unsigned long long kb = shfl64(ck, b);
+        crank += (cand && kb < ck) ? 1 : 0;
       }
+      if (cand) { M.kscr[crank] = ck; M.pscr[crank] = cp; }
+      __syncwarp();
+      const int ncand = __popc(cmask);
+      ck = (int)lane < ncand ? M.kscr[lane] : ~0ull;
+    }
+    uint32_t cpos = M.pscr[lane];
+    __syncwarp();
     // the 32 smallest of (k-buffer, candidates) form a bitonic sequence: merge
     {
       const unsigned long long rk = shfl64(ck, 31 - (int)lane);
@@ -382,23 +391,22 @@ __device__ __forceinline__ void grad_range(const WarpMem& M, WarpAcc& A, int e0,
 // Per-lane map of the appearance part of a gradient row (rg_internal.cuh
 // grad_stride): lane c owns float4 chunk 4 + c.  SH chunks: channel `ch`,
 // coefficients 4q..4q+3 (their Y(d) values precomputed per ray in y);
-// SG chunks: component `comp`, lobes 4h..4h+3.
+// SG chunks: lobe `lobe`, half 0 = (k0, k1, k2, lambda), half 1 = (p0, p1, p2, -).
 struct AppMap {
   float4 y;          // SH: Y(d) of the lane's 4 coefficients (0 past nc)
-  int ch;            // SH channel, or SG component (0..6); -1: no chunk
-  int sg;            // 1 if an SG chunk
-  int h4;            // SG: first lobe of the chunk
-  float dcomp;       // SG components 4..6: d[comp - 4]
+  int ch;            // SH channel (0..2), -1 otherwise
+  int lobe;          // SG lobe, -1 otherwise
+  int half;          // SG half
   int nchunks;
 };
-__device__ __forceinline__ AppMap app_map(const SceneView& S, const float3& d, const float* Y) {
+__device__ __forceinline__ AppMap app_map(const SceneView& S, const float* Y) {
   AppMap m;
   const int c = (int)lane_id();
   const int nc = (S.deg + 1) * (S.deg + 1);
-  const int qsh = sh_pad(S.deg) / 4, qsg = sg_pad(S.lobes) / 4;
-  m.nchunks = 3 * qsh + 7 * qsg;
+  const int qsh = sh_pad(S.deg) / 4;
+  m.nchunks = 3 * qsh + 2 * S.lobes;
   m.y = make_float4(0.f, 0.f, 0.f, 0.f);
-  m.ch = -1; m.sg = 0; m.h4 = 0; m.dcomp = 0.f;
+  m.ch = -1; m.lobe = -1; m.half = 0;
   if (c < 3 * qsh) {
     m.ch = c / qsh;
     const int q = c % qsh;
@@ -407,11 +415,8 @@ __device__ __forceinline__ AppMap app_map(const SceneView& S, const float3& d, c
     m.y.z = 4 * q + 2 < nc ? Y[4 * q + 2] : 0.f;
     m.y.w = 4 * q + 3 < nc ? Y[4 * q + 3] : 0.f;
   } else if (c < m.nchunks) {
-    const int cc = c - 3 * qsh;
-    m.sg = 1;
-    m.ch = cc / qsg;
-    m.h4 = 4 * (cc % qsg);
-    m.dcomp = m.ch == 4 ? d.x : (m.ch == 5 ? d.y : d.z);
+    m.lobe = (c - 3 * qsh) >> 1;
+    m.half = (c - 3 * qsh) & 1;
   }
   return m;
 }
@@ -486,31 +491,25 @@ __device__ __noinline__ void scatter_batch(const SceneView& S, const WarpMem& M,
     const float2 acb = A.b[e];
     const float d0 = acc.w, d1 = acb.x, d2 = acb.y;
     const int pos = __float_as_int(M.e2[e].y);
-    // per-lobe terms, lane j < lobes: e_j = exp(lambda (d.p - 1)), kd = <dc, k> e_j
-    float ej = 0.f, kd = 0.f, dpm = 0.f, lam = 0.f;
-    if ((int)lane < S.lobes) {
-      const float* q = S.app + (size_t)pos * S.app_stride + 3 * nc + 7 * lane;
-      lam = __ldg(q + 3);
-      dpm = R.d.x * __ldg(q + 4) + R.d.y * __ldg(q + 5) + R.d.z * __ldg(q + 6) - 1.0f;
-      ej = ex2_approx(lam * dpm * kLog2e);
-      kd = (d0 * __ldg(q) + d1 * __ldg(q + 1) + d2 * __ldg(q + 2)) * ej;
-    }
-    float v[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int src = (am.h4 + k) & 31;
-      const float e_k = __shfl_sync(kFull, ej, src);
-      const float kd_k = __shfl_sync(kFull, kd, src);
-      const float dpm_k = __shfl_sync(kFull, dpm, src);
-      const float lam_k = __shfl_sync(kFull, lam, src);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (am.ch >= 0) {            // SH: dc[ch] * Y(d) of 4 coefficients
       const float dsel = am.ch == 0 ? d0 : (am.ch == 1 ? d1 : d2);
-      const float yk = k == 0 ? am.y.x : (k == 1 ? am.y.y : (k == 2 ? am.y.z : am.y.w));
-      const float sg_v = am.ch < 3 ? dsel * e_k : (am.ch == 3 ? kd_k * dpm_k : kd_k * lam_k * am.dcomp);
-      v[k] = am.sg ? (am.h4 + k < S.lobes ? sg_v : 0.f) : dsel * yk;
+      v = make_float4(dsel * am.y.x, dsel * am.y.y, dsel * am.y.z, dsel * am.y.w);
+    } else if (am.lobe >= 0) {   // SG lobe j: e = exp(lambda (d.p - 1)), kd = <dc, k> e
+      const float* q = S.app + (size_t)pos * S.app_stride + 3 * nc + 7 * am.lobe;
+      const float lam = __ldg(q + 3);
+      const float dpm = R.d.x * __ldg(q + 4) + R.d.y * __ldg(q + 5) + R.d.z * __ldg(q + 6) - 1.0f;
+      const float ej = ex2_approx(lam * dpm * kLog2e);
+      if (am.half == 0) {
+        const float kd = (d0 * __ldg(q) + d1 * __ldg(q + 1) + d2 * __ldg(q + 2)) * ej;
+        v = make_float4(d0 * ej, d1 * ej, d2 * ej, kd * dpm);
+      } else {
+        const float kdl = (d0 * __ldg(q) + d1 * __ldg(q + 1) + d2 * __ldg(q + 2)) * ej * lam;
+        v = make_float4(kdl * R.d.x, kdl * R.d.y, kdl * R.d.z, 0.f);
+      }
     }
     if ((int)lane < am.nchunks)
-      atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + lane,
-                make_float4(v[0], v[1], v[2], v[3]));
+      atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + lane, v);
   }
 }
 
@@ -600,7 +599,7 @@ __global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderAr
     if (BWD) {
       float Y[16];
       sh_basis(P.S.deg, R.d.x, R.d.y, R.d.z, Y);
-      am = app_map(P.S, R.d, Y);
+      am = app_map(P.S, Y);
 #pragma unroll
       for (int m = 0; m < 16; ++m)
         if ((int)lane == m) M.Y[m] = Y[m];
@@ -924,15 +923,15 @@ __global__ void __launch_bounds__(256) k_finalize(const float* gbuf, int gstride
   const int nc = (g.sh_degree + 1) * (g.sh_degree + 1);
   // appearance: SH channel-major [3][ncp], SG component-major [7][gp] (grad_stride)
   const float* ap = row + 16;
-  const int ncp = sh_pad(g.sh_degree), gp = sg_pad(g.sg_count);
+  const int ncp = sh_pad(g.sh_degree);
   for (int m = 0; m < nc; ++m)
     for (int ch = 0; ch < 3; ++ch) put(out.sh, ((size_t)i * nc + m) * 3 + ch, ap[ch * ncp + m]);
-  const float* sp = ap + 3 * ncp;
+  const float* sp = ap + 3 * ncp;   // lobe-major [G][8]: k0 k1 k2 lambda p0 p1 p2 -
   for (int j = 0; j < g.sg_count; ++j) {
     const size_t ij = (size_t)i * g.sg_count + j;
-    for (int a = 0; a < 3; ++a) put(out.sg_amp, 3 * ij + a, sp[a * gp + j]);
-    put(out.sg_sharp, ij, sp[3 * gp + j]);
-    for (int a = 0; a < 3; ++a) put(out.sg_axis, 3 * ij + a, sp[(4 + a) * gp + j]);
+    for (int a = 0; a < 3; ++a) put(out.sg_amp, 3 * ij + a, sp[8 * j + a]);
+    put(out.sg_sharp, ij, sp[8 * j + 3]);
+    for (int a = 0; a < 3; ++a) put(out.sg_axis, 3 * ij + a, sp[8 * j + 4 + a]);
   }
   if (bad && stats) atomicAdd(&stats->nonfinite_grads, (unsigned long long)bad);
 }

@@ -2,13 +2,27 @@
 usage: ncu_regions.py report kernel-substring"""
 import collections, csv, re, subprocess, sys
 rep, ksub = sys.argv[1], sys.argv[2]
-REG = [("rg_render.cu", 114, 206, "fetch"), ("rg_render.cu", 207, 260, "setup_pair+color"),
-       ("rg_render.cu", 267, 299, "eval_range"), ("rg_render.cu", 300, 340, "grad_range"),
-       ("rg_render.cu", 341, 471, "scatter"), ("rg_render.cu", 576, 612, "expire"),
-       ("rg_render.cu", 613, 640, "refill"), ("rg_render.cu", 641, 692, "slab+eval loop"),
-       ("rg_render.cu", 693, 760, "composite"), ("rg_render.cu", 761, 790, "bwd tail"),
-       ("rg_render.cu", 512, 575, "ray setup"), ("rg_internal.cuh", 120, 150, "isect_exact"),
-       ("rg_internal.cuh", 150, 170, "offset_at"), ("rg_render.cu", 94, 113, "box_t")]
+import os
+CSRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                    "paper_2408_03356_b200", "csrc")
+def auto_regions():
+    """function definitions and '// ---- label' markers delimit regions"""
+    reg = []
+    for fn in ("rg_render.cu", "rg_internal.cuh"):
+        lines = open(os.path.join(CSRC, fn)).read().splitlines()
+        marks = []
+        for i, l in enumerate(lines, 1):
+            m = re.match(r"^(?:template.*\n)?__(?:device|global)__.*?\b(\w+)\s*\(", l)
+            if m and not l.strip().endswith(";"):
+                marks.append((i, m.group(1)))
+            m2 = re.match(r"^\s*// ---- (\w[\w ]*)", l)
+            if m2:
+                marks.append((i, "k:" + m2.group(1)[:20]))
+        for k, (a, name) in enumerate(marks):
+            b = marks[k + 1][0] - 1 if k + 1 < len(marks) else len(lines)
+            reg.append((fn, a, b, name))
+    return reg
+REG = auto_regions()
 def page(view):
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", view],
                          capture_output=True, text=True).stdout
