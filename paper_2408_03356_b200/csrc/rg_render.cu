@@ -88,6 +88,8 @@ struct WarpMem {
 struct WarpAcc {
   float4 a[kSlots];    // Sw, Sw1, Sw2, dc_r
   float2 b[kSlots];    // dc_g, dc_b
+  float4 s0[8], s1[8]; // per-sample backward values of the current group: {tk, dls, dc0, dc1},
+                       // {dc2, gc, inv, live}
 };
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
@@ -340,43 +342,39 @@ struct SampleGrad {   // per-sample backward quantities (lanes of sample j)
   float dls, dc0, dc1, dc2, gc, inv;
 };
 
-// accumulate the per-pair moments of slots [e0, e1) for this group's samples
+// accumulate the per-pair moments of slots [e0, e1) over this group's samples:
+// lane = slot, loop over the GW samples whose backward values the composite
+// step left in A.s0/A.s1 (broadcast reads), moments kept in registers.
 template <int GW>
-__device__ __forceinline__ void grad_range(const WarpMem& M, WarpAcc& A, int e0, int e1,
-                                           const Lanes<GW>& L, float tk, bool live,
-                                           const SampleGrad& H) {
-  constexpr int ER = Lanes<GW>::ER;
-  const int rounds = (e1 - e0 + ER - 1) / ER;
-  for (int rr = 0; rr < rounds; ++rr) {
-    const int e = e0 + L.esub + rr * ER;
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
-    if (e < e1 && live) {
+__device__ __forceinline__ void grad_range(const WarpMem& M, WarpAcc& A, int e0, int e1) {
+  __syncwarp();
+  for (int base = e0; base < e1; base += 32) {
+    const int e = base + (int)lane_id();
+    if (e < e1) {
       const float4 a = M.e0[e];
-      if (a.x <= tk && tk <= a.y) {
-        const float4 q = M.e1[e];
-        const float cb = M.e2[e].x;
-        const float tau = tk - a.z;
-        const float w = ex2_approx(fmaf(tau, fmaf(q.y, tau, q.x), a.w));
-        const float dldw = H.dls + (H.dc0 * q.z + H.dc1 * q.w + H.dc2 * cb - H.gc) * H.inv;
-        const float wd = w * dldw, wi = w * H.inv;
-        a0 = wd;
-        a1 = wd * tau;
-        a2 = wd * tau * tau;
-        a3 = wi * H.dc0;
-        a4 = wi * H.dc1;
-        a5 = wi * H.dc2;
-      }
-    }
+      const float4 q = M.e1[e];
+      const float cb = M.e2[e].x;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
 #pragma unroll
-    for (int off = 1; off < GW; off <<= 1) {
-      a0 += __shfl_xor_sync(kFull, a0, off);
-      a1 += __shfl_xor_sync(kFull, a1, off);
-      a2 += __shfl_xor_sync(kFull, a2, off);
-      a3 += __shfl_xor_sync(kFull, a3, off);
-      a4 += __shfl_xor_sync(kFull, a4, off);
-      a5 += __shfl_xor_sync(kFull, a5, off);
-    }
-    if (L.j == 0 && e < e1) {
+      for (int j = 0; j < GW; ++j) {
+        const float4 s0 = A.s0[j];
+        const float tk = s0.x;
+        if (a.x <= tk && tk <= a.y) {
+          const float4 s1 = A.s1[j];
+          if (s1.w != 0.f) {
+            const float tau = tk - a.z;
+            const float w = ex2_approx(fmaf(tau, fmaf(q.y, tau, q.x), a.w));
+            const float dldw = s0.y + (s0.z * q.z + s0.w * q.w + s1.x * cb - s1.y) * s1.z;
+            const float wd = w * dldw, wi = w * s1.z;
+            a0 += wd;
+            a1 = fmaf(wd, tau, a1);
+            a2 = fmaf(wd * tau, tau, a2);
+            a3 = fmaf(wi, s0.z, a3);
+            a4 = fmaf(wi, s0.w, a4);
+            a5 = fmaf(wi, s1.x, a5);
+          }
+        }
+      }
       float4 v = A.a[e];
       float2 w = A.b[e];
       v.x += a0; v.y += a1; v.z += a2; v.w += a3;
@@ -798,15 +796,22 @@ __global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderAr
           const float v2 = __shfl_up_sync(kFull, p2, dd, GW);
           if (L.j >= dd) { p0 += v0; p1 += v1; p2 += v2; }
         }
-        SampleGrad H = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (BWD && live) {
-          const float Ta = Tb * e_s;
-          H.dc0 = gr0 * wgt; H.dc1 = gr1 * wgt; H.dc2 = gr2 * wgt;
-          const float gcj = gr0 * cr + gr1 * cg + gr2 * cb;
-          const float gS = gr0 * (Pp0 - (C0 + p0)) + gr1 * (Pp1 - (C1 + p1)) + gr2 * (Pp2 - (C2 + p2));
-          H.dls = c.dt * (Ta * gcj - gS);
-          H.gc = H.dc0 * cr + H.dc1 * cg + H.dc2 * cb;
-          H.inv = inv_s;
+        if (BWD) {   // per-sample dL/dsigma_k, dL/dc_k for the gradient pass
+          SampleGrad H = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          if (live) {
+            const float Ta = Tb * e_s;
+            H.dc0 = gr0 * wgt; H.dc1 = gr1 * wgt; H.dc2 = gr2 * wgt;
+            const float gcj = gr0 * cr + gr1 * cg + gr2 * cb;
+            const float gS =
+                gr0 * (Pp0 - (C0 + p0)) + gr1 * (Pp1 - (C1 + p1)) + gr2 * (Pp2 - (C2 + p2));
+            H.dls = c.dt * (Ta * gcj - gS);
+            H.gc = H.dc0 * cr + H.dc1 * cg + H.dc2 * cb;
+            H.inv = inv_s;
+          }
+          if (L.esub == 0) {
+            A.s0[L.j] = make_float4(tk, H.dls, H.dc0, H.dc1);
+            A.s1[L.j] = make_float4(H.dc2, H.gc, H.inv, live ? 1.f : 0.f);
+          }
         }
         const float tot_x = __shfl_sync(kFull, incl, GW - 1, GW);
         const float t0c = __shfl_sync(kFull, p0, GW - 1, GW);
@@ -820,7 +825,7 @@ __global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderAr
         const unsigned smask = __ballot_sync(kFull, live && L.esub == 0);
         if (lane == 0) cnt.samples += __popc(smask);
         if (BWD) {
-          grad_range<GW>(M, A, 0, n_use, L, tk, live, H);
+          grad_range<GW>(M, A, 0, n_use);
           if (more) {
             unsigned long long cur2 = cursor;
             int remaining = K - n_use;
@@ -835,7 +840,7 @@ __global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderAr
                 A.b[kA + lane] = make_float2(0.f, 0.f);
               }
               __syncwarp();
-              grad_range<GW>(M, A, kA, kA + got, L, tk, live, H);
+              grad_range<GW>(M, A, kA, kA + got);
               scatter_batch(P.S, M, A, kA, got >= 32 ? kFull : ((1u << got) - 1u), R, am, P.gbuf,
                             P.gstride);
               remaining -= got;
