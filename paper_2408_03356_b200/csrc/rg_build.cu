@@ -256,18 +256,33 @@ __global__ void __launch_bounds__(kThreads) k_pack(rg_gaussians g, rg_config c,
   gp[2] = make_float4(M[4], M[5], M[6], M[7]);
   gp[3] = make_float4(M[8], r2, __int_as_float(i), 0.0f);
   for (int k = 0; k < 6; ++k) leaf_box[6 * (size_t)p + k] = box_orig[6 * (size_t)i + k];
-  // appearance: SH [(deg+1)^2 x 3], then per lobe (k0,k1,k2, lambda, p0,p1,p2)
-  const int nc = (g.sh_degree + 1) * (g.sh_degree + 1);
-  float* ap = app + (size_t)p * stride;
-  for (int k = 0; k < 3 * nc; ++k) ap[k] = g.sh[(size_t)i * 3 * nc + k];
-  for (int j = 0; j < g.sg_count; ++j) {
-    const size_t ij = (size_t)i * g.sg_count + j;
-    float* dst = ap + 3 * nc + 7 * j;
-    dst[0] = g.sg_amp[3 * ij]; dst[1] = g.sg_amp[3 * ij + 1]; dst[2] = g.sg_amp[3 * ij + 2];
-    dst[3] = g.sg_sharp[ij];
-    dst[4] = g.sg_axis[3 * ij]; dst[5] = g.sg_axis[3 * ij + 1]; dst[6] = g.sg_axis[3 * ij + 2];
+  (void)app;
+  (void)stride;
+}
+
+// appearance record in Morton order, one warp per Gaussian row (coalesced):
+// SH [(deg+1)^2 x 3], then per lobe (k0,k1,k2, lambda, p0,p1,p2), zero pad.
+__global__ void __launch_bounds__(kThreads) k_pack_app(rg_gaussians g, const uint32_t* order,
+                                                       float* app, int stride) {
+  const int lane = threadIdx.x & 31;
+  const int nc3 = 3 * (g.sh_degree + 1) * (g.sh_degree + 1);
+  const int G = g.sg_count;
+  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < g.n;
+       p += (gridDim.x * blockDim.x) >> 5) {
+    const size_t i = order[p];
+    float* ap = app + (size_t)p * stride;
+    for (int f = lane; f < stride; f += 32) {
+      float v = 0.0f;
+      if (f < nc3) {
+        v = g.sh[i * nc3 + f];
+      } else if (f < nc3 + 7 * G) {
+        const int j = (f - nc3) / 7, r = (f - nc3) - 7 * j;
+        const size_t ij = i * G + j;
+        v = r < 3 ? g.sg_amp[3 * ij + r] : (r == 3 ? g.sg_sharp[ij] : g.sg_axis[3 * ij + r - 4]);
+      }
+      ap[f] = v;
+    }
   }
-  for (int k = 3 * nc + 7 * g.sg_count; k < stride; ++k) ap[k] = 0.0f;
 }
 
 // --- Karras 2012 ---------------------------------------------------------------
@@ -361,7 +376,15 @@ __device__ __forceinline__ float box_area(const float* b) {
 __global__ void k_collapse_init(int n, const float* leaf_box, WideNode* wide, int2* wq,
                                 int* counts) {
   const int l = threadIdx.x;
-  if (l < 4) counts[l] = 0;
+  if (l == 0) {
+    // [0] wide nodes allocated, [1] head, [2] done, [3] error, [4] reserved
+    for (int k = 0; k < 8; ++k) counts[k] = 0;
+    counts[0] = 1;
+    if (n > 1) {
+      wq[0] = make_int2(0, 0);   // binary root -> wide node 0
+      counts[4] = 1;
+    }
+  }
   if (n == 1) {
     wide[0].lox[l] = l == 0 ? leaf_box[0] : INFINITY;
     wide[0].loy[l] = l == 0 ? leaf_box[1] : INFINITY;
@@ -370,20 +393,38 @@ __global__ void k_collapse_init(int n, const float* leaf_box, WideNode* wide, in
     wide[0].hiy[l] = l == 0 ? leaf_box[4] : -INFINITY;
     wide[0].hiz[l] = l == 0 ? leaf_box[5] : -INFINITY;
     wide[0].child[l] = l == 0 ? ~0 : kWideEmpty;
-    if (l == 0) counts[0] = 1;
-  } else if (l == 0) {
-    wq[0] = make_int2(0, 0);   // binary root -> wide node 0
-    counts[0] = 1;             // wide nodes allocated
-    counts[1] = 1;             // items in the current queue
   }
 }
 
-__global__ void __launch_bounds__(128) k_collapse(const float4* nodes, const float* leaf_box,
-                                                  WideNode* wide, const int2* qin, int2* qout,
-                                                  int* counts, int in_slot, int out_slot) {
-  const int nin = counts[in_slot];
-  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < nin; it += gridDim.x * blockDim.x) {
-    const int2 job = qin[it];
+// One persistent launch over a device work queue of (binary id, wide id)
+// items.  counts: [0] wide nodes allocated, [1] head (claims), [2] items done,
+// [3] error flag, [4] items reserved.  The queue is pre-filled with -1; an
+// item is written with one 8-byte store after its slot is reserved.  A thread
+// whose claimed slot is not reserved exits once done == reserved is observed
+// (done read before reserved): every reserved item is then finished, so no
+// further item can appear.
+__global__ void __launch_bounds__(128) k_collapse_persistent(const float4* nodes, WideNode* wide,
+                                                             int2* q, int* counts) {
+  volatile int* vc = counts;
+  volatile long long* vq = reinterpret_cast<volatile long long*>(q);
+  while (true) {
+    const int it = atomicAdd(counts + 1, 1);
+    bool have = false;
+    long long raw = -1;
+    while (true) {
+      const int done = vc[2];
+      __threadfence();
+      const int res = vc[4];
+      if (it < res) {
+        raw = vq[it];
+        if ((int)(raw & 0xFFFFFFFF) != -1) { have = true; break; }
+      } else if (done == res) {
+        break;
+      }
+      __nanosleep(64);
+    }
+    if (!have) return;
+    const int2 job = make_int2((int)(raw & 0xFFFFFFFF), (int)(raw >> 32));
     int ids[kWide];
     float bx[kWide][6];
     int m = 0;
@@ -412,14 +453,18 @@ __global__ void __launch_bounds__(128) k_collapse(const float4* nodes, const flo
       for (int k = 0; k < 6; ++k) bx[m][k] = w[6 + k];
       ++m;
     }
+    int nint = 0;
+    for (int k = 0; k < m; ++k) nint += ids[k] >= 0;
+    const int wid0 = nint ? atomicAdd(counts + 0, nint) : 0;
+    int slot = 0;
     WideNode& W = wide[job.y];
     for (int k = 0; k < kWide; ++k) {
       if (k < m) {
         int child = ids[k];
         if (child >= 0) {
-          const int wid = atomicAdd(counts + 0, 1);
-          const int slot = atomicAdd(counts + out_slot, 1);
-          qout[slot] = make_int2(child, wid);
+          const int wid = wid0 + slot++;
+          const int qs = atomicAdd(counts + 4, 1);               // reserve a queue slot
+          vq[qs] = ((long long)wid << 32) | (unsigned)child;     // publish with one store
           child = wid;
         }
         W.lox[k] = bx[k][0]; W.loy[k] = bx[k][1]; W.loz[k] = bx[k][2];
@@ -431,14 +476,15 @@ __global__ void __launch_bounds__(128) k_collapse(const float4* nodes, const flo
         W.child[k] = kWideEmpty;
       }
     }
+    __threadfence();
+    atomicAdd(counts + 2, 1);                // this item is done
   }
 }
 
-__global__ void k_collapse_next(int* counts, int in_slot) {
-  counts[in_slot] = 0;   // the consumed queue becomes the next output queue
+// error flag: unfinished items or wide-node capacity exceeded
+__global__ void k_collapse_check(int* counts, int capacity) {
+  counts[3] = (counts[2] != counts[4] || counts[0] > capacity) ? 1 : 0;
 }
-
-__global__ void k_collapse_check(int* counts, int last_out) { counts[3] = counts[last_out]; }
 
 inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -471,7 +517,7 @@ BvhLayout bvh_layout(int n, int deg, int lobes) {
   L.wide = take(sizeof(WideNode) * wide_capacity(n));
   L.wq_a = take(8 * nn);
   L.wq_b = take(8 * nn);
-  L.wcounts = take(16);
+  L.wcounts = take(32);
   L.total = o;
   return L;
 }
@@ -484,7 +530,7 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
   k_init<<<1, 32, 0, st>>>(bounds, root_box);
   count_launches(1);
   if (n == 0) return cudaGetLastError();
-  count_launches(n > 1 ? 17 : 16);
+  count_launches(n > 1 ? 18 : 17);
   const int blocks = (n + kThreads - 1) / kThreads;
   float* box_orig = reinterpret_cast<float*>(ws + L.box_orig);
   int* flags = reinterpret_cast<int*>(ws + L.flags);
@@ -510,6 +556,11 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
   float* leaf_box = reinterpret_cast<float*>(ws + L.leaf_box);
   k_pack<<<blocks, kThreads, 0, st>>>(g, c, va, box_orig, flags, geom, app,
                                       app_stride(g.sh_degree, g.sg_count), leaf_box);
+  {
+    const int warps_needed = n, per_block = kThreads / 32;
+    const int ablocks = min((warps_needed + per_block - 1) / per_block, 148 * 16);
+    k_pack_app<<<ablocks, kThreads, 0, st>>>(g, va, app, app_stride(g.sh_degree, g.sg_count));
+  }
   float4* nodes = reinterpret_cast<float4*>(ws + L.nodes);
   int* parent_int = reinterpret_cast<int*>(ws + L.parent_int);
   int* parent_leaf = reinterpret_cast<int*>(ws + L.parent_leaf);
@@ -523,20 +574,18 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
   // 32-wide collapse (level-synchronous; queue slots 1/2 alternate)
   WideNode* wide = reinterpret_cast<WideNode*>(ws + L.wide);
   int2* qa = reinterpret_cast<int2*>(ws + L.wq_a);
-  int2* qb = reinterpret_cast<int2*>(ws + L.wq_b);
   int* wc = reinterpret_cast<int*>(ws + L.wcounts);
+  if (n > 1) cudaMemsetAsync(qa, 0xFF, 8 * (size_t)n, st);
   k_collapse_init<<<1, 32, 0, st>>>(n, leaf_box, wide, qa, wc);
   count_launches(1);
   if (n > 1) {
-    const int grid = 148 * 4;
-    for (int r = 0; r < kCollapseRounds; ++r) {
-      const int in_slot = 1 + (r & 1), out_slot = 2 - (r & 1);
-      k_collapse<<<grid, 128, 0, st>>>(nodes, leaf_box, wide, (r & 1) ? qb : qa,
-                                       (r & 1) ? qa : qb, wc, in_slot, out_slot);
-      k_collapse_next<<<1, 1, 0, st>>>(wc, in_slot);
-    }
-    k_collapse_check<<<1, 1, 0, st>>>(wc, 2 - ((kCollapseRounds - 1) & 1));
-    count_launches(2 * kCollapseRounds + 1);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // all blocks co-resident (waiting threads spin): 2 blocks of 128 per SM
+    k_collapse_persistent<<<2 * sms, 128, 0, st>>>(nodes, wide, qa, wc);
+    k_collapse_check<<<1, 1, 0, st>>>(wc, (int)wide_capacity(n));
+    count_launches(2);
   }
   return cudaGetLastError();
 }

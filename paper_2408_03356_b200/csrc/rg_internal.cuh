@@ -236,7 +236,6 @@ struct BvhLayout {
       wcounts, total;
   int tiles;
 };
-constexpr int kCollapseRounds = 40;
 BvhLayout bvh_layout(int n, int deg, int lobes);
 cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, const BvhLayout& L,
                          cudaStream_t st);

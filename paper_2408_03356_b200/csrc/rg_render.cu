@@ -925,20 +925,41 @@ __global__ void __launch_bounds__(256) k_finalize(const float* gbuf, int gstride
   put(out.density, i, row[3]);
   for (int a = 0; a < 3; ++a) put(out.scale, 3 * (size_t)i + a, ds[a]);
   for (int a = 0; a < 4; ++a) put(out.quat, 4 * (size_t)i + a, dq[a]);
-  const int nc = (g.sh_degree + 1) * (g.sh_degree + 1);
-  // appearance: SH channel-major [3][ncp], SG component-major [7][gp] (grad_stride)
-  const float* ap = row + 16;
-  const int ncp = sh_pad(g.sh_degree);
-  for (int m = 0; m < nc; ++m)
-    for (int ch = 0; ch < 3; ++ch) put(out.sh, ((size_t)i * nc + m) * 3 + ch, ap[ch * ncp + m]);
-  const float* sp = ap + 3 * ncp;   // lobe-major [G][8]: k0 k1 k2 lambda p0 p1 p2 -
-  for (int j = 0; j < g.sg_count; ++j) {
-    const size_t ij = (size_t)i * g.sg_count + j;
-    for (int a = 0; a < 3; ++a) put(out.sg_amp, 3 * ij + a, sp[8 * j + a]);
-    put(out.sg_sharp, ij, sp[8 * j + 3]);
-    for (int a = 0; a < 3; ++a) put(out.sg_axis, 3 * ij + a, sp[8 * j + 4 + a]);
-  }
   if (bad && stats) atomicAdd(&stats->nonfinite_grads, (unsigned long long)bad);
+}
+
+// appearance part of the rows, one warp per Gaussian, coalesced on the caller
+// layout: SH grads from channel-major [3][ncp], SG from lobe-major [G][8]
+__global__ void __launch_bounds__(256) k_finalize_app(const float* gbuf, int gstride,
+                                                      const uint32_t* order, rg_gaussians g,
+                                                      rg_gaussian_grads out, rg_stats* stats) {
+  const int lane = threadIdx.x & 31;
+  const int nc = (g.sh_degree + 1) * (g.sh_degree + 1), nc3 = 3 * nc;
+  const int ncp = sh_pad(g.sh_degree), G = g.sg_count;
+  uint32_t bad = 0;
+  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < g.n;
+       p += (gridDim.x * blockDim.x) >> 5) {
+    const size_t i = order[p];
+    const float* ap = gbuf + (size_t)p * gstride + 16;
+    for (int f = lane; f < nc3 + 7 * G; f += 32) {
+      if (f < nc3) {
+        const int m = f / 3, ch = f - 3 * m;
+        const float v = ap[ch * ncp + m];
+        bad += !isfinite(v);
+        if (out.sh) out.sh[i * nc3 + f] += v;
+      } else {
+        const int j = (f - nc3) / 7, r = (f - nc3) - 7 * j;
+        const float v = ap[3 * ncp + 8 * j + r];
+        bad += !isfinite(v);
+        const size_t ij = i * G + j;
+        if (r < 3) { if (out.sg_amp) out.sg_amp[3 * ij + r] += v; }
+        else if (r == 3) { if (out.sg_sharp) out.sg_sharp[ij] += v; }
+        else if (out.sg_axis) out.sg_axis[3 * ij + r - 4] += v;
+      }
+    }
+  }
+  bad = __reduce_add_sync(0xffffffffu, bad);
+  if (bad && lane == 0 && stats) atomicAdd(&stats->nonfinite_grads, (unsigned long long)bad);
 }
 
 __global__ void k_camera_rays(const rg_camera cam, float* o, float* d) {
@@ -1058,7 +1079,9 @@ cudaError_t launch_backward(const rg_gaussians& g, const rg_bvh& b, const rg_con
   if (A.n_rays > 0) { launch_render<true>(A, grid, kSmemBwd, st); count_launches(1); }
   if (b.n > 0) {
     k_finalize<<<(b.n + 255) / 256, 256, 0, st>>>(gbuf, gs, b.order, g, grads, stats);
-    count_launches(1);
+    const int ablocks = (int)std::min<long long>(((long long)b.n + 7) / 8, 148 * 16);
+    k_finalize_app<<<ablocks, 256, 0, st>>>(gbuf, gs, b.order, g, grads, stats);
+    count_launches(2);
   }
   return cudaGetLastError();
 }
