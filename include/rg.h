@@ -157,19 +157,24 @@ rg_status rg_camera_rays(const rg_camera* cam, float* origin, float* dir, void* 
      T   [R]    = final transmittance,
      replay [R] = index of the slab after which the ray terminated early
                   (T <= t_eps), or -1; consumed by rg_render_backward.
-   fetch_log: optional device [R, log_words] int32 (training): the forward records
-   each ray's BVH query results so that rg_render_backward can replay the march
-   without traversing (a ray whose record does not fit is marked and traversed
-   again by the backward).  log_words >= 2 when fetch_log != NULL.
+   fetch_log: optional device buffer of log_bytes bytes (training), at least
+   rg_fetch_log_bytes(R, 0): the forward records each ray's BVH query results
+   and set-up pair data so that rg_render_backward can replay the march without
+   traversing or re-evaluating colours.  A ray whose record does not fit is
+   marked and recomputed by the backward (results are identical either way).
    stats: optional device rg_stats.  debug: if debug_records != NULL, the first
    debug_rays rays append up to debug_cap (slab, caller index) pairs per ray of
    their integrated per-slab hit sets (in order) to debug_records
    [debug_rays, debug_cap, 2] and their record count to debug_counts. */
 rg_status rg_render_forward(const rg_gaussians* g, const rg_bvh* bvh, const rg_config* cfg,
                             const rg_rays* rays, const rg_camera* cam, float* rgb, float* T,
-                            int32_t* replay, int32_t* fetch_log, int32_t log_words,
+                            int32_t* replay, void* fetch_log, size_t log_bytes,
                             rg_stats* stats, int32_t debug_rays, int32_t debug_cap,
                             int32_t* debug_counts, int32_t* debug_records, void* stream);
+
+/* Bytes of a fetch log for n_rays rays with room for pairs_per_ray set-up
+   pairs per ray on average (pairs_per_ray <= 0: a default of 48). */
+size_t rg_fetch_log_bytes(int32_t n_rays, int32_t pairs_per_ray);
 
 /* ---- backward (a11-a12) ------------------------------------------------- */
 /* Workspace for rg_render_backward: the Morton-ordered gradient accumulator. */
@@ -182,8 +187,8 @@ size_t rg_backward_workspace_bytes(int32_t n, int32_t sh_degree, int32_t sg_coun
    `grads` (caller order).  Non-finite gradient values are counted in stats. */
 rg_status rg_render_backward(const rg_gaussians* g, const rg_bvh* bvh, const rg_config* cfg,
                              const rg_rays* rays, const rg_camera* cam, const float* rgb,
-                             const float* T, const int32_t* replay, const int32_t* fetch_log,
-                             int32_t log_words, const float* d_rgb,
+                             const float* T, const int32_t* replay, const void* fetch_log,
+                             size_t log_bytes, const float* d_rgb,
                              const rg_gaussian_grads* grads, rg_stats* stats, void* ws,
                              size_t ws_bytes, void* stream);
 

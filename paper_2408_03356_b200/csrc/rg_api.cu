@@ -123,7 +123,7 @@ rg_status rg_camera_rays(const rg_camera* cam, float* origin, float* dir, void* 
 
 rg_status rg_render_forward(const rg_gaussians* g, const rg_bvh* bvh, const rg_config* cfg,
                             const rg_rays* rays, const rg_camera* cam, float* rgb, float* T,
-                            int32_t* replay, int32_t* fetch_log, int32_t log_words,
+                            int32_t* replay, void* fetch_log, size_t log_bytes,
                             rg_stats* stats, int32_t debug_rays, int32_t debug_cap,
                             int32_t* debug_counts, int32_t* debug_records, void* stream) {
   if (!gaussians_ok(g) || !config_ok(cfg) || !bvh_ok(bvh, g) || !rays_ok(rays, cam))
@@ -132,12 +132,20 @@ rg_status rg_render_forward(const rg_gaussians* g, const rg_bvh* bvh, const rg_c
   if (n > 0 && (!rgb || !T || !replay)) return RG_ERR_INVALID_ARG;
   if (debug_records && (debug_rays < 0 || debug_cap < 1 || !debug_counts))
     return RG_ERR_INVALID_ARG;
-  if (fetch_log && log_words < 2) return RG_ERR_INVALID_ARG;
+  if (fetch_log && (log_bytes < rg_fetch_log_bytes((int32_t)n, 1) ||
+                    (reinterpret_cast<uintptr_t>(fetch_log) & 255) != 0))
+    return RG_ERR_INVALID_ARG;
   const cudaError_t e = launch_forward(*g, *bvh, *cfg, rays, cam, rgb, T, replay, fetch_log,
-                                       log_words, stats,
+                                       log_bytes, stats,
                                        debug_rays, debug_cap, debug_counts, debug_records,
                                        static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? RG_OK : RG_ERR_CUDA;
+}
+
+size_t rg_fetch_log_bytes(int32_t n_rays, int32_t pairs_per_ray) {
+  if (n_rays < 0) return 0;
+  const size_t ppr = pairs_per_ray > 0 ? (size_t)pairs_per_ray : 48;
+  return fetch_log_header_bytes(n_rays) + 48 * ppr * (size_t)(n_rays > 0 ? n_rays : 1);
 }
 
 size_t rg_backward_workspace_bytes(int32_t n, int32_t sh_degree, int32_t sg_count) {
@@ -148,8 +156,8 @@ size_t rg_backward_workspace_bytes(int32_t n, int32_t sh_degree, int32_t sg_coun
 
 rg_status rg_render_backward(const rg_gaussians* g, const rg_bvh* bvh, const rg_config* cfg,
                              const rg_rays* rays, const rg_camera* cam, const float* rgb,
-                             const float* T, const int32_t* replay, const int32_t* fetch_log,
-                             int32_t log_words, const float* d_rgb,
+                             const float* T, const int32_t* replay, const void* fetch_log,
+                             size_t log_bytes, const float* d_rgb,
                              const rg_gaussian_grads* grads, rg_stats* stats, void* ws,
                              size_t ws_bytes, void* stream) {
   if (!gaussians_ok(g) || !config_ok(cfg) || !bvh_ok(bvh, g) || !rays_ok(rays, cam) || !grads)
@@ -159,9 +167,11 @@ rg_status rg_render_backward(const rg_gaussians* g, const rg_bvh* bvh, const rg_
   if (!ws || (reinterpret_cast<uintptr_t>(ws) & 15) != 0) return RG_ERR_INVALID_ARG;
   if (ws_bytes < rg_backward_workspace_bytes(g->n, g->sh_degree, g->sg_count))
     return RG_ERR_WORKSPACE_TOO_SMALL;
-  if (fetch_log && log_words < 2) return RG_ERR_INVALID_ARG;
+  if (fetch_log && (log_bytes < rg_fetch_log_bytes((int32_t)n, 1) ||
+                    (reinterpret_cast<uintptr_t>(fetch_log) & 255) != 0))
+    return RG_ERR_INVALID_ARG;
   const cudaError_t e = launch_backward(*g, *bvh, *cfg, rays, cam, rgb, T, replay, fetch_log,
-                                        log_words, d_rgb, *grads,
+                                        log_bytes, d_rgb, *grads,
                                         stats, static_cast<float*>(ws),
                                         static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? RG_OK : RG_ERR_CUDA;

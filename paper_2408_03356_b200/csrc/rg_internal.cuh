@@ -230,6 +230,14 @@ __device__ __forceinline__ void sh_basis(int deg, float x, float y, float z, flo
 // ---------------------------------------------------------------------------
 // host-side launchers (defined in the .cu files)
 // ---------------------------------------------------------------------------
+// fetch log (training): [0, 256) arena counter (u64); then per-ray records of
+// kLogWords int32 ([0] words used or -1, then (count, arena entry offset) per
+// fetch); then the arena of 48-B pair slots (3 float4 each).
+constexpr int kLogWords = 64;
+__host__ __device__ inline size_t fetch_log_header_bytes(int n_rays) {
+  return 256 + ((4 * (size_t)kLogWords * (size_t)(n_rays > 0 ? n_rays : 1) + 255) & ~(size_t)255);
+}
+
 struct BvhLayout {
   size_t geom, app, nodes, leaf_box, root_box, codes, keys_a, keys_b, vals_a, vals_b,
       box_orig, flags, parent_int, parent_leaf, refit_cnt, bounds, hist, wide, wq_a, wq_b,
@@ -242,13 +250,13 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
 cudaError_t launch_camera_rays(const rg_camera& cam, float* o, float* d, cudaStream_t st);
 cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,
                            const rg_rays* rays, const rg_camera* cam, float* rgb, float* T,
-                           int32_t* replay, int32_t* log, int log_words, rg_stats* stats,
+                           int32_t* replay, void* log, size_t log_bytes, rg_stats* stats,
                            int dbg_rays, int dbg_cap,
                            int32_t* dbg_counts, int32_t* dbg_rec, cudaStream_t st);
 cudaError_t launch_backward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,
                             const rg_rays* rays, const rg_camera* cam, const float* rgb,
-                            const float* T, const int32_t* replay, const int32_t* log,
-                            int log_words, const float* d_rgb,
+                            const float* T, const int32_t* replay, const void* log,
+                            size_t log_bytes, const float* d_rgb,
                             const rg_gaussian_grads& grads, rg_stats* stats, float* gbuf,
                             cudaStream_t st);
 void count_launches(unsigned n);

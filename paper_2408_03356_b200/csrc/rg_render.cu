@@ -61,8 +61,10 @@ struct RenderArgs {
   float* rgb;
   float* T;
   int32_t* replay;
-  int32_t* log;            // per-ray fetch log [n_rays, log_words] (forward writes, backward reads)
-  int log_words;
+  int32_t* log;            // per-ray fetch records [n_rays, kLogWords] (forward writes)
+  float4* arena;           // pair slots (3 float4 each)
+  unsigned long long* arena_ctr;
+  long long arena_cap;     // slots
   rg_stats* stats;
   int dbg_rays, dbg_cap;
   int32_t* dbg_counts;
@@ -609,7 +611,7 @@ __global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderAr
     int count = 0, nret = 0;
     unsigned long long cursor = 0;
     bool exhausted = false;
-    int32_t* lg = P.log ? P.log + (size_t)ray * P.log_words : nullptr;
+    int32_t* lg = P.log ? P.log + (size_t)ray * kLogWords : nullptr;
     int lp = 1;
     bool log_ok = lg != nullptr;
     const bool replay_log = BWD && lg != nullptr && lg[0] >= 0;
@@ -679,28 +681,41 @@ __global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderAr
         unsigned long long key = 0;
         uint32_t pos = 0;
         int got;
-        if (BWD && replay_log) {      // the forward's query results, no traversal
+        if (BWD && replay_log) {      // the forward's set-up pairs: no traversal, no set-up
           got = lg[lp];
-          if ((int)lane < got) pos = (uint32_t)lg[lp + 1 + lane];
-          lp += 1 + got;
+          const long long off = (long long)(unsigned)lg[lp + 1];
+          lp += 2;
+          if ((int)lane < got) {
+            const float4* src = P.arena + 3 * (off + lane);
+            M.e0[count + lane] = src[0];
+            M.e1[count + lane] = src[1];
+            M.e2[count + lane] = src[2];
+          }
         } else {
           got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
+          if ((int)lane < got) setup_pair(P.S, M, count + (int)lane, R, pos);
           if (!BWD && log_ok) {
-            if (lp + 1 + got > P.log_words) {
+            unsigned long long off = 0;
+            if (lane == 0 && got > 0) off = atomicAdd(P.arena_ctr, (unsigned long long)got);
+            off = shfl64(off, 0);
+            if (lp + 2 > kLogWords || (long long)(off + got) > P.arena_cap) {
               log_ok = false;
             } else {
-              if (lane == 0) lg[lp] = got;
-              if ((int)lane < got) lg[lp + 1 + lane] = (int)pos;
-              lp += 1 + got;
+              if (lane == 0) { lg[lp] = got; lg[lp + 1] = (int)off; }
+              lp += 2;
+              __syncwarp();
+              if ((int)lane < got) {
+                float4* dst = P.arena + 3 * (off + lane);
+                dst[0] = M.e0[count + lane];
+                dst[1] = M.e1[count + lane];
+                dst[2] = M.e2[count + lane];
+              }
             }
           }
         }
-        if ((int)lane < got) {
-          setup_pair(P.S, M, count + (int)lane, R, pos);
-          if (BWD) {
-            A.a[count + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-            A.b[count + lane] = make_float2(0.f, 0.f);
-          }
+        if (BWD && (int)lane < got) {
+          A.a[count + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+          A.b[count + lane] = make_float2(0.f, 0.f);
         }
         if (lane == 0) cnt.pairs += got;
         count += got;
@@ -1029,6 +1044,17 @@ void launch_render(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st)
 constexpr size_t kSmemFwd = sizeof(WarpMem) * kWarps;
 constexpr size_t kSmemBwd = (sizeof(WarpMem) + sizeof(WarpAcc)) * kWarps;
 
+// fetch-log layout (rg_internal.cuh): counter | per-ray records | arena
+void set_log(RenderArgs& A, const void* log, size_t log_bytes, int n_rays) {
+  if (!log) return;
+  char* base = const_cast<char*>(static_cast<const char*>(log));
+  const size_t hdr = fetch_log_header_bytes(n_rays);
+  A.arena_ctr = reinterpret_cast<unsigned long long*>(base);
+  A.log = reinterpret_cast<int32_t*>(base + 256);
+  A.arena = reinterpret_cast<float4*>(base + hdr);
+  A.arena_cap = (long long)((log_bytes - hdr) / 48);
+}
+
 }  // namespace
 
 cudaError_t launch_camera_rays(const rg_camera& cam, float* o, float* d, cudaStream_t st) {
@@ -1039,7 +1065,7 @@ cudaError_t launch_camera_rays(const rg_camera& cam, float* o, float* d, cudaStr
 
 cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,
                            const rg_rays* rays, const rg_camera* cam, float* rgb, float* T,
-                           int32_t* replay, int32_t* log, int log_words, rg_stats* stats,
+                           int32_t* replay, void* log, size_t log_bytes, rg_stats* stats,
                            int dbg_rays, int dbg_cap, int32_t* dbg_counts, int32_t* dbg_rec,
                            cudaStream_t st) {
   (void)g;
@@ -1050,7 +1076,8 @@ cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_conf
   ray_grid(A, rays, cam, grid);
   if (A.n_rays == 0) return cudaSuccess;
   A.rgb = rgb; A.T = T; A.replay = replay; A.stats = stats;
-  A.log = log; A.log_words = log_words;
+  set_log(A, log, log_bytes, A.n_rays);
+  if (log) cudaMemsetAsync(A.arena_ctr, 0, 8, st);
   A.dbg_rays = dbg_rec ? dbg_rays : 0;
   A.dbg_cap = dbg_cap; A.dbg_counts = dbg_counts; A.dbg_rec = dbg_rec;
   launch_render<false>(A, grid, kSmemFwd, st);
@@ -1060,18 +1087,17 @@ cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_conf
 
 cudaError_t launch_backward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,
                             const rg_rays* rays, const rg_camera* cam, const float* rgb,
-                            const float* T, const int32_t* replay, const int32_t* log,
-                            int log_words, const float* d_rgb,
+                            const float* T, const int32_t* replay, const void* log,
+                            size_t log_bytes, const float* d_rgb,
                             const rg_gaussian_grads& grads, rg_stats* stats, float* gbuf,
                             cudaStream_t st) {
   (void)T;
   RenderArgs A = {};
-  A.log = const_cast<int32_t*>(log);
-  A.log_words = log_words;
   A.S = view_of(b);
   A.c = c;
   dim3 grid;
   ray_grid(A, rays, cam, grid);
+  set_log(A, log, log_bytes, A.n_rays);
   const int gs = grad_stride(b.sh_degree, b.sg_count);
   if (b.n > 0) cudaMemsetAsync(gbuf, 0, sizeof(float) * (size_t)gs * b.n, st);
   A.stats = stats;

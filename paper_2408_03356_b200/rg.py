@@ -65,7 +65,7 @@ class _BVH(C.Structure):
 
 EXPORTS = ("rg_status_string", "rg_version", "rg_kernel_launches", "rg_bvh_workspace_bytes", "rg_build_bvh",
            "rg_camera_rays", "rg_render_forward", "rg_backward_workspace_bytes",
-           "rg_render_backward", "rg_l1_loss_grad")
+           "rg_render_backward", "rg_l1_loss_grad", "rg_fetch_log_bytes")
 
 _lib = None
 
@@ -98,11 +98,13 @@ def lib(load_only: bool = False):
     L.rg_camera_rays.restype = C.c_int
     L.rg_camera_rays.argtypes = [P, P, P, P]
     L.rg_render_forward.restype = C.c_int
-    L.rg_render_forward.argtypes = [P, P, P, P, P, P, P, P, P, I32, P, I32, I32, P, P, P]
+    L.rg_render_forward.argtypes = [P, P, P, P, P, P, P, P, P, SZ, P, I32, I32, P, P, P]
+    L.rg_fetch_log_bytes.restype = SZ
+    L.rg_fetch_log_bytes.argtypes = [I32, I32]
     L.rg_backward_workspace_bytes.restype = SZ
     L.rg_backward_workspace_bytes.argtypes = [I32, I32, I32]
     L.rg_render_backward.restype = C.c_int
-    L.rg_render_backward.argtypes = [P, P, P, P, P, P, P, P, P, I32, P, P, P, P, SZ, P]
+    L.rg_render_backward.argtypes = [P, P, P, P, P, P, P, P, P, SZ, P, P, P, P, SZ, P]
     L.rg_l1_loss_grad.restype = C.c_int
     L.rg_l1_loss_grad.argtypes = [P, P, C.c_int64, C.c_float, P, P, P]
     _lib = L
@@ -295,11 +297,10 @@ def _ray_args(rays, camera):
     return None, C.byref(cs), camera.n_rays, (cs,)
 
 
-LOG_WORDS = 256   # per-ray fetch-log words (training): covers ~200 pair set-ups
-
-
-def new_log(n_rays, device="cuda", words=LOG_WORDS):
-    return torch.empty(n_rays, words, dtype=torch.int32, device=device)
+def new_log(n_rays, device="cuda", pairs_per_ray=0):
+    """Fetch-log buffer for a training forward (rg_fetch_log_bytes)."""
+    nbytes = int(lib().rg_fetch_log_bytes(int(n_rays), int(pairs_per_ray)))
+    return torch.empty(nbytes, dtype=torch.uint8, device=device)
 
 
 def render_forward(scene: Gaussians, bvh: BVH, cfg: Config, *, rays=None, camera=None,
@@ -320,7 +321,7 @@ def render_forward(scene: Gaussians, bvh: BVH, cfg: Config, *, rays=None, camera
         dr = torch.full((dbg_n, dbg_cap, 2), -1, dtype=torch.int32, device=dev)
         out["debug_counts"], out["debug_records"] = dc, dr
     gs, cs = scene.struct(), cfg.struct()
-    lw = int(log.shape[1]) if log is not None else 0
+    lw = int(log.numel()) if log is not None else 0
     _check(lib().rg_render_forward(C.byref(gs), C.byref(bvh.h), C.byref(cs), rp, cp,
                                    _ptr(out["rgb"]), _ptr(out["T"]), _ptr(out["replay"]),
                                    _ptr(log), lw, _ptr(stats), dbg_n, dbg_cap, _ptr(dc), _ptr(dr),
@@ -351,7 +352,7 @@ def render_backward(scene: Gaussians, bvh: BVH, cfg: Config, fwd: dict, d_rgb, *
     gs, cs = scene.struct(), cfg.struct()
     d_rgb = d_rgb.contiguous()
     log = fwd.get("log")
-    lw = int(log.shape[1]) if log is not None else 0
+    lw = int(log.numel()) if log is not None else 0
     _check(lib().rg_render_backward(C.byref(gs), C.byref(bvh.h), C.byref(cs), rp, cp,
                                     _ptr(fwd["rgb"]), _ptr(fwd["T"]), _ptr(fwd["replay"]),
                                     _ptr(log), lw, _ptr(d_rgb), C.byref(g), _ptr(stats), _ptr(ws),
