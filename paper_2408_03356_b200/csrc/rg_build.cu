@@ -261,7 +261,8 @@ __global__ void __launch_bounds__(kThreads) k_pack(rg_gaussians g, rg_config c,
 }
 
 // appearance record in Morton order, one warp per Gaussian row (coalesced):
-// SH [(deg+1)^2 x 3], then per lobe (k0,k1,k2, lambda, p0,p1,p2), zero pad.
+// SH [(deg+1)^2 x 3] zero-padded to 48 floats, then per lobe
+// (k0,k1,k2, lambda, p0,p1,p2), zero pad.
 __global__ void __launch_bounds__(kThreads) k_pack_app(rg_gaussians g, const uint32_t* order,
                                                        float* app, int stride) {
   const int lane = threadIdx.x & 31;
@@ -275,8 +276,8 @@ __global__ void __launch_bounds__(kThreads) k_pack_app(rg_gaussians g, const uin
       float v = 0.0f;
       if (f < nc3) {
         v = g.sh[i * nc3 + f];
-      } else if (f < nc3 + 7 * G) {
-        const int j = (f - nc3) / 7, r = (f - nc3) - 7 * j;
+      } else if (f >= kShFloats && f < kShFloats + 7 * G) {
+        const int j = (f - kShFloats) / 7, r = (f - kShFloats) - 7 * j;
         const size_t ij = i * G + j;
         v = r < 3 ? g.sg_amp[3 * ij + r] : (r == 3 ? g.sg_sharp[ij] : g.sg_axis[3 * ij + r - 4]);
       }

@@ -25,8 +25,12 @@ constexpr int kACap = 32;                         // active-list capacity per ra
 constexpr int kGroup = 8;                         // samples per register group
 constexpr float kLog2e = 1.4426950408889634f;
 
+// appearance record: SH region fixed at 16 coefficients x 3 (zero past the
+// degree) so that the SG lobes (7 floats each) always start at float 48
+constexpr int kShFloats = 48;
 __host__ __device__ inline int app_floats(int deg, int lobes) {
-  return 3 * (deg + 1) * (deg + 1) + 7 * lobes;
+  (void)deg;
+  return kShFloats + 7 * lobes;
 }
 __host__ __device__ inline int app_stride(int deg, int lobes) {
   return (app_floats(deg, lobes) + 3) & ~3;

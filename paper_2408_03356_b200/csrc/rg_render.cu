@@ -253,33 +253,47 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
   return nk;
 }
 
-__device__ __forceinline__ float3 pair_color(const SceneView& S, int pos, const float3& d) {
-  float Y[16];
-  sh_basis(S.deg, d.x, d.y, d.z, Y);
-  const float* ap = S.app + (size_t)pos * S.app_stride;
-  const int nc = (S.deg + 1) * (S.deg + 1);
-  float r = 0.f, g = 0.f, b = 0.f;
+__device__ __forceinline__ float f4c(const float4& v, int q) {
+  return q == 0 ? v.x : (q == 1 ? v.y : (q == 2 ? v.z : v.w));
+}
+
+// c_l(d): SH part from 12 float4 loads against the per-ray Y(d) in shared
+// memory (zero past the degree, record zero-padded to 16 coefficients), then
+// the SG lobes from the float4s covering floats 48..48+7G.
+__device__ __forceinline__ float3 pair_color(const SceneView& S, const WarpMem& M, int pos,
+                                             const float3& d) {
+  const float4* ap4 = reinterpret_cast<const float4*>(S.app + (size_t)pos * S.app_stride);
+  float4 v[12];
 #pragma unroll
-  for (int m = 0; m < 16; ++m) {
-    if (m < nc) {
-      r = fmaf(Y[m], __ldg(ap + 3 * m), r);
-      g = fmaf(Y[m], __ldg(ap + 3 * m + 1), g);
-      b = fmaf(Y[m], __ldg(ap + 3 * m + 2), b);
+  for (int k = 0; k < 12; ++k) v[k] = __ldg(ap4 + k);
+  float acc[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int k = 0; k < 12; ++k)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int f = 4 * k + q;   // coefficient f / 3, channel f % 3 (compile-time)
+      acc[f % 3] = fmaf(M.Y[f / 3], f4c(v[k], q), acc[f % 3]);
+    }
+  if (S.lobes > 0) {
+    float4 w[13];
+#pragma unroll
+    for (int k = 0; k < 13; ++k)
+      if (4 * k < 7 * S.lobes) w[k] = __ldg(ap4 + 12 + k);
+#pragma unroll
+    for (int j = 0; j < kMaxLobes; ++j) {
+      if (j < S.lobes) {
+        float p[7];
+#pragma unroll
+        for (int r = 0; r < 7; ++r) p[r] = f4c(w[(7 * j + r) / 4], (7 * j + r) % 4);
+        const float dp = d.x * p[4] + d.y * p[5] + d.z * p[6];
+        const float e = ex2_approx(p[3] * (dp - 1.0f) * kLog2e);
+        acc[0] = fmaf(p[0], e, acc[0]);
+        acc[1] = fmaf(p[1], e, acc[1]);
+        acc[2] = fmaf(p[2], e, acc[2]);
+      }
     }
   }
-  const float* lp = ap + 3 * nc;
-#pragma unroll
-  for (int j = 0; j < kMaxLobes; ++j) {
-    if (j < S.lobes) {
-      const float* q = lp + 7 * j;
-      const float dp = d.x * __ldg(q + 4) + d.y * __ldg(q + 5) + d.z * __ldg(q + 6);
-      const float e = ex2_approx(__ldg(q + 3) * (dp - 1.0f) * kLog2e);
-      r = fmaf(__ldg(q), e, r);
-      g = fmaf(__ldg(q + 1), e, g);
-      b = fmaf(__ldg(q + 2), e, b);
-    }
-  }
-  return make_float3(r, g, b);
+  return make_float3(acc[0], acc[1], acc[2]);
 }
 
 // Per-(ray, Gaussian) set-up into slot `sl`: exact interval and the exponent
@@ -299,7 +313,7 @@ __device__ __noinline__ void setup_pair(const SceneView& S, WarpMem& M, int sl, 
   const float u2 = g2.z * x0 + g2.w * x1 + g3.x * x2;
   const float qm = u0 * u0 + u1 * u1 + u2 * u2;
   const float b1 = u0 * pg.dl0 + u1 * pg.dl1 + u2 * pg.dl2;
-  const float3 col = pair_color(S, (int)pos, R.d);
+  const float3 col = pair_color(S, M, (int)pos, R.d);
   M.e0[sl] = make_float4(pg.te, pg.tx, pg.tm, lg2_approx(g0.w) - 0.5f * kLog2e * qm);
   M.e1[sl] = make_float4(-kLog2e * b1, -0.5f * kLog2e * pg.A, col.x, col.y);
   M.e2[sl] = make_float4(col.z, __int_as_float((int)pos), g3.z, 0.f);
@@ -482,7 +496,6 @@ __device__ __noinline__ void scatter_batch(const SceneView& S, const WarpMem& M,
     atomicAdd(row + 2, make_float4(dM[4], dM[5], dM[6], dM[7]));
     atomicAdd(row + 3, make_float4(dM[8], 0.f, 0.f, 0.f));
   }
-  const int nc = (S.deg + 1) * (S.deg + 1);
   while (mask) {
     const int b = __ffs(mask) - 1;
     mask &= mask - 1;
@@ -496,7 +509,7 @@ __device__ __noinline__ void scatter_batch(const SceneView& S, const WarpMem& M,
       const float dsel = am.ch == 0 ? d0 : (am.ch == 1 ? d1 : d2);
       v = make_float4(dsel * am.y.x, dsel * am.y.y, dsel * am.y.z, dsel * am.y.w);
     } else if (am.lobe >= 0) {   // SG lobe j: e = exp(lambda (d.p - 1)), kd = <dc, k> e
-      const float* q = S.app + (size_t)pos * S.app_stride + 3 * nc + 7 * am.lobe;
+      const float* q = S.app + (size_t)pos * S.app_stride + kShFloats + 7 * am.lobe;
       const float lam = __ldg(q + 3);
       const float dpm = R.d.x * __ldg(q + 4) + R.d.y * __ldg(q + 5) + R.d.z * __ldg(q + 6) - 1.0f;
       const float ej = ex2_approx(lam * dpm * kLog2e);
@@ -596,13 +609,14 @@ __global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderAr
     R.inv = make_float3(1.0f / R.d.x, 1.0f / R.d.y, 1.0f / R.d.z);
     R.oinv = make_float3(R.o.x * R.inv.x, R.o.y * R.inv.y, R.o.z * R.inv.z);
     AppMap am;
-    if (BWD) {
+    {   // Y(d) once per ray (zero past the degree): colour set-up and SH gradients
       float Y[16];
       sh_basis(P.S.deg, R.d.x, R.d.y, R.d.z, Y);
-      am = app_map(P.S, Y);
+      const int nc = (P.S.deg + 1) * (P.S.deg + 1);
 #pragma unroll
       for (int m = 0; m < 16; ++m)
-        if ((int)lane == m) M.Y[m] = Y[m];
+        if ((int)lane == m) M.Y[m] = m < nc ? Y[m] : 0.f;
+      if (BWD) am = app_map(P.S, Y);
       __syncwarp();
     }
     Lanes<GW> L;
