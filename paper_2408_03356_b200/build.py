@@ -21,6 +21,8 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-I", os.path.join(ROOT, "include")]
 if os.environ.get("RG_MIN_BLOCKS"):
     FLAGS += [f"-DRG_MIN_BLOCKS={int(os.environ['RG_MIN_BLOCKS'])}"]
+for _flag in os.environ.get("RG_DEFINES", "").split():
+    FLAGS += [f"-D{_flag}"]
 
 
 def _inputs():

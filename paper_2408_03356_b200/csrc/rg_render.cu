@@ -253,47 +253,28 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
   return nk;
 }
 
-__device__ __forceinline__ float f4c(const float4& v, int q) {
-  return q == 0 ? v.x : (q == 1 ? v.y : (q == 2 ? v.z : v.w));
-}
-
-// c_l(d): SH part from 12 float4 loads against the per-ray Y(d) in shared
-// memory (zero past the degree, record zero-padded to 16 coefficients), then
-// the SG lobes from the float4s covering floats 48..48+7G.
+// c_l(d) = sum_m c~_m Y_m(d) + sum_j k_j e^{lambda_j (d.p_j - 1)} (Eq. 14-15):
+// Y(d) is per-ray in shared memory (zero past the degree, so the fixed 16-
+// coefficient SH region of the record needs no predicate); SG lobes at 48+7j.
 __device__ __forceinline__ float3 pair_color(const SceneView& S, const WarpMem& M, int pos,
                                              const float3& d) {
-  const float4* ap4 = reinterpret_cast<const float4*>(S.app + (size_t)pos * S.app_stride);
-  float4 v[12];
+  const float* ap = S.app + (size_t)pos * S.app_stride;
+  float r = 0.f, g = 0.f, b = 0.f;
 #pragma unroll
-  for (int k = 0; k < 12; ++k) v[k] = __ldg(ap4 + k);
-  float acc[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-  for (int k = 0; k < 12; ++k)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int f = 4 * k + q;   // coefficient f / 3, channel f % 3 (compile-time)
-      acc[f % 3] = fmaf(M.Y[f / 3], f4c(v[k], q), acc[f % 3]);
-    }
-  if (S.lobes > 0) {
-    float4 w[13];
-#pragma unroll
-    for (int k = 0; k < 13; ++k)
-      if (4 * k < 7 * S.lobes) w[k] = __ldg(ap4 + 12 + k);
-#pragma unroll
-    for (int j = 0; j < kMaxLobes; ++j) {
-      if (j < S.lobes) {
-        float p[7];
-#pragma unroll
-        for (int r = 0; r < 7; ++r) p[r] = f4c(w[(7 * j + r) / 4], (7 * j + r) % 4);
-        const float dp = d.x * p[4] + d.y * p[5] + d.z * p[6];
-        const float e = ex2_approx(p[3] * (dp - 1.0f) * kLog2e);
-        acc[0] = fmaf(p[0], e, acc[0]);
-        acc[1] = fmaf(p[1], e, acc[1]);
-        acc[2] = fmaf(p[2], e, acc[2]);
-      }
-    }
+  for (int m = 0; m < 16; ++m) {
+    r = fmaf(M.Y[m], __ldg(ap + 3 * m), r);
+    g = fmaf(M.Y[m], __ldg(ap + 3 * m + 1), g);
+    b = fmaf(M.Y[m], __ldg(ap + 3 * m + 2), b);
   }
-  return make_float3(acc[0], acc[1], acc[2]);
+  for (int j = 0; j < S.lobes; ++j) {
+    const float* q = ap + kShFloats + 7 * j;
+    const float dp = d.x * __ldg(q + 4) + d.y * __ldg(q + 5) + d.z * __ldg(q + 6);
+    const float e = ex2_approx(__ldg(q + 3) * (dp - 1.0f) * kLog2e);
+    r = fmaf(__ldg(q), e, r);
+    g = fmaf(__ldg(q + 1), e, g);
+    b = fmaf(__ldg(q + 2), e, b);
+  }
+  return make_float3(r, g, b);
 }
 
 // Per-(ray, Gaussian) set-up into slot `sl`: exact interval and the exponent
