@@ -82,7 +82,6 @@ struct RenderArgs {
 struct WarpMem {
   float4 e0[kSlots], e1[kSlots], e2[kSlots];
   int stk[kStk];
-  Counters cnt;        // per-ray counters (lane 0 updates; registers stay free)
   uint32_t lq[64];     // fetch: queued leaves awaiting the exact test
   unsigned long long kscr[32];   // fetch: candidate sort scratch
   uint32_t pscr[32];
@@ -516,16 +515,16 @@ __device__ __forceinline__ int skip_to(float te, int s, int B, float dt, float t
   return est;
 }
 
-// the per-ray counters live in shared memory, updated by lane 0 only
 __device__ __forceinline__ void flush_stats(rg_stats* st, const Counters& c, bool hit) {
-  __syncwarp();
-  if (lane_id() != 0) return;
-  const uint32_t v[10] = {1u, hit ? 1u : 0u, c.slabs, c.pairs, c.evals, c.samples, c.overflows,
-                          c.fetches, c.nodes, c.stackov};
+  const unsigned lane = lane_id();
+  const uint32_t v[10] = {lane == 0 ? 1u : 0u, (lane == 0 && hit) ? 1u : 0u, c.slabs, c.pairs,
+                          c.evals, c.samples, c.overflows, c.fetches, c.nodes, c.stackov};
   unsigned long long* dst = reinterpret_cast<unsigned long long*>(st);
 #pragma unroll
-  for (int k = 0; k < 10; ++k)
-    if (v[k]) atomicAdd(dst + k, (unsigned long long)v[k]);
+  for (int k = 0; k < 10; ++k) {
+    const uint32_t s = __reduce_add_sync(kFull, v[k]);
+    if (lane == 0 && s) atomicAdd(dst + k, (unsigned long long)s);
+  }
 }
 
 // Kahan accumulation
@@ -575,8 +574,7 @@ __global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderAr
   float C0 = 0.f, C1 = 0.f, C2 = 0.f, k0c = 0.f, k1c = 0.f, k2c = 0.f;
   float tau = 0.f, tauc = 0.f, T = 1.f;
   int replay = -1;
-  Counters& cnt = M.cnt;
-  if (lane == 0) cnt = Counters{};
+  Counters cnt = {};
   const bool dbg = (!BWD) && P.dbg_rec != nullptr && ray < P.dbg_rays;
   int dbg_n = 0;
   float gr0 = 0.f, gr1 = 0.f, gr2 = 0.f, Pp0 = 0.f, Pp1 = 0.f, Pp2 = 0.f;
@@ -775,10 +773,7 @@ __global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderAr
             if (fetch(P.S, M, R, tlo, thi, cur2, 1, pk, pp, cnt) > 0 && lane == 0) cnt.overflows++;
           }
         }
-        {
-          const uint32_t evs = __reduce_add_sync(kFull, ev);
-          if (lane == 0) cnt.evals += evs;
-        }
+        cnt.evals += ev;
         // reduce over the entry subsets: every lane of sample j holds the totals
 #pragma unroll
         for (int off = GW; off < 32; off <<= 1) {
