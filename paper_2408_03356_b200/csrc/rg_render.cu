@@ -90,8 +90,8 @@ struct WarpMem {
 struct WarpAcc {
   float4 a[kSlots];    // Sw, Sw1, Sw2, dc_r
   float2 b[kSlots];    // dc_g, dc_b
-  float4 s0[8], s1[8]; // per-sample backward values of the current group: {tk, dls, dc0, dc1},
-                       // {dc2, gc, inv, live}
+  float4 s0[32], s1[32];  // per-sample backward values of the current group / window:
+                          // {tk, dls, dc0, dc1}, {dc2, gc, inv, live}
 };
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
@@ -682,8 +682,11 @@ __global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderAr
           count = nc;
         }
       }
-      // ---- refill in key order until every Gaussian entering by t_hi is held
-      while (!exhausted && count < kA && (count == 0 || M.e0[count - 1].x <= thi)) {
+      // 4-slab window (B = 8: 32 samples, one per lane); thr = t_hi of its last slab
+      const bool win = (GW == 8) && (B == 8);
+      const float thr = win ? fminf(t1, fma_((float)(k0 + 4 * B), c.dt, t0)) : thi;
+      // ---- refill in key order until every Gaussian entering by thr is held
+      while (!exhausted && count < kA && (count == 0 || M.e0[count - 1].x <= thr)) {
         const int want = min(32, kA - count);
         unsigned long long key = 0;
         uint32_t pos = 0;
@@ -737,6 +740,172 @@ __global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderAr
       if (M.e0[0].x > thi) {   // empty slab(s): jump to the slab holding the next entry
         s = skip_to(M.e0[0].x, s, B, c.dt, t0, t1);
         continue;
+      }
+      if (win) {
+        // ---- window of slabs s..s+3 when the held list is complete for it and no
+        // slab can exceed K: lane k integrates sample 8s + k over all members
+        int n3;
+        {
+          const unsigned m0 = __ballot_sync(kFull, (int)lane < count && M.e0[lane].x <= thr);
+          const unsigned m1 =
+              __ballot_sync(kFull, (int)lane + 32 < count && M.e0[lane + 32].x <= thr);
+          n3 = __popc(m0) + __popc(m1);
+        }
+        if ((n3 < count || exhausted) && n3 <= K) {
+          const float tk = sample_t(k0 + (int)lane, c.dt, t0);
+          const bool val = tk < t1;
+          float sg = 0.f, sr = 0.f, sgg = 0.f, sb = 0.f;
+          uint32_t ev = 0;
+#pragma unroll 2
+          for (int e = 0; e < n3; ++e) {
+            const float4 a = M.e0[e];
+            if (val && a.x <= tk && tk <= a.y) {
+              const float4 q = M.e1[e];
+              const float cbv = M.e2[e].x;
+              const float tau_ = tk - a.z;
+              const float w = ex2_approx(fmaf(tau_, fmaf(q.y, tau_, q.x), a.w));
+              sg += w;
+              sr = fmaf(w, q.z, sr);
+              sgg = fmaf(w, q.w, sgg);
+              sb = fmaf(w, cbv, sb);
+              ++ev;
+            }
+          }
+          const bool live0 = val && sg > 0.f;
+          const float x = live0 ? sg * c.dt : 0.f;
+          float incl = x;
+#pragma unroll
+          for (int dd = 1; dd < 32; dd <<= 1) {
+            const float v = __shfl_up_sync(kFull, incl, dd);
+            if ((int)lane >= dd) incl += v;
+          }
+          const float Tb = ex2_approx(-(tau + (incl - x)) * kLog2e);
+          const float e_s = ex2_approx(-x * kLog2e);
+          const float al = alpha_of(x, e_s);
+          const float inv_s = live0 ? 1.0f / sg : 0.f;
+          const float cr = sr * inv_s, cg = sgg * inv_s, cb = sb * inv_s;
+          const float wgt = live0 ? Tb * al : 0.f;
+          float p0 = wgt * cr, p1 = wgt * cg, p2 = wgt * cb;
+#pragma unroll
+          for (int dd = 1; dd < 32; dd <<= 1) {
+            const float v0 = __shfl_up_sync(kFull, p0, dd);
+            const float v1 = __shfl_up_sync(kFull, p1, dd);
+            const float v2 = __shfl_up_sync(kFull, p2, dd);
+            if ((int)lane >= dd) { p0 += v0; p1 += v1; p2 += v2; }
+          }
+          // first slab whose end has T <= T_eps (forward) / the recorded one (backward)
+          int wlast = 3;
+          bool term = false;
+          if (BWD) {
+            if (replay_in >= s && replay_in <= s + 3) { wlast = replay_in - s; term = true; }
+          } else {
+            const float Te = ex2_approx(-(tau + incl) * kLog2e);
+            const unsigned tm = __ballot_sync(kFull, ((lane & 7u) == 7u) && Te <= c.t_eps);
+            if (tm) { wlast = (__ffs(tm) - 1) >> 3; term = true; }
+          }
+          const int last = 8 * wlast + 7;
+          const bool inwin = (int)lane <= last;
+          const bool live = live0 && inwin;
+          // per-slab sets (counters, debug dump): members of slab s+w, key order
+          for (int w = 0; w <= wlast; ++w) {
+            const float lo_w = fma_((float)(k0 + 8 * w), c.dt, t0);
+            if (!(sample_t(k0 + 8 * w, c.dt, t0) < t1)) break;
+            const float hi_w = fminf(t1, fma_((float)(k0 + 8 * w + 8), c.dt, t0));
+            const unsigned q0 = __ballot_sync(
+                kFull, (int)lane < n3 && M.e0[lane].x <= hi_w && M.e0[lane].y >= lo_w);
+            const unsigned q1 = __ballot_sync(
+                kFull, (int)lane + 32 < n3 && M.e0[lane + 32].x <= hi_w && M.e0[lane + 32].y >= lo_w);
+            if ((q0 | q1) && lane == 0) cnt.slabs++;
+            if (dbg && (q0 | q1)) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const unsigned qm = h ? q1 : q0;
+                if ((qm >> lane) & 1u) {
+                  const int r = dbg_n + __popc(qm & ((1u << lane) - 1u));
+                  if (r < P.dbg_cap) {
+                    int32_t* rr = P.dbg_rec + 2 * ((size_t)ray * P.dbg_cap + r);
+                    rr[0] = s + w;
+                    rr[1] = (int32_t)__float_as_uint(M.e2[h * 32 + lane].z);
+                  }
+                }
+                dbg_n = min(P.dbg_cap, dbg_n + __popc(qm));
+              }
+            }
+          }
+          {
+            const uint32_t evs = __reduce_add_sync(kFull, inwin ? ev : 0u);
+            const unsigned smask = __ballot_sync(kFull, live);
+            if (lane == 0) { cnt.evals += evs; cnt.samples += __popc(smask); }
+          }
+          if (BWD) {
+            SampleGrad H = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (live) {
+              const float Ta = Tb * e_s;
+              H.dc0 = gr0 * wgt; H.dc1 = gr1 * wgt; H.dc2 = gr2 * wgt;
+              const float gcj = gr0 * cr + gr1 * cg + gr2 * cb;
+              const float gS =
+                  gr0 * (Pp0 - (C0 + p0)) + gr1 * (Pp1 - (C1 + p1)) + gr2 * (Pp2 - (C2 + p2));
+              H.dls = c.dt * (Ta * gcj - gS);
+              H.gc = H.dc0 * cr + H.dc1 * cg + H.dc2 * cb;
+              H.inv = inv_s;
+            }
+            A.s0[lane] = make_float4(tk, H.dls, H.dc0, H.dc1);
+            A.s1[lane] = make_float4(H.dc2, H.gc, H.inv, live ? 1.f : 0.f);
+            __syncwarp();
+            // lane = member, loop over the window samples its interval covers
+            for (int base = 0; base < n3; base += 32) {
+              const int e = base + (int)lane;
+              if (e < n3) {
+                const float4 a = M.e0[e];
+                const float4 q = M.e1[e];
+                const float cbv = M.e2[e].x;
+                const float kf = (float)k0 + 0.5f;
+                int kl = (int)floorf((a.x - t0) / c.dt - kf) - 1;
+                int kh = (int)ceilf((a.y - t0) / c.dt - kf) + 1;
+                kl = max(kl, 0);
+                kh = min(kh, last);
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
+                for (int k = kl; k <= kh; ++k) {
+                  const float4 s0 = A.s0[k];
+                  const float tkk = s0.x;
+                  if (a.x <= tkk && tkk <= a.y) {
+                    const float4 s1 = A.s1[k];
+                    if (s1.w != 0.f) {
+                      const float tau_ = tkk - a.z;
+                      const float w = ex2_approx(fmaf(tau_, fmaf(q.y, tau_, q.x), a.w));
+                      const float dldw = s0.y + (s0.z * q.z + s0.w * q.w + s1.x * cbv - s1.y) * s1.z;
+                      const float wd = w * dldw, wi = w * s1.z;
+                      a0 += wd;
+                      a1 = fmaf(wd, tau_, a1);
+                      a2 = fmaf(wd * tau_, tau_, a2);
+                      a3 = fmaf(wi, s0.z, a3);
+                      a4 = fmaf(wi, s0.w, a4);
+                      a5 = fmaf(wi, s1.x, a5);
+                    }
+                  }
+                }
+                float4 v = A.a[e];
+                float2 w2 = A.b[e];
+                v.x += a0; v.y += a1; v.z += a2; v.w += a3;
+                w2.x += a4; w2.y += a5;
+                A.a[e] = v;
+                A.b[e] = w2;
+              }
+            }
+            __syncwarp();
+          }
+          kadd(tau, tauc, __shfl_sync(kFull, incl, last));
+          kadd(C0, k0c, __shfl_sync(kFull, p0, last));
+          kadd(C1, k1c, __shfl_sync(kFull, p1, last));
+          kadd(C2, k2c, __shfl_sync(kFull, p2, last));
+          T = ex2_approx(-tau * kLog2e);
+          if (term) {
+            if (!BWD) replay = s + wlast;
+            break;
+          }
+          s += 4;
+          continue;
+        }
       }
       int n_in;
       {
