@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderAr
           const bool inwin = (int)lane <= last;
           const bool live = live0 && inwin;
           // per-slab sets (counters, debug dump): members of slab s+w, key order
-          for (int w = 0; w <= wlast; ++w) {
+          for (int w = 0; w <= wlast && (P.stats != nullptr || dbg); ++w) {
             const float lo_w = fma_((float)(k0 + 8 * w), c.dt, t0);
             if (!(sample_t(k0 + 8 * w, c.dt, t0) < t1)) break;
             const float hi_w = fminf(t1, fma_((float)(k0 + 8 * w + 8), c.dt, t0));
