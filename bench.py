@@ -55,6 +55,16 @@ def alu_work(stats, c, which):
     return f, m
 
 
+def _ncu_traffic(stage):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/r1/ncu_traffic.json); None when absent."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1", "ncu_traffic.json")
+    try:
+        return json.load(open(p)).get(stage)
+    except (OSError, ValueError):
+        return None
+
+
 def peaks(sm_mhz):
     sms = 148
     fp32 = sms * 128 * 2 * sm_mhz * 1e6      # FLOP/s
@@ -334,7 +344,7 @@ def run_ours(args):
         "config": {"workload": "C1 Blender-like training step: 300k Gaussians SH3+7SG, 800x800 view per rank "
                                "(build + fwd + L1 grad + bwd + finalize + grad all-reduce)",
                    "global_batch": total_rays, "seq_len": None, "parallelism": f"dp{world}",
-                   "l2": "per-step working set (records 139 MB, params 130 MB, grad buffers 270 MB) > 126 MB L2; no flush"},
+                   "l2": "per-step working set (fetch-log arena ~720 MB, params 130 MB, grad buffers 270 MB) > 126 MB L2; no flush"},
         "fwd": {"value": world * R / (fwd_ms * 1e-3) / 1e6, "unit": "Mrays/s", "ms": fwd_ms,
                 "fps_per_gpu": 1e3 / fwd_ms, "paper_fps_rtx4090": PAPER_FPS},
         "stages_ms": stage_ms,
@@ -343,7 +353,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "roofline": {"bound": "alu", "kernel": f"k_render<{'true' if dom == 'backward' else 'false'}> ({dom})",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": None,
+                     "traffic": _ncu_traffic(dom),
                      "work": {"flops": flops, "mufu": mufu, "mufu_weight": 16, "sm_mhz_for_peak": mhz},
                      "peak_source": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (B200_PROFILING.md counts); MUFU 16/SM/clk"},
         "counters": {"fwd": sf, "bwd": sb},
