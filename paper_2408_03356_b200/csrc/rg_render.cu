@@ -852,19 +852,23 @@ __global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderAr
             A.s0[lane] = make_float4(tk, H.dls, H.dc0, H.dc1);
             A.s1[lane] = make_float4(H.dc2, H.gc, H.inv, live ? 1.f : 0.f);
             __syncwarp();
-            // lane = member, loop over the window samples its interval covers
-            for (int base = 0; base < n3; base += 32) {
-              const int e = base + (int)lane;
+            // lane = (member, part): P2 members per pass, each member's window samples
+            // split into 32/P2 parts of P2 samples; parts reduced by xor shuffles
+            const int P2 = n3 <= 8 ? 8 : (n3 <= 16 ? 16 : 32);
+            for (int base = 0; base < n3; base += P2) {
+              const int e = base + ((int)lane & (P2 - 1));
+              const int part0 = (int)lane & ~(P2 - 1);   // first sample of this lane's part
+              float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
+              float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
               if (e < n3) {
-                const float4 a = M.e0[e];
+                a = M.e0[e];
                 const float4 q = M.e1[e];
                 const float cbv = M.e2[e].x;
                 const float kf = (float)k0 + 0.5f;
                 int kl = (int)floorf((a.x - t0) / c.dt - kf) - 1;
                 int kh = (int)ceilf((a.y - t0) / c.dt - kf) + 1;
-                kl = max(kl, 0);
-                kh = min(kh, last);
-                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
+                kl = max(kl, part0);
+                kh = min(kh, min(last, part0 + P2 - 1));
                 for (int k = kl; k <= kh; ++k) {
                   const float4 s0 = A.s0[k];
                   const float tkk = s0.x;
@@ -884,6 +888,16 @@ __global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderAr
                     }
                   }
                 }
+              }
+              for (int off = P2; off < 32; off <<= 1) {
+                a0 += __shfl_xor_sync(kFull, a0, off);
+                a1 += __shfl_xor_sync(kFull, a1, off);
+                a2 += __shfl_xor_sync(kFull, a2, off);
+                a3 += __shfl_xor_sync(kFull, a3, off);
+                a4 += __shfl_xor_sync(kFull, a4, off);
+                a5 += __shfl_xor_sync(kFull, a5, off);
+              }
+              if (e < n3 && part0 == 0) {
                 float4 v = A.a[e];
                 float2 w2 = A.b[e];
                 v.x += a0; v.y += a1; v.z += a2; v.w += a3;
