@@ -82,6 +82,7 @@ struct RenderArgs {
 struct WarpMem {
   float4 e0[kSlots], e1[kSlots], e2[kSlots];
   int stk[kStk];
+  float stn[kStk];     // entry distance of each stacked node's box (pop-time pruning)
   uint32_t lq[64];     // fetch: queued leaves awaiting the exact test
   unsigned long long kscr[32];   // fetch: candidate sort scratch
   uint32_t pscr[32];
@@ -142,7 +143,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
   const float slack = 1e-5f * (fabsf(seg_lo) + fabsf(seg_hi)) + 1e-6f;
   const float lo_s = seg_lo - slack, hi_s = seg_hi + slack;
   int sp = 1, qn = 0;
-  if (lane == 0) M.stk[0] = 0;
+  if (lane == 0) { M.stk[0] = 0; M.stn[0] = -INFINITY; }
   __syncwarp();
   // Exact leaf tests are batched: box-passing leaves are queued in shared
   // memory and tested 32 at a time (all lanes busy), then the candidates are
@@ -208,7 +209,9 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
   };
   while (sp > 0) {
     const int node = M.stk[sp - 1];
+    const float ntn = M.stn[sp - 1];
     --sp;
+    if (ntn > te_lim + slack) continue;   // the k-buffer filled since it was pushed
     if (lane == 0) cnt.nodes++;
     const WideNode& W = S.wide[node];
     const int child = __ldg(&W.child[lane]);
@@ -240,7 +243,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
       const int np = __popc(im);
       __syncwarp();
       if (sp + np <= kStk) {
-        if (hit && child >= 0) M.stk[sp + rank] = child;
+        if (hit && child >= 0) { M.stk[sp + rank] = child; M.stn[sp + rank] = tn; }
         sp += np;
       } else if (lane == 0) {
         cnt.stackov++;
