@@ -1225,13 +1225,24 @@ void ray_grid(RenderArgs& A, const rg_rays* rays, const rg_camera* cam, dim3& gr
   }
 }
 
+// dynamic shared memory above the 48 KB default needs a per-kernel opt-in
+template <bool BWD, int GW>
+void launch_one(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
+  static bool opted = false;
+  if (!opted) {
+    cudaFuncSetAttribute(k_render<BWD, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    opted = true;
+  }
+  k_render<BWD, GW><<<grid, kBlock, smem, st>>>(A);
+}
+
 template <bool BWD>
 void launch_render(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
   const int B = A.c.slab_samples;
-  if (B >= 5) k_render<BWD, 8><<<grid, kBlock, smem, st>>>(A);
-  else if (B >= 3) k_render<BWD, 4><<<grid, kBlock, smem, st>>>(A);
-  else if (B == 2) k_render<BWD, 2><<<grid, kBlock, smem, st>>>(A);
-  else k_render<BWD, 1><<<grid, kBlock, smem, st>>>(A);
+  if (B >= 5) launch_one<BWD, 8>(A, grid, smem, st);
+  else if (B >= 3) launch_one<BWD, 4>(A, grid, smem, st);
+  else if (B == 2) launch_one<BWD, 2>(A, grid, smem, st);
+  else launch_one<BWD, 1>(A, grid, smem, st);
 }
 
 constexpr size_t kSmemFwd = sizeof(WarpMem) * kWarps;
