@@ -27,6 +27,7 @@
 // burst of float4 atomics (one per lane) into a Morton-ordered buffer;
 // k_finalize converts (mu, M) -> (mu, q, s) and un-permutes.
 #include "rg_internal.cuh"
+#include <cuda_fp16.h>
 
 namespace rg {
 
@@ -42,7 +43,7 @@ constexpr int kTrans = kA;             // transient chunk slots (slab sets > kA)
 constexpr int kRet = kA + 32;          // retired (expired, not yet scattered) slots, backward
 constexpr int kSlots = kA + 64;
 static_assert(kA == 64, "expire/n_in handle two 32-slot chunks");
-constexpr int kStk = 256;              // traversal stack (wide nodes)
+constexpr int kStk = 192;              // traversal stack (wide nodes; max depth seen: C1 45, C3 85)
 constexpr unsigned kFull = 0xffffffffu;
 
 struct Counters {
@@ -82,7 +83,8 @@ struct RenderArgs {
 struct WarpMem {
   float4 e0[kSlots], e1[kSlots], e2[kSlots];
   int stk[kStk];
-  float stn[kStk];     // entry distance of each stacked node's box (pop-time pruning)
+  __half stn[kStk];    // entry distance of each stacked node's box, rounded down (pop-time
+                       // pruning); half keeps the backward block <= 48 KB (196 KB carve-out)
   uint32_t lq[64];     // fetch: queued leaves awaiting the exact test
   unsigned long long kscr[32];   // fetch: candidate sort scratch
   uint32_t pscr[32];
@@ -143,7 +145,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
   const float slack = 1e-5f * (fabsf(seg_lo) + fabsf(seg_hi)) + 1e-6f;
   const float lo_s = seg_lo - slack, hi_s = seg_hi + slack;
   int sp = 1, qn = 0;
-  if (lane == 0) { M.stk[0] = 0; M.stn[0] = -INFINITY; }
+  if (lane == 0) { M.stk[0] = 0; M.stn[0] = __float2half_rd(-INFINITY); }
   __syncwarp();
   // Exact leaf tests are batched: box-passing leaves are queued in shared
   // memory and tested 32 at a time (all lanes busy), then the candidates are
@@ -209,7 +211,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
   };
   while (sp > 0) {
     const int node = M.stk[sp - 1];
-    const float ntn = M.stn[sp - 1];
+    const float ntn = __half2float(M.stn[sp - 1]);
     --sp;
     if (ntn > te_lim + slack) continue;   // the k-buffer filled since it was pushed
     if (lane == 0) cnt.nodes++;
@@ -243,8 +245,11 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
       const int np = __popc(im);
       __syncwarp();
       if (sp + np <= kStk) {
-        if (hit && child >= 0) { M.stk[sp + rank] = child; M.stn[sp + rank] = tn; }
+        if (hit && child >= 0) { M.stk[sp + rank] = child; M.stn[sp + rank] = __float2half_rd(tn); }
         sp += np;
+#ifdef RG_STACK_PROBE
+        if (lane == 0 && (uint32_t)sp > cnt.stackov) cnt.stackov = sp;   // max depth, not overflows
+#endif
       } else if (lane == 0) {
         cnt.stackov++;
       }
@@ -538,6 +543,12 @@ __device__ __forceinline__ void flush_stats(rg_stats* st, const Counters& c, boo
 #pragma unroll
   for (int k = 0; k < 10; ++k) {
     const uint32_t s = __reduce_add_sync(kFull, v[k]);
+#ifdef RG_STACK_PROBE
+    if (k == 9) {
+      if (lane == 0) atomicMax(dst + k, (unsigned long long)c.stackov);
+      continue;
+    }
+#endif
     if (lane == 0 && s) atomicAdd(dst + k, (unsigned long long)s);
   }
 }
@@ -1247,6 +1258,9 @@ void launch_render(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st)
 
 constexpr size_t kSmemFwd = sizeof(WarpMem) * kWarps;
 constexpr size_t kSmemBwd = (sizeof(WarpMem) + sizeof(WarpAcc)) * kWarps;
+// 4 resident backward blocks must fit the 196 KB shared-memory carve-out (1 KB
+// reserved per block): a larger carve-out halves L1 and costs ~6% (measured)
+static_assert(kSmemBwd <= 48 * 1024 + 128, "backward block exceeds the 196 KB carve-out budget");
 
 // fetch-log layout (rg_internal.cuh): counter | per-ray records | arena
 void set_log(RenderArgs& A, const void* log, size_t log_bytes, int n_rays) {
