@@ -34,7 +34,10 @@ namespace rg {
 namespace {
 
 #ifndef RG_MIN_BLOCKS
-#define RG_MIN_BLOCKS 4                // resident blocks per SM the register budget targets
+#define RG_MIN_BLOCKS 4                // resident blocks per SM the register budget targets (bwd)
+#endif
+#ifndef RG_MIN_BLOCKS_FWD
+#define RG_MIN_BLOCKS_FWD RG_MIN_BLOCKS   // forward (no WarpAcc: smem allows more blocks)
 #endif
 constexpr int kWarps = 4;              // rays (warps) per block
 constexpr int kBlock = 32 * kWarps;
@@ -573,7 +576,7 @@ __device__ __forceinline__ void dbg_put(const RenderArgs& P, int ray, int& dbg_n
 }
 
 template <bool BWD, int GW>
-__global__ void __launch_bounds__(kBlock, RG_MIN_BLOCKS) k_render(const RenderArgs P) {
+__global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FWD) k_render(const RenderArgs P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const unsigned lane = lane_id();
   const int wid = threadIdx.x >> 5;

@@ -3,6 +3,8 @@ import sys, time, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2408_03356_b200 import rg, synth
+nostats = "--nostats" in sys.argv
+sys.argv = [a for a in sys.argv if a != "--nostats"]
 name = sys.argv[1] if len(sys.argv) > 1 else "blender"
 wl = synth.workload(name)
 sc, cam, p = wl.scene, wl.cameras[0], wl.params
@@ -14,7 +16,7 @@ for it in range(3):
     st = rg.new_stats()
     e0, e1, e2, e3 = ev(), ev(), ev(), ev()
     e0.record(); b = rg.build_bvh(g, cfg); e1.record()
-    f = rg.render_forward(g, b, cfg, camera=cam, stats=st, log=lg); e2.record()
+    f = rg.render_forward(g, b, cfg, camera=cam, stats=None if nostats else st, log=lg); e2.record()
     up = torch.full_like(f["rgb"], 1.0 / f["rgb"].numel())
     gr = rg.render_backward(g, b, cfg, f, up, camera=cam); e3.record()
     torch.cuda.synchronize()
