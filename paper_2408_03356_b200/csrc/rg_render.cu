@@ -86,8 +86,9 @@ struct RenderArgs {
 struct WarpMem {
   float4 e0[kSlots], e1[kSlots], e2[kSlots];
   int stk[kStk];
-  __half stn[kStk];    // entry distance of each stacked node's box, rounded down (pop-time
-                       // pruning); half keeps the backward block <= 48 KB (196 KB carve-out)
+  uint16_t stn[kStk];  // entry distance of each stacked node's box: half rounded down, as an
+                       // order-preserving 16-bit key (pop-time selection and pruning); 16 bits
+                       // keep the backward block <= 48 KB (196 KB carve-out)
   uint32_t lq[64];     // fetch: queued leaves awaiting the exact test
   unsigned long long kscr[32];   // fetch: candidate sort scratch
   uint32_t pscr[32];
@@ -130,6 +131,17 @@ struct Ray {
   float3 o, d, inv, oinv;
 };
 
+// entry distance <-> order-preserving 16-bit key (fp16 rounded toward -inf:
+// a decoded key never exceeds the distance, so pruning on it is conservative)
+__device__ __forceinline__ uint16_t stn_enc(float t) {
+  const unsigned short b = __half_as_ushort(__float2half_rd(t));
+  return (b & 0x8000u) ? (uint16_t)(~b & 0xFFFFu) : (uint16_t)(b | 0x8000u);
+}
+__device__ __forceinline__ float stn_dec(uint16_t k) {
+  const unsigned short b = (k & 0x8000u) ? (unsigned short)(k & 0x7FFFu) : (unsigned short)(~k & 0xFFFFu);
+  return __half2float(__ushort_as_half(b));
+}
+
 // Warp-cooperative k-nearest query on the 32-wide BVH: the kmax (<= 32)
 // smallest keys (t_entry bits, index) > cursor among Gaussians whose exact
 // support interval satisfies t_exit >= seg_lo and t_entry <= seg_hi.
@@ -148,7 +160,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
   const float slack = 1e-5f * (fabsf(seg_lo) + fabsf(seg_hi)) + 1e-6f;
   const float lo_s = seg_lo - slack, hi_s = seg_hi + slack;
   int sp = 1, qn = 0;
-  if (lane == 0) { M.stk[0] = 0; M.stn[0] = __float2half_rd(-INFINITY); }
+  if (lane == 0) { M.stk[0] = 0; M.stn[0] = stn_enc(-INFINITY); }
   __syncwarp();
   // Exact leaf tests are batched: box-passing leaves are queued in shared
   // memory and tested 32 at a time (all lanes busy), then the candidates are
@@ -213,10 +225,31 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
     }
   };
   while (sp > 0) {
+#ifdef RG_SORTED_PUSH
     const int node = M.stk[sp - 1];
-    const float ntn = __half2float(M.stn[sp - 1]);
+    const float ntn = stn_dec(M.stn[sp - 1]);
     --sp;
     if (ntn > te_lim + slack) continue;   // the k-buffer filled since it was pushed
+#else
+    // pop the node with the smallest entry distance among the top 32 (approximately
+    // best-first); when even that one lies beyond the k-th key, drop all 32
+    int node;
+    {
+      const int nwin = min(sp, 32);
+      const unsigned k16 = (int)lane < nwin ? (unsigned)M.stn[sp - 1 - (int)lane] : 0xFFFFu;
+      const unsigned kmin = __reduce_min_sync(kFull, k16);
+      if (stn_dec((uint16_t)kmin) > te_lim + slack) {
+        sp -= nwin;
+        continue;
+      }
+      const int si = sp - 1 - (__ffs(__ballot_sync(kFull, k16 == kmin)) - 1);
+      node = M.stk[si];
+      __syncwarp();
+      if (lane == 0 && si != sp - 1) { M.stk[si] = M.stk[sp - 1]; M.stn[si] = M.stn[sp - 1]; }
+      --sp;
+      __syncwarp();
+    }
+#endif
     if (lane == 0) cnt.nodes++;
     const WideNode& W = S.wide[node];
     const int child = __ldg(&W.child[lane]);
@@ -234,9 +267,10 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
         qn += __popc(lm);
       }
     }
-    // internal children: push sorted so that the nearest is on top
+    // internal children
     const unsigned im = __ballot_sync(kFull, hit && child >= 0);
     if (im) {
+#ifdef RG_SORTED_PUSH   // pushed sorted so that the nearest is on top
       int rank = 0;
       unsigned mm = im;
       while (mm) {
@@ -245,10 +279,13 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
         const float tb = __shfl_sync(kFull, tn, b);
         rank += (tb > tn) || (tb == tn && b < (int)lane);
       }
+#else                   // any order: the pop selects
+      const int rank = __popc(im & lt_mask);
+#endif
       const int np = __popc(im);
       __syncwarp();
       if (sp + np <= kStk) {
-        if (hit && child >= 0) { M.stk[sp + rank] = child; M.stn[sp + rank] = __float2half_rd(tn); }
+        if (hit && child >= 0) { M.stk[sp + rank] = child; M.stn[sp + rank] = stn_enc(tn); }
         sp += np;
 #ifdef RG_STACK_PROBE
         if (lane == 0 && (uint32_t)sp > cnt.stackov) cnt.stackov = sp;   // max depth, not overflows
