@@ -61,7 +61,9 @@ struct WideNode {
   float lox[kWide], loy[kWide], loz[kWide], hix[kWide], hiy[kWide], hiz[kWide];
   int child[kWide];
 };
-__host__ __device__ inline size_t wide_capacity(int n) { return (size_t)(n / 2 + 2); }
+__host__ __device__ constexpr size_t wide_capacity(int n) { return (size_t)(n / 2 + 2); }
+// largest scene: the traversal stack packs wide-node ids into 22 bits
+constexpr int kMaxGaussians = (1 << 23) - 8;
 
 struct SceneView {
   const float4* geom;

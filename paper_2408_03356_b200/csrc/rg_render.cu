@@ -46,7 +46,7 @@ constexpr int kTrans = kA;             // transient chunk slots (slab sets > kA)
 constexpr int kRet = kA + 32;          // retired (expired, not yet scattered) slots, backward
 constexpr int kSlots = kA + 64;
 static_assert(kA == 64, "expire/n_in handle two 32-slot chunks");
-constexpr int kStk = 192;              // traversal stack (wide nodes; max depth seen: C1 45, C3 85)
+constexpr int kStk = 320;              // traversal stack (wide nodes; max depth seen: C1 56, C3 149)
 constexpr unsigned kFull = 0xffffffffu;
 
 struct Counters {
@@ -85,10 +85,9 @@ struct RenderArgs {
 //   e0 = {t_entry, t_exit, t_mid, c0}   e1 = {c1, c2, r, g}   e2 = {b, pos, idx, -}
 struct WarpMem {
   float4 e0[kSlots], e1[kSlots], e2[kSlots];
-  int stk[kStk];
-  uint16_t stn[kStk];  // entry distance of each stacked node's box: half rounded down, as an
-                       // order-preserving 16-bit key (pop-time selection and pruning); 16 bits
-                       // keep the backward block <= 48 KB (196 KB carve-out)
+  uint32_t stk[kStk];  // stacked node: (10-bit order key of its box's entry distance, rounded
+                       // down) << 22 | wide node id; one word keeps the backward block
+                       // <= 48 KB (196 KB carve-out)
   uint32_t lq[64];     // fetch: queued leaves awaiting the exact test
   unsigned long long kscr[32];   // fetch: candidate sort scratch
   uint32_t pscr[32];
@@ -131,15 +130,20 @@ struct Ray {
   float3 o, d, inv, oinv;
 };
 
-// entry distance <-> order-preserving 16-bit key (fp16 rounded toward -inf:
-// a decoded key never exceeds the distance, so pruning on it is conservative)
-__device__ __forceinline__ uint16_t stn_enc(float t) {
-  const unsigned short b = __half_as_ushort(__float2half_rd(t));
-  return (b & 0x8000u) ? (uint16_t)(~b & 0xFFFFu) : (uint16_t)(b | 0x8000u);
+// stack word: order-preserving 10-bit key of the entry distance (fp16 rounded
+// toward -inf, low 6 mantissa bits dropped toward -inf: a decoded key never
+// exceeds the distance, so pruning on it is conservative) | 22-bit node id
+constexpr uint32_t kNodeBits = 22;
+static_assert(wide_capacity(kMaxGaussians) <= (1u << kNodeBits), "node ids must fit the stack word");
+__device__ __forceinline__ uint32_t stk_enc(float t, int node) {
+  const unsigned b = __half_as_ushort(__float2half_rd(t));
+  const unsigned k16 = (b & 0x8000u) ? (~b & 0xFFFFu) : (b | 0x8000u);
+  return ((k16 >> 6) << kNodeBits) | (uint32_t)node;
 }
-__device__ __forceinline__ float stn_dec(uint16_t k) {
-  const unsigned short b = (k & 0x8000u) ? (unsigned short)(k & 0x7FFFu) : (unsigned short)(~k & 0xFFFFu);
-  return __half2float(__ushort_as_half(b));
+__device__ __forceinline__ float stk_dist(uint32_t w) {
+  const unsigned k16 = (w >> kNodeBits) << 6;
+  const unsigned b = (k16 & 0x8000u) ? (k16 & 0x7FFFu) : (~k16 & 0xFFFFu);
+  return __half2float(__ushort_as_half((unsigned short)b));
 }
 
 // Warp-cooperative k-nearest query on the 32-wide BVH: the kmax (<= 32)
@@ -160,7 +164,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
   const float slack = 1e-5f * (fabsf(seg_lo) + fabsf(seg_hi)) + 1e-6f;
   const float lo_s = seg_lo - slack, hi_s = seg_hi + slack;
   int sp = 1, qn = 0;
-  if (lane == 0) { M.stk[0] = 0; M.stn[0] = stn_enc(-INFINITY); }
+  if (lane == 0) M.stk[0] = stk_enc(-INFINITY, 0);
   __syncwarp();
   // Exact leaf tests are batched: box-passing leaves are queued in shared
   // memory and tested 32 at a time (all lanes busy), then the candidates are
@@ -226,26 +230,26 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
   };
   while (sp > 0) {
 #ifdef RG_SORTED_PUSH
-    const int node = M.stk[sp - 1];
-    const float ntn = stn_dec(M.stn[sp - 1]);
+    const uint32_t top = M.stk[sp - 1];
+    const int node = (int)(top & ((1u << kNodeBits) - 1u));
     --sp;
-    if (ntn > te_lim + slack) continue;   // the k-buffer filled since it was pushed
+    if (stk_dist(top) > te_lim + slack) continue;   // the k-buffer filled since it was pushed
 #else
     // pop the node with the smallest entry distance among the top 32 (approximately
     // best-first); when even that one lies beyond the k-th key, drop all 32
     int node;
     {
       const int nwin = min(sp, 32);
-      const unsigned k16 = (int)lane < nwin ? (unsigned)M.stn[sp - 1 - (int)lane] : 0xFFFFu;
-      const unsigned kmin = __reduce_min_sync(kFull, k16);
-      if (stn_dec((uint16_t)kmin) > te_lim + slack) {
+      const uint32_t w = (int)lane < nwin ? M.stk[sp - 1 - (int)lane] : 0xFFFFFFFFu;
+      const uint32_t wmin = __reduce_min_sync(kFull, w);
+      if (stk_dist(wmin) > te_lim + slack) {
         sp -= nwin;
         continue;
       }
-      const int si = sp - 1 - (__ffs(__ballot_sync(kFull, k16 == kmin)) - 1);
-      node = M.stk[si];
+      node = (int)(wmin & ((1u << kNodeBits) - 1u));
+      const int si = sp - 1 - (__ffs(__ballot_sync(kFull, w == wmin)) - 1);
       __syncwarp();
-      if (lane == 0 && si != sp - 1) { M.stk[si] = M.stk[sp - 1]; M.stn[si] = M.stn[sp - 1]; }
+      if (lane == 0 && si != sp - 1) M.stk[si] = M.stk[sp - 1];
       --sp;
       __syncwarp();
     }
@@ -285,7 +289,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
       const int np = __popc(im);
       __syncwarp();
       if (sp + np <= kStk) {
-        if (hit && child >= 0) { M.stk[sp + rank] = child; M.stn[sp + rank] = stn_enc(tn); }
+        if (hit && child >= 0) M.stk[sp + rank] = stk_enc(tn, child);
         sp += np;
 #ifdef RG_STACK_PROBE
         if (lane == 0 && (uint32_t)sp > cnt.stackov) cnt.stackov = sp;   // max depth, not overflows
