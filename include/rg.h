@@ -49,8 +49,7 @@ typedef enum {
 
 /* Scene parameters P = {(sigma~, c~, mu, q, s)}. */
 typedef struct {
-  int32_t n;          /* number of Gaussians, 0 <= n <= 8388600 (RG_ERR_INVALID_ARG above:
-                         the traversal stack packs 22-bit wide-node ids) */
+  int32_t n;          /* number of Gaussians, >= 0 */
   int32_t sh_degree;  /* L1 of Eq. 14, 0..3 */
   int32_t sg_count;   /* number of SG lobes (Eq. 15), 0..7 */
   int32_t pad_;
@@ -137,8 +136,7 @@ unsigned long long rg_kernel_launches(void);
 
 /* ---- BVH build -------------------------------- */
 /* Workspace bytes for rg_build_bvh on n Gaussians with the given appearance
-   sizes (0 for invalid sizes, incl. n > 8388600).  The workspace must be
-   256-B aligned. */
+   sizes (0 for invalid sizes).  The workspace must be 256-B aligned. */
 size_t rg_bvh_workspace_bytes(int32_t n, int32_t sh_degree, int32_t sg_count);
 
 /* Preprocess (R(q), M = S^-1 R^T, support radius, padded tight AABB: P:176-183,

@@ -30,7 +30,7 @@ bool config_ok(const rg_config* c) {
 }
 
 bool gaussians_ok(const rg_gaussians* g) {
-  if (!g || g->n < 0 || g->n > kMaxGaussians) return false;
+  if (!g || g->n < 0) return false;
   if (g->sh_degree < 0 || g->sh_degree > kMaxDeg) return false;
   if (g->sg_count < 0 || g->sg_count > kMaxLobes) return false;
   if (g->n == 0) return true;
@@ -77,7 +77,7 @@ const char* rg_version(void) {
 }
 
 size_t rg_bvh_workspace_bytes(int32_t n, int32_t sh_degree, int32_t sg_count) {
-  if (n < 0 || n > kMaxGaussians || sh_degree < 0 || sh_degree > kMaxDeg || sg_count < 0 || sg_count > kMaxLobes)
+  if (n < 0 || sh_degree < 0 || sh_degree > kMaxDeg || sg_count < 0 || sg_count > kMaxLobes)
     return 0;
   return bvh_layout(n, sh_degree, sg_count).total;
 }
@@ -149,7 +149,7 @@ size_t rg_fetch_log_bytes(int32_t n_rays, int32_t pairs_per_ray) {
 }
 
 size_t rg_backward_workspace_bytes(int32_t n, int32_t sh_degree, int32_t sg_count) {
-  if (n < 0 || n > kMaxGaussians || sh_degree < 0 || sh_degree > kMaxDeg || sg_count < 0 || sg_count > kMaxLobes)
+  if (n < 0 || sh_degree < 0 || sh_degree > kMaxDeg || sg_count < 0 || sg_count > kMaxLobes)
     return 0;
   return sizeof(float) * (size_t)grad_stride(sh_degree, sg_count) * (size_t)(n > 0 ? n : 1);
 }

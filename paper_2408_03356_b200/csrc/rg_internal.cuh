@@ -62,8 +62,6 @@ struct WideNode {
   int child[kWide];
 };
 __host__ __device__ constexpr size_t wide_capacity(int n) { return (size_t)(n / 2 + 2); }
-// largest scene: the traversal stack packs wide-node ids into 22 bits
-constexpr int kMaxGaussians = (1 << 23) - 8;
 
 struct SceneView {
   const float4* geom;

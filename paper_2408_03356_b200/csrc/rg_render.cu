@@ -46,7 +46,7 @@ constexpr int kTrans = kA;             // transient chunk slots (slab sets > kA)
 constexpr int kRet = kA + 32;          // retired (expired, not yet scattered) slots, backward
 constexpr int kSlots = kA + 64;
 static_assert(kA == 64, "expire/n_in handle two 32-slot chunks");
-constexpr int kStk = 320;              // traversal stack (wide nodes; max depth seen: C1 56, C3 149)
+constexpr int kStk = 240;              // traversal stack (wide nodes; max depth seen: C1 56, C3 149)
 constexpr unsigned kFull = 0xffffffffu;
 
 struct Counters {
@@ -85,12 +85,10 @@ struct RenderArgs {
 //   e0 = {t_entry, t_exit, t_mid, c0}   e1 = {c1, c2, r, g}   e2 = {b, pos, idx, -}
 struct WarpMem {
   float4 e0[kSlots], e1[kSlots], e2[kSlots];
-  uint32_t stk[kStk];  // stacked node: (10-bit order key of its box's entry distance, rounded
-                       // down) << 22 | wide node id; one word keeps the backward block
-                       // <= 48 KB (196 KB carve-out)
+  uint32_t stk[kStk];  // stacked wide node ids
+  uint16_t stn[kStk];  // their boxes' entry distances as 16-bit order keys (fp16 rounded
+                       // down): pop-time selection and pruning
   uint32_t lq[64];     // fetch: queued leaves awaiting the exact test
-  unsigned long long kscr[32];   // fetch: candidate sort scratch
-  uint32_t pscr[32];
   float Y[16];
 };
 struct WarpAcc {
@@ -130,19 +128,14 @@ struct Ray {
   float3 o, d, inv, oinv;
 };
 
-// stack word: order-preserving 10-bit key of the entry distance (fp16 rounded
-// toward -inf, low 6 mantissa bits dropped toward -inf: a decoded key never
-// exceeds the distance, so pruning on it is conservative) | 22-bit node id
-constexpr uint32_t kNodeBits = 22;
-static_assert(wide_capacity(kMaxGaussians) <= (1u << kNodeBits), "node ids must fit the stack word");
-__device__ __forceinline__ uint32_t stk_enc(float t, int node) {
+// entry distance <-> order-preserving 16-bit key (fp16 rounded toward -inf:
+// a decoded key never exceeds the distance, so pruning on it is conservative)
+__device__ __forceinline__ uint16_t stn_enc(float t) {
   const unsigned b = __half_as_ushort(__float2half_rd(t));
-  const unsigned k16 = (b & 0x8000u) ? (~b & 0xFFFFu) : (b | 0x8000u);
-  return ((k16 >> 6) << kNodeBits) | (uint32_t)node;
+  return (uint16_t)((b & 0x8000u) ? (~b & 0xFFFFu) : (b | 0x8000u));
 }
-__device__ __forceinline__ float stk_dist(uint32_t w) {
-  const unsigned k16 = (w >> kNodeBits) << 6;
-  const unsigned b = (k16 & 0x8000u) ? (k16 & 0x7FFFu) : (~k16 & 0xFFFFu);
+__device__ __forceinline__ float stn_dec(unsigned k) {
+  const unsigned b = (k & 0x8000u) ? (k & 0x7FFFu) : (~k & 0xFFFFu);
   return __half2float(__ushort_as_half((unsigned short)b));
 }
 
@@ -156,6 +149,9 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
   const unsigned lane = lane_id();
   const unsigned lt_mask = (1u << lane) - 1u;
   if (lane == 0) cnt.fetches++;
+  // candidate sort scratch aliases the transient slots, dead during every fetch
+  unsigned long long* const kscr = reinterpret_cast<unsigned long long*>(&M.e0[kTrans]);
+  uint32_t* const pscr = reinterpret_cast<uint32_t*>(&M.e1[kTrans]);
   key = ~0ull;
   pos = 0;
   int nk = 0;
@@ -164,7 +160,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
   const float slack = 1e-5f * (fabsf(seg_lo) + fabsf(seg_hi)) + 1e-6f;
   const float lo_s = seg_lo - slack, hi_s = seg_hi + slack;
   int sp = 1, qn = 0;
-  if (lane == 0) M.stk[0] = stk_enc(-INFINITY, 0);
+  if (lane == 0) { M.stk[0] = 0; M.stn[0] = stn_enc(-INFINITY); }
   __syncwarp();
   // Exact leaf tests are batched: box-passing leaves are queued in shared
   // memory and tested 32 at a time (all lanes busy), then the candidates are
@@ -202,12 +198,12 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
         const unsigned long long kb = shfl64(ck, b);
         crank += (cand && kb < ck) ? 1 : 0;
       }
-      if (cand) { M.kscr[crank] = ck; M.pscr[crank] = cp; }
+      if (cand) { kscr[crank] = ck; pscr[crank] = cp; }
       __syncwarp();
       const int ncand = __popc(cmask);
-      ck = (int)lane < ncand ? M.kscr[lane] : ~0ull;
+      ck = (int)lane < ncand ? kscr[lane] : ~0ull;
     }
-    uint32_t cpos = M.pscr[lane];
+    uint32_t cpos = pscr[lane];
     __syncwarp();
     // the 32 smallest of (k-buffer, candidates) form a bitonic sequence: merge
     {
@@ -230,26 +226,26 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
   };
   while (sp > 0) {
 #ifdef RG_SORTED_PUSH
-    const uint32_t top = M.stk[sp - 1];
-    const int node = (int)(top & ((1u << kNodeBits) - 1u));
+    const int node = (int)M.stk[sp - 1];
+    const float ntn = stn_dec(M.stn[sp - 1]);
     --sp;
-    if (stk_dist(top) > te_lim + slack) continue;   // the k-buffer filled since it was pushed
+    if (ntn > te_lim + slack) continue;   // the k-buffer filled since it was pushed
 #else
     // pop the node with the smallest entry distance among the top 32 (approximately
     // best-first); when even that one lies beyond the k-th key, drop all 32
     int node;
     {
       const int nwin = min(sp, 32);
-      const uint32_t w = (int)lane < nwin ? M.stk[sp - 1 - (int)lane] : 0xFFFFFFFFu;
-      const uint32_t wmin = __reduce_min_sync(kFull, w);
-      if (stk_dist(wmin) > te_lim + slack) {
+      const unsigned k16 = (int)lane < nwin ? (unsigned)M.stn[sp - 1 - (int)lane] : 0xFFFFu;
+      const unsigned kmin = __reduce_min_sync(kFull, k16);
+      if (stn_dec(kmin) > te_lim + slack) {
         sp -= nwin;
         continue;
       }
-      node = (int)(wmin & ((1u << kNodeBits) - 1u));
-      const int si = sp - 1 - (__ffs(__ballot_sync(kFull, w == wmin)) - 1);
+      const int si = sp - 1 - (__ffs(__ballot_sync(kFull, k16 == kmin)) - 1);
+      node = (int)M.stk[si];
       __syncwarp();
-      if (lane == 0 && si != sp - 1) M.stk[si] = M.stk[sp - 1];
+      if (lane == 0 && si != sp - 1) { M.stk[si] = M.stk[sp - 1]; M.stn[si] = M.stn[sp - 1]; }
       --sp;
       __syncwarp();
     }
@@ -289,7 +285,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
       const int np = __popc(im);
       __syncwarp();
       if (sp + np <= kStk) {
-        if (hit && child >= 0) M.stk[sp + rank] = stk_enc(tn, child);
+        if (hit && child >= 0) { M.stk[sp + rank] = (uint32_t)child; M.stn[sp + rank] = stn_enc(tn); }
         sp += np;
 #ifdef RG_STACK_PROBE
         if (lane == 0 && (uint32_t)sp > cnt.stackov) cnt.stackov = sp;   // max depth, not overflows
