@@ -306,6 +306,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
 // coefficient SH region of the record needs no predicate); SG lobes at 48+7j.
 __device__ __forceinline__ float3 pair_color(const SceneView& S, const WarpMem& M, int pos,
                                              const float3& d) {
+#ifdef RG_SCALAR_COLOR
   const float* ap = S.app + (size_t)pos * S.app_stride;
   float r = 0.f, g = 0.f, b = 0.f;
 #pragma unroll
@@ -323,6 +324,44 @@ __device__ __forceinline__ float3 pair_color(const SceneView& S, const WarpMem& 
     b = fmaf(__ldg(q + 2), e, b);
   }
   return make_float3(r, g, b);
+#else
+  // 16-B loads: the record is 16-B aligned, SH [m][3] in floats 0..47, lobe j in
+  // floats 48+7j..54+7j (2 or 3 float4s, neighbours re-read from L1)
+  const float4* a4 = reinterpret_cast<const float4*>(S.app + (size_t)pos * S.app_stride);
+  float acc[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < kShFloats / 4; ++i) {
+    const float4 v = __ldg(a4 + i);
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int f = 4 * i + k;
+      acc[f % 3] = fmaf(M.Y[f / 3], vv[k], acc[f % 3]);
+    }
+  }
+  const int L = S.lobes;
+#pragma unroll
+  for (int j = 0; j < kMaxLobes; ++j) {
+    if (j >= L) break;
+    const int f0 = kShFloats + 7 * j;           // compile-time after unrolling
+    const int i0 = f0 / 4, i1 = (f0 + 6) / 4;   // float4s covering the lobe (2 or 3)
+    float w[12];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      if (i0 + i <= i1) {
+        const float4 v = __ldg(a4 + i0 + i);
+        w[4 * i] = v.x; w[4 * i + 1] = v.y; w[4 * i + 2] = v.z; w[4 * i + 3] = v.w;
+      }
+    }
+    const float* p = w + (f0 - 4 * i0);
+    const float dp = d.x * p[4] + d.y * p[5] + d.z * p[6];
+    const float e = ex2_approx(p[3] * (dp - 1.0f) * kLog2e);
+    acc[0] = fmaf(p[0], e, acc[0]);
+    acc[1] = fmaf(p[1], e, acc[1]);
+    acc[2] = fmaf(p[2], e, acc[2]);
+  }
+  return make_float3(acc[0], acc[1], acc[2]);
+#endif
 }
 
 // Per-(ray, Gaussian) set-up into slot `sl`: exact interval and the exponent
