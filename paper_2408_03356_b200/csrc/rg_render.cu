@@ -304,9 +304,12 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
 // c_l(d) = sum_m c~_m Y_m(d) + sum_j k_j e^{lambda_j (d.p_j - 1)} (Eq. 14-15):
 // Y(d) is per-ray in shared memory (zero past the degree, so the fixed 16-
 // coefficient SH region of the record needs no predicate); SG lobes at 48+7j.
+// VEC: 16-B loads (forward: -5% time); scalar loads in the backward, where the
+// extra registers of the vector form cost more (+3%) than they save
+template <bool VEC>
 __device__ __forceinline__ float3 pair_color(const SceneView& S, const WarpMem& M, int pos,
                                              const float3& d) {
-#ifdef RG_SCALAR_COLOR
+  if (!VEC) {
   const float* ap = S.app + (size_t)pos * S.app_stride;
   float r = 0.f, g = 0.f, b = 0.f;
 #pragma unroll
@@ -324,7 +327,7 @@ __device__ __forceinline__ float3 pair_color(const SceneView& S, const WarpMem& 
     b = fmaf(__ldg(q + 2), e, b);
   }
   return make_float3(r, g, b);
-#else
+  }
   // 16-B loads: the record is 16-B aligned, SH [m][3] in floats 0..47, lobe j in
   // floats 48+7j..54+7j (2 or 3 float4s, neighbours re-read from L1)
   const float4* a4 = reinterpret_cast<const float4*>(S.app + (size_t)pos * S.app_stride);
@@ -361,7 +364,6 @@ __device__ __forceinline__ float3 pair_color(const SceneView& S, const WarpMem& 
     acc[2] = fmaf(p[2], e, acc[2]);
   }
   return make_float3(acc[0], acc[1], acc[2]);
-#endif
 }
 
 // Per-(ray, Gaussian) set-up into slot `sl`: exact interval and the exponent
@@ -379,6 +381,7 @@ __device__ __forceinline__ float3 pair_color(const SceneView& S, const WarpMem& 
 #else
 #define RG_SCATTER_ATTR __forceinline__
 #endif
+template <bool VEC>
 __device__ RG_SETUP_ATTR void setup_pair(const SceneView& S, WarpMem& M, int sl, const Ray& R,
                                         uint32_t pos) {
   const float4* gp = S.geom + 4 * (size_t)pos;
@@ -393,7 +396,7 @@ __device__ RG_SETUP_ATTR void setup_pair(const SceneView& S, WarpMem& M, int sl,
   const float u2 = g2.z * x0 + g2.w * x1 + g3.x * x2;
   const float qm = u0 * u0 + u1 * u1 + u2 * u2;
   const float b1 = u0 * pg.dl0 + u1 * pg.dl1 + u2 * pg.dl2;
-  const float3 col = pair_color(S, M, (int)pos, R.d);
+  const float3 col = pair_color<VEC>(S, M, (int)pos, R.d);
   M.e0[sl] = make_float4(pg.te, pg.tx, pg.tm, lg2_approx(g0.w) - 0.5f * kLog2e * qm);
   M.e1[sl] = make_float4(-kLog2e * b1, -0.5f * kLog2e * pg.A, col.x, col.y);
   M.e2[sl] = make_float4(col.z, __int_as_float((int)pos), g3.z, 0.f);
@@ -796,7 +799,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
           }
         } else {
           got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
-          if ((int)lane < got) setup_pair(P.S, M, count + (int)lane, R, pos);
+          if ((int)lane < got) setup_pair<!BWD>(P.S, M, count + (int)lane, R, pos);
           if (!BWD && log_ok) {
             unsigned long long off = 0;
             if (lane == 0 && got > 0) off = atomicAdd(P.arena_ctr, (unsigned long long)got);
@@ -1045,7 +1048,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             unsigned long long key;
             uint32_t pos;
             const int got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
-            if ((int)lane < got) setup_pair(P.S, M, kTrans + (int)lane, R, pos);
+            if ((int)lane < got) setup_pair<!BWD>(P.S, M, kTrans + (int)lane, R, pos);
             __syncwarp();
             eval_range<GW>(M, kA, kA + got, L, tk, val, sg, sr, sgg, sb, ev);
             if (dbg && g0 == 0) dbg_put(P, ray, dbg_n, s, got, M, kA);
@@ -1133,7 +1136,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
               uint32_t pos;
               const int got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
               if ((int)lane < got) {
-                setup_pair(P.S, M, kTrans + (int)lane, R, pos);
+                setup_pair<!BWD>(P.S, M, kTrans + (int)lane, R, pos);
                 A.a[kA + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
                 A.b[kA + lane] = make_float2(0.f, 0.f);
               }
