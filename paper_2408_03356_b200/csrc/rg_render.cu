@@ -654,7 +654,9 @@ __device__ __forceinline__ void dbg_put(const RenderArgs& P, int ray, int& dbg_n
   dbg_n = min(P.dbg_cap, dbg_n + n);
 }
 
-template <bool BWD, int GW>
+// INSTR: counters (rg_stats) and the debug dump; the uninstrumented variant
+// compiles them out (8 fewer live registers through the march)
+template <bool BWD, int GW, bool INSTR>
 __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FWD) k_render(const RenderArgs P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const unsigned lane = lane_id();
@@ -683,7 +685,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
   float tau = 0.f, tauc = 0.f, T = 1.f;
   int replay = -1;
   Counters cnt = {};
-  const bool dbg = (!BWD) && P.dbg_rec != nullptr && ray < P.dbg_rays;
+  const bool dbg = INSTR && (!BWD) && P.dbg_rec != nullptr && ray < P.dbg_rays;
   int dbg_n = 0;
   float gr0 = 0.f, gr1 = 0.f, gr2 = 0.f, Pp0 = 0.f, Pp1 = 0.f, Pp2 = 0.f;
   int replay_in = -1;
@@ -903,7 +905,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
           const bool inwin = (int)lane <= last;
           const bool live = live0 && inwin;
           // per-slab sets (counters, debug dump): members of slab s+w, key order
-          for (int w = 0; w <= wlast && (P.stats != nullptr || dbg); ++w) {
+          for (int w = 0; w <= wlast && INSTR && (P.stats != nullptr || dbg); ++w) {
             const float lo_w = fma_((float)(k0 + 8 * w), c.dt, t0);
             if (!(sample_t(k0 + 8 * w, c.dt, t0) < t1)) break;
             const float hi_w = fminf(t1, fma_((float)(k0 + 8 * w + 8), c.dt, t0));
@@ -1178,9 +1180,9 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
     P.rgb[3 * ray + 2] = C2 + T * c.background[2];
     P.T[ray] = T;
     P.replay[ray] = replay;
-    if (P.dbg_counts && ray < P.dbg_rays) P.dbg_counts[ray] = dbg_n;
+    if (INSTR && P.dbg_counts && ray < P.dbg_rays) P.dbg_counts[ray] = dbg_n;
   }
-  if (P.stats) flush_stats(P.stats, cnt, hit);
+  if (INSTR && P.stats) flush_stats(P.stats, cnt, hit);
 }
 
 // (mu, M) -> (mu, q, s) and Morton -> caller order
@@ -1319,23 +1321,30 @@ void ray_grid(RenderArgs& A, const rg_rays* rays, const rg_camera* cam, dim3& gr
 }
 
 // dynamic shared memory above the 48 KB default needs a per-kernel opt-in
-template <bool BWD, int GW>
+template <bool BWD, int GW, bool INSTR>
 void launch_one(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
   static bool opted = false;
   if (!opted) {
-    cudaFuncSetAttribute(k_render<BWD, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_render<BWD, GW, INSTR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     opted = true;
   }
-  k_render<BWD, GW><<<grid, kBlock, smem, st>>>(A);
+  k_render<BWD, GW, INSTR><<<grid, kBlock, smem, st>>>(A);
+}
+
+template <bool BWD, int GW>
+void launch_gw(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
+  if (A.stats != nullptr || A.dbg_rec != nullptr) launch_one<BWD, GW, true>(A, grid, smem, st);
+  else launch_one<BWD, GW, false>(A, grid, smem, st);
 }
 
 template <bool BWD>
 void launch_render(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
   const int B = A.c.slab_samples;
-  if (B >= 5) launch_one<BWD, 8>(A, grid, smem, st);
-  else if (B >= 3) launch_one<BWD, 4>(A, grid, smem, st);
-  else if (B == 2) launch_one<BWD, 2>(A, grid, smem, st);
-  else launch_one<BWD, 1>(A, grid, smem, st);
+  if (B >= 5) launch_gw<BWD, 8>(A, grid, smem, st);
+  else if (B >= 3) launch_gw<BWD, 4>(A, grid, smem, st);
+  else if (B == 2) launch_gw<BWD, 2>(A, grid, smem, st);
+  else launch_gw<BWD, 1>(A, grid, smem, st);
 }
 
 constexpr size_t kSmemFwd = sizeof(WarpMem) * kWarps;

@@ -1,6 +1,10 @@
 """Group ncu per-instruction metrics of a kernel into source regions (dev tool).
-usage: ncu_regions.py report kernel-substring"""
+usage: ncu_regions.py report kernel-substring [--rev GIT_REV]
+--rev reads the sources of the profiled build from git (line numbers drift)"""
 import collections, csv, re, subprocess, sys
+REV = None
+if "--rev" in sys.argv:
+    i = sys.argv.index("--rev"); REV = sys.argv[i + 1]; del sys.argv[i:i + 2]
 rep, ksub = sys.argv[1], sys.argv[2]
 import os
 CSRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
@@ -9,7 +13,12 @@ def auto_regions():
     """function definitions and '// ---- label' markers delimit regions"""
     reg = []
     for fn in ("rg_render.cu", "rg_internal.cuh"):
-        lines = open(os.path.join(CSRC, fn)).read().splitlines()
+        if REV:
+            lines = subprocess.run(["git", "show", f"{REV}:paper_2408_03356_b200/csrc/{fn}"],
+                                   capture_output=True, text=True, check=True,
+                                   cwd=os.path.dirname(CSRC)).stdout.splitlines()
+        else:
+            lines = open(os.path.join(CSRC, fn)).read().splitlines()
         marks = []
         for i, l in enumerate(lines, 1):
             m = re.match(r"^(?:template.*\n)?__(?:device|global)__.*?\b(\w+)\s*\(", l)
