@@ -225,12 +225,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
     }
   };
   while (sp > 0) {
-#ifdef RG_SORTED_PUSH
-    const int node = (int)M.stk[sp - 1];
-    const float ntn = stn_dec(M.stn[sp - 1]);
-    --sp;
-    if (ntn > te_lim + slack) continue;   // the k-buffer filled since it was pushed
-#else
+#ifdef RG_BEST32
     // pop the node with the smallest entry distance among the top 32 (approximately
     // best-first); when even that one lies beyond the k-th key, drop all 32
     int node;
@@ -249,6 +244,11 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
       --sp;
       __syncwarp();
     }
+#else
+    const int node = (int)M.stk[sp - 1];
+    const float ntn = stn_dec(M.stn[sp - 1]);
+    --sp;
+    if (ntn > te_lim + slack) continue;   // the k-buffer filled since it was pushed
 #endif
     if (lane == 0) cnt.nodes++;
     const WideNode& W = S.wide[node];
@@ -270,22 +270,19 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
     // internal children
     const unsigned im = __ballot_sync(kFull, hit && child >= 0);
     if (im) {
-#ifdef RG_SORTED_PUSH   // pushed sorted so that the nearest is on top
-      int rank = 0;
-      unsigned mm = im;
-      while (mm) {
-        const int b = __ffs(mm) - 1;
-        mm &= mm - 1;
-        const float tb = __shfl_sync(kFull, tn, b);
-        rank += (tb > tn) || (tb == tn && b < (int)lane);
-      }
-#else                   // any order: the pop selects
+#ifdef RG_BEST32         // any order: the pop selects
+      const unsigned k16 = stn_enc(tn);
       const int rank = __popc(im & lt_mask);
+#else                     // the nearest child on top, the rest in lane order below it
+      const unsigned k16 = (hit && child >= 0) ? stn_enc(tn) : 0xFFFFu;
+      const unsigned kmin = __reduce_min_sync(kFull, k16);
+      const int first = __ffs(__ballot_sync(kFull, k16 == kmin)) - 1;
+      const int rank = (int)lane == first ? __popc(im) - 1 : __popc(im & lt_mask & ~(1u << first));
 #endif
       const int np = __popc(im);
       __syncwarp();
       if (sp + np <= kStk) {
-        if (hit && child >= 0) { M.stk[sp + rank] = (uint32_t)child; M.stn[sp + rank] = stn_enc(tn); }
+        if (hit && child >= 0) { M.stk[sp + rank] = (uint32_t)child; M.stn[sp + rank] = (uint16_t)k16; }
         sp += np;
 #ifdef RG_STACK_PROBE
         if (lane == 0 && (uint32_t)sp > cnt.stackov) cnt.stackov = sp;   // max depth, not overflows
