@@ -225,7 +225,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
     }
   };
   while (sp > 0) {
-#ifdef RG_BEST32
+#ifndef RG_NEAREST_TOP
     // pop the node with the smallest entry distance among the top 32 (approximately
     // best-first); when even that one lies beyond the k-th key, drop all 32
     int node;
@@ -270,7 +270,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
     // internal children
     const unsigned im = __ballot_sync(kFull, hit && child >= 0);
     if (im) {
-#ifdef RG_BEST32         // any order: the pop selects
+#ifndef RG_NEAREST_TOP   // any order: the pop selects
       const unsigned k16 = stn_enc(tn);
       const int rank = __popc(im & lt_mask);
 #else                     // the nearest child on top, the rest in lane order below it
