@@ -65,6 +65,23 @@ def _ncu_traffic(stage):
         return None
 
 
+def _microbench():
+    """Measured FFMA / MUFU / RED rates (tools/microbench.cu, profiles/r1/microbench.json)."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1", "microbench.json")
+    try:
+        return json.load(open(p))
+    except (OSError, ValueError):
+        return {}
+
+
+def red_ops(stats, deg, lobes):
+    """float4 reductions the backward scatter issues: 4 geometry + the appearance
+    chunks (3 * pad4(nc) / 4 + 2 * lobes) per pair (upper bound: pairs whose
+    moments are all zero are skipped)."""
+    nc = (deg + 1) ** 2
+    return stats["pairs"] * (4 + 3 * ((nc + 3) // 4) + 2 * lobes)
+
+
 def peaks(sm_mhz):
     sms = 148
     fp32 = sms * 128 * 2 * sm_mhz * 1e6      # FLOP/s
@@ -335,6 +352,15 @@ def run_ours(args):
     flops, mufu = alu_work(sb if dom == "backward" else sf, costs, "bwd" if dom == "backward" else "fwd")
     t_dom = stage_ms[dom] * 1e-3
     achieved = (flops + 16.0 * mufu) / t_dom / 1e12
+    # the backward's second bound: float4 reductions into the gradient rows (L2 RED rate)
+    mb = _microbench()
+    red_line = None
+    if dom == "backward" and mb.get("red_f32x4_gops"):
+        ops = red_ops(sb, sc.sh_degree, sc.sg_count)
+        ach = ops / t_dom / 1e9
+        red_line = {"ops": int(ops), "achieved_gops": ach, "peak_gops": mb["red_f32x4_gops"],
+                    "frac": ach / mb["red_f32x4_gops"], "unit": "G float4 RED/s",
+                    "peak_source": "tools/microbench.cu (profiles/r1/microbench.json)"}
     peak = pf / 1e12
     line = {
         "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": world,
@@ -355,7 +381,9 @@ def run_ours(args):
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "traffic": _ncu_traffic(dom),
                      "work": {"flops": flops, "mufu": mufu, "mufu_weight": 16, "sm_mhz_for_peak": mhz},
-                     "peak_source": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (B200_PROFILING.md counts); MUFU 16/SM/clk"},
+                     "peak_source": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (B200_PROFILING.md counts); MUFU 16/SM/clk",
+                     "measured_ffma_tflops": mb.get("ffma_tflops"),
+                     "red": red_line},
         "counters": {"fwd": sf, "bwd": sb},
         "clocks": clk,
     }

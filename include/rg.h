@@ -147,6 +147,19 @@ size_t rg_bvh_workspace_bytes(int32_t n, int32_t sh_degree, int32_t sg_count);
 rg_status rg_build_bvh(const rg_gaussians* g, const rg_config* cfg, void* ws, size_t ws_bytes,
                        rg_bvh* out, void* stream);
 
+/* UpdateBVH by refit (the paper rebuilds after each
+   optimiser step): recomputes every record, AABB and box for new
+   parameter VALUES while keeping the topology (Morton order, Karras tree,
+   32-wide collapse) of the rg_build_bvh call that filled `bvh` on this same
+   workspace.  Rendering results are identical to a rebuild (traversal is exact
+   against conservative boxes); only traversal efficiency degrades as the means
+   drift from their Morton order, so callers rebuild periodically.  `bvh` keeps
+   its pointers.  Errors: RG_ERR_INVALID_ARG as rg_build_bvh, or when n,
+   sh_degree, sg_count or the workspace differ from the build's;
+   RG_ERR_WORKSPACE_TOO_SMALL. */
+rg_status rg_refit_bvh(const rg_gaussians* g, const rg_config* cfg, void* ws, size_t ws_bytes,
+                       rg_bvh* bvh, void* stream);
+
 /* ---- rays -------------------------------------------------------------- */
 /* Writes the camera's rays (ARITH-7) to device o/d [R,3]. */
 rg_status rg_camera_rays(const rg_camera* cam, float* origin, float* dir, void* stream);

@@ -112,6 +112,22 @@ rg_status rg_build_bvh(const rg_gaussians* g, const rg_config* cfg, void* ws, si
   return RG_OK;
 }
 
+rg_status rg_refit_bvh(const rg_gaussians* g, const rg_config* cfg, void* ws, size_t ws_bytes,
+                       rg_bvh* bvh, void* stream) {
+  if (!gaussians_ok(g) || !config_ok(cfg) || !ws || !bvh) return RG_ERR_INVALID_ARG;
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return RG_ERR_INVALID_ARG;
+  const BvhLayout L = bvh_layout(g->n, g->sh_degree, g->sg_count);
+  if (ws_bytes < L.total) return RG_ERR_WORKSPACE_TOO_SMALL;
+  char* w = static_cast<char*>(ws);
+  // same topology: built by rg_build_bvh on this workspace with the same sizes
+  if (bvh->n != g->n || bvh->sh_degree != g->sh_degree || bvh->sg_count != g->sg_count ||
+      bvh->geom != static_cast<const void*>(w + L.geom) || bvh->wide != static_cast<const void*>(w + L.wide))
+    return RG_ERR_INVALID_ARG;
+  cudaGetLastError();
+  const cudaError_t e = launch_refit(*g, *cfg, w, L, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? RG_OK : RG_ERR_CUDA;
+}
+
 rg_status rg_camera_rays(const rg_camera* cam, float* origin, float* dir, void* stream) {
   if (!cam || !rays_ok(nullptr, cam)) return RG_ERR_INVALID_ARG;
   const int n = (cam->x1 - cam->x0) * (cam->y1 - cam->y0);

@@ -375,12 +375,13 @@ __device__ __forceinline__ float box_area(const float* b) {
 }
 
 __global__ void k_collapse_init(int n, const float* leaf_box, WideNode* wide, int2* wq,
-                                int* counts) {
+                                int* wide_src, int* counts) {
   const int l = threadIdx.x;
   if (l == 0) {
     // [0] wide nodes allocated, [1] head, [2] done, [3] error, [4] reserved
     for (int k = 0; k < 8; ++k) counts[k] = 0;
     counts[0] = 1;
+    wide_src[0] = 0;
     if (n > 1) {
       wq[0] = make_int2(0, 0);   // binary root -> wide node 0
       counts[4] = 1;
@@ -405,7 +406,7 @@ __global__ void k_collapse_init(int n, const float* leaf_box, WideNode* wide, in
 // (done read before reserved): every reserved item is then finished, so no
 // further item can appear.
 __global__ void __launch_bounds__(128) k_collapse_persistent(const float4* nodes, WideNode* wide,
-                                                             int2* q, int* counts) {
+                                                             int2* q, int* wide_src, int* counts) {
   volatile int* vc = counts;
   volatile long long* vq = reinterpret_cast<volatile long long*>(q);
   while (true) {
@@ -464,6 +465,7 @@ __global__ void __launch_bounds__(128) k_collapse_persistent(const float4* nodes
         int child = ids[k];
         if (child >= 0) {
           const int wid = wid0 + slot++;
+          wide_src[wid] = child;                                 // for rg_refit_bvh
           const int qs = atomicAdd(counts + 4, 1);               // reserve a queue slot
           vq[qs] = ((long long)wid << 32) | (unsigned)child;     // publish with one store
           child = wid;
@@ -479,6 +481,34 @@ __global__ void __launch_bounds__(128) k_collapse_persistent(const float4* nodes
     }
     __threadfence();
     atomicAdd(counts + 2, 1);                // this item is done
+  }
+}
+
+// refit of the wide nodes after k_refit (rg_refit_bvh): one warp per wide
+// node, lane = child slot; an internal child's box is the union of its binary
+// node's two child boxes, a leaf's its padded AABB; the topology is kept.
+__global__ void __launch_bounds__(128) k_wide_refit(const float4* nodes, const float* leaf_box,
+                                                    const int* wide_src, const int* counts,
+                                                    WideNode* wide) {
+  const int lane = threadIdx.x & 31;
+  const int nw = counts[0];
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nw;
+       w += (gridDim.x * blockDim.x) >> 5) {
+    WideNode& W = wide[w];
+    const int child = W.child[lane];
+    if (child == kWideEmpty) continue;
+    float b[6];
+    if (child < 0) {
+      for (int k = 0; k < 6; ++k) b[k] = leaf_box[6 * (size_t)(~child) + k];
+    } else {
+      const float* x = reinterpret_cast<const float*>(nodes + 4 * (size_t)wide_src[child]);
+      for (int k = 0; k < 3; ++k) {
+        b[k] = fminf(x[k], x[6 + k]);
+        b[3 + k] = fmaxf(x[3 + k], x[9 + k]);
+      }
+    }
+    W.lox[lane] = b[0]; W.loy[lane] = b[1]; W.loz[lane] = b[2];
+    W.hix[lane] = b[3]; W.hiy[lane] = b[4]; W.hiz[lane] = b[5];
   }
 }
 
@@ -517,7 +547,7 @@ BvhLayout bvh_layout(int n, int deg, int lobes) {
   L.hist = take(4 * 256 * (size_t)L.tiles);
   L.wide = take(sizeof(WideNode) * wide_capacity(n));
   L.wq_a = take(8 * nn);
-  L.wq_b = take(8 * nn);
+  L.wide_src = take(8 * nn);
   L.wcounts = take(32);
   L.total = o;
   return L;
@@ -576,18 +606,65 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
   WideNode* wide = reinterpret_cast<WideNode*>(ws + L.wide);
   int2* qa = reinterpret_cast<int2*>(ws + L.wq_a);
   int* wc = reinterpret_cast<int*>(ws + L.wcounts);
+  int* wsrc = reinterpret_cast<int*>(ws + L.wide_src);
   if (n > 1) cudaMemsetAsync(qa, 0xFF, 8 * (size_t)n, st);
-  k_collapse_init<<<1, 32, 0, st>>>(n, leaf_box, wide, qa, wc);
+  k_collapse_init<<<1, 32, 0, st>>>(n, leaf_box, wide, qa, wsrc, wc);
   count_launches(1);
   if (n > 1) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // all blocks co-resident (waiting threads spin): 2 blocks of 128 per SM
-    k_collapse_persistent<<<2 * sms, 128, 0, st>>>(nodes, wide, qa, wc);
+    k_collapse_persistent<<<2 * sms, 128, 0, st>>>(nodes, wide, qa, wsrc, wc);
     k_collapse_check<<<1, 1, 0, st>>>(wc, (int)wide_capacity(n));
     count_launches(2);
   }
+  return cudaGetLastError();
+}
+
+// UpdateBVH by refit: new parameters, same n and the
+// topology of the last launch_build on this workspace (Morton order, Karras
+// tree, 32-wide collapse).  Records, AABBs and every box are recomputed; a
+// stale order only costs traversal efficiency, never correctness (boxes stay
+// conservative unions).
+cudaError_t launch_refit(const rg_gaussians& g, const rg_config& c, char* ws, const BvhLayout& L,
+                         cudaStream_t st) {
+  const int n = g.n;
+  float* root_box = reinterpret_cast<float*>(ws + L.root_box);
+  int* bounds = reinterpret_cast<int*>(ws + L.bounds);
+  k_init<<<1, 32, 0, st>>>(bounds, root_box);
+  count_launches(1);
+  if (n == 0) return cudaGetLastError();
+  const int blocks = (n + kThreads - 1) / kThreads;
+  float* box_orig = reinterpret_cast<float*>(ws + L.box_orig);
+  int* flags = reinterpret_cast<int*>(ws + L.flags);
+  k_preprocess<<<blocks, kThreads, 0, st>>>(g, c, box_orig, flags, bounds);
+  const uint32_t* va = reinterpret_cast<const uint32_t*>(ws + L.vals_a);
+  float4* geom = reinterpret_cast<float4*>(ws + L.geom);
+  float* app = reinterpret_cast<float*>(ws + L.app);
+  float* leaf_box = reinterpret_cast<float*>(ws + L.leaf_box);
+  const int stride = app_stride(g.sh_degree, g.sg_count);
+  k_pack<<<blocks, kThreads, 0, st>>>(g, c, va, box_orig, flags, geom, app, stride, leaf_box);
+  k_pack_app<<<min((n + kThreads / 32 - 1) / (kThreads / 32), 148 * 16), kThreads, 0, st>>>(
+      g, va, app, stride);
+  float4* nodes = reinterpret_cast<float4*>(ws + L.nodes);
+  int* cnt = reinterpret_cast<int*>(ws + L.refit_cnt);
+  if (n > 1) cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)(n - 1), st);
+  k_refit<<<blocks, kThreads, 0, st>>>(leaf_box, nodes, reinterpret_cast<const int*>(ws + L.parent_int),
+                                       reinterpret_cast<const int*>(ws + L.parent_leaf), cnt,
+                                       root_box, n);
+  WideNode* wide = reinterpret_cast<WideNode*>(ws + L.wide);
+  int* wsrc = reinterpret_cast<int*>(ws + L.wide_src);
+  int* wc = reinterpret_cast<int*>(ws + L.wcounts);
+  count_launches(5);
+  if (n == 1) {
+    k_collapse_init<<<1, 32, 0, st>>>(n, leaf_box, wide, reinterpret_cast<int2*>(ws + L.wq_a), wsrc,
+                                      wc);
+  } else {
+    const int wblocks = min((int)((wide_capacity(n) + 3) / 4), 148 * 8);
+    k_wide_refit<<<wblocks, 128, 0, st>>>(nodes, leaf_box, wsrc, wc, wide);
+  }
+  count_launches(1);
   return cudaGetLastError();
 }
 

@@ -244,12 +244,14 @@ __host__ __device__ inline size_t fetch_log_header_bytes(int n_rays) {
 
 struct BvhLayout {
   size_t geom, app, nodes, leaf_box, root_box, codes, keys_a, keys_b, vals_a, vals_b,
-      box_orig, flags, parent_int, parent_leaf, refit_cnt, bounds, hist, wide, wq_a, wq_b,
+      box_orig, flags, parent_int, parent_leaf, refit_cnt, bounds, hist, wide, wq_a, wide_src,
       wcounts, total;
   int tiles;
 };
 BvhLayout bvh_layout(int n, int deg, int lobes);
 cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, const BvhLayout& L,
+                         cudaStream_t st);
+cudaError_t launch_refit(const rg_gaussians& g, const rg_config& c, char* ws, const BvhLayout& L,
                          cudaStream_t st);
 cudaError_t launch_camera_rays(const rg_camera& cam, float* o, float* d, cudaStream_t st);
 cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,

@@ -64,6 +64,7 @@ class _BVH(C.Structure):
 
 
 EXPORTS = ("rg_status_string", "rg_version", "rg_kernel_launches", "rg_bvh_workspace_bytes", "rg_build_bvh",
+           "rg_refit_bvh",
            "rg_camera_rays", "rg_render_forward", "rg_backward_workspace_bytes",
            "rg_render_backward", "rg_l1_loss_grad", "rg_fetch_log_bytes")
 
@@ -95,6 +96,8 @@ def lib(load_only: bool = False):
     L.rg_bvh_workspace_bytes.argtypes = [I32, I32, I32]
     L.rg_build_bvh.restype = C.c_int
     L.rg_build_bvh.argtypes = [P, P, P, SZ, P, P]
+    L.rg_refit_bvh.restype = C.c_int
+    L.rg_refit_bvh.argtypes = [P, P, P, SZ, P, P]
     L.rg_camera_rays.restype = C.c_int
     L.rg_camera_rays.argtypes = [P, P, P, P]
     L.rg_render_forward.restype = C.c_int
@@ -261,6 +264,18 @@ def build_bvh(scene: Gaussians, cfg: Config, ws=None) -> BVH:
     _check(L.rg_build_bvh(C.byref(gs), C.byref(cs), _ptr(ws), nbytes, C.byref(h), _stream()),
            "rg_build_bvh")
     return BVH(ws, h, scene)
+
+
+def refit_bvh(bvh: BVH, scene: Gaussians, cfg: Config) -> BVH:
+    """UpdateBVH by refit (rg_refit_bvh): new parameter values of a scene with
+    the same n / sh_degree / sg_count, topology of the last build kept."""
+    _require_cuda()
+    L = lib()
+    gs, cs = scene.struct(), cfg.struct()
+    _check(L.rg_refit_bvh(C.byref(gs), C.byref(cs), _ptr(bvh.ws), bvh.ws.numel(), C.byref(bvh.h),
+                          _stream()), "rg_refit_bvh")
+    bvh.scene = scene
+    return bvh
 
 
 def camera_struct(cam) -> _Camera:

@@ -1,0 +1,133 @@
+"""GPU parity of the SURVEY §8(f) NEXT rows against the oracle / against the
+hot path they extend.
+
+  * rg_refit_bvh (UpdateBVH by refit): leaf boxes and root box bit-exact vs the
+    oracle's for the new parameters, every wide-node box the exact union of the
+    leaf boxes below it, forward bit-identical to a fresh rebuild and within the
+    pixel bar of the oracle, gradients within the gradient bar.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2408_03356_b200 import rg, synth
+from test_gpu_parity import PIX_TOL, compare_pixels, grad_check
+
+pytestmark = pytest.mark.gpu
+
+
+def _perturbed(sc, seed, inactive=()):
+    """new parameter values, same n / degree / lobes: means move (stale Morton
+    order), scales and densities change, some Gaussians turn inactive"""
+    rng = np.random.default_rng(seed)
+    s2 = sc.copy()
+    s2.mean += rng.normal(0, 0.03, s2.mean.shape).astype(np.float32)
+    s2.scale *= rng.uniform(0.7, 1.4, s2.scale.shape).astype(np.float32)
+    s2.density *= rng.uniform(0.5, 2.0, s2.density.shape).astype(np.float32)
+    s2.sh += rng.normal(0, 0.05, s2.sh.shape).astype(np.float32)
+    for i in inactive:
+        s2.density[i] = 0.5 * 0.1        # below sigma_eps = 0.1
+    return s2
+
+
+def _leaf_boxes_by_index(ref):
+    out = np.empty_like(ref.leaf_boxes)
+    out[ref.order] = ref.leaf_boxes
+    return out
+
+
+def _check_refit_tree(b, boxes_morton, root):
+    wf, wi = b.wide_nodes()
+    wf, wi = wf.cpu().numpy(), wi.cpu().numpy()
+    n = len(boxes_morton)
+    seen = np.zeros(n, int)
+
+    def walk(w):
+        lo = np.full(3, np.inf, np.float32); hi = np.full(3, -np.inf, np.float32)
+        for k in range(32):
+            ch = wi[w, 6, k]
+            if ch == 0x7FFFFFFF:
+                continue
+            sub = boxes_morton[~ch] if ch < 0 else walk(ch)
+            if ch < 0:
+                seen[~ch] += 1
+            assert np.array_equal(wf[w, :6, k], sub)
+            lo = np.minimum(lo, sub[:3]); hi = np.maximum(hi, sub[3:])
+        return np.concatenate([lo, hi])
+    import sys
+    sys.setrecursionlimit(10000)
+    assert np.array_equal(walk(0), root)
+    assert np.all(seen == 1)
+
+
+@pytest.mark.parametrize("n", [1, 2, 700, 5000])
+def test_refit_boxes_bitexact(oracle, n):
+    sc = synth.random_scene(1300 + n, n, sh_degree=1, sg_count=2, density_range=(1, 30),
+                            scale_range=(0.02, 0.08), extent=0.5)
+    p = synth.RenderParams()
+    g = rg.Gaussians.from_scene(sc)
+    b = rg.build_bvh(g, rg.Config.of(p))
+    order = b.debug_views()["order"].cpu().numpy().view(np.uint32).copy()
+    s2 = _perturbed(sc, 7, inactive=range(0, n, 5))
+    g2 = rg.Gaussians.from_scene(s2)
+    rg.refit_bvh(b, g2, rg.Config.of(p))
+    torch.cuda.synchronize()
+    v = {k: t.cpu().numpy() for k, t in b.debug_views().items()}
+    assert np.array_equal(v["order"].view(np.uint32), order)          # topology kept
+    ref = oracle.BVH(s2, p)
+    boxes = _leaf_boxes_by_index(ref)[order]
+    assert np.array_equal(v["leaf_box"], boxes)
+    assert np.array_equal(v["root_box"], ref.root)
+    if n > 1:
+        _check_refit_tree(b, boxes, ref.root)
+
+
+def test_refit_forward_equals_rebuild_and_oracle(oracle):
+    sc = synth.random_scene(1400, 400, sh_degree=3, sg_count=7, density_range=(2, 30),
+                            scale_range=(0.03, 0.1), extent=0.5)
+    p = synth.RenderParams(dt=3e-3, t_eps=1e-4)
+    cfg = rg.Config.of(p)
+    o, d = synth.random_rays(1401, 2000)
+    to, td = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
+    s2 = _perturbed(sc, 8, inactive=range(3, 400, 11))
+    g2 = rg.Gaussians.from_scene(s2)
+    b = rg.build_bvh(rg.Gaussians.from_scene(sc), cfg)
+    rg.refit_bvh(b, g2, cfg)
+    f_refit = rg.render_forward(g2, b, cfg, rays=(to, td))
+    f_build = rg.render_forward(g2, rg.build_bvh(g2, cfg), cfg, rays=(to, td))
+    torch.cuda.synchronize()
+    for k in ("rgb", "T", "replay"):
+        assert torch.equal(f_refit[k], f_build[k]), k
+    ref = oracle.render(s2, p, o, d, mode=2)
+    res = {k: f_refit[k].cpu().numpy() for k in ("rgb", "T", "replay")}
+    compare_pixels(oracle, s2, p, o, d, res, ref)
+
+
+def test_refit_backward_matches_oracle(oracle):
+    sc = synth.random_scene(1500, 80, sh_degree=2, sg_count=3, density_range=(3, 40),
+                            scale_range=(0.04, 0.12), extent=0.4)
+    p = synth.RenderParams(dt=4e-3, t_eps=1e-4)
+    cfg = rg.Config.of(p)
+    o, d = oracle.camera_rays(synth.orbit_camera(2.2, 60, 20, 20, 20, 24.0))
+    to, td = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
+    s2 = _perturbed(sc, 9)
+    g2 = rg.Gaussians.from_scene(s2)
+    b = rg.build_bvh(rg.Gaussians.from_scene(sc), cfg)
+    rg.refit_bvh(b, g2, cfg)
+    fwd = rg.render_forward(g2, b, cfg, rays=(to, td), log=rg.new_log(len(o)))
+    up = np.random.default_rng(3).normal(size=(len(o), 3)).astype(np.float32)
+    grads = rg.render_backward(g2, b, cfg, fwd, torch.from_numpy(up).cuda(), rays=(to, td))
+    torch.cuda.synchronize()
+    ref = oracle.backward(s2, p, o, d, up.astype(np.float64), mode=2)
+    grad_check(grads, ref)
+
+
+def test_refit_rejects_other_topology():
+    sc = synth.random_scene(1600, 50)
+    p = synth.RenderParams()
+    cfg = rg.Config.of(p)
+    b = rg.build_bvh(rg.Gaussians.from_scene(sc), cfg)
+    with pytest.raises(rg.RGError):
+        rg.refit_bvh(b, rg.Gaussians.from_scene(synth.random_scene(1601, 51)), cfg)
+    with pytest.raises(rg.RGError):
+        rg.refit_bvh(b, rg.Gaussians.from_scene(synth.random_scene(1602, 50, sh_degree=1)), cfg)
