@@ -325,6 +325,18 @@ def run_ours(args):
     e3.record(stream)
     torch.cuda.synchronize(); barrier()
     fwd_ms = max_over_ranks(e2.elapsed_time(e3) / args.steps)
+    # ---- UpdateBVH by refit (rg_refit_bvh): reported beside the
+    # rebuild the step uses (the paper rebuilds after every step)
+    for _ in range(args.warmup):
+        rg.refit_bvh(bvh, g, cfg)
+    torch.cuda.synchronize()
+    e6, e7 = ev(), ev()
+    e6.record(stream)
+    for _ in range(args.steps):
+        rg.refit_bvh(bvh, g, cfg)
+    e7.record(stream)
+    torch.cuda.synchronize()
+    refit_ms = max_over_ranks(e6.elapsed_time(e7) / args.steps)
     # ---- end to end through the public API with host buffers
     for _ in range(args.warmup):
         tgt_dev.copy_(tgt_host, non_blocking=True); step(tgt_dev); loss_host.copy_(loss, non_blocking=True)
@@ -374,6 +386,7 @@ def run_ours(args):
         "fwd": {"value": world * R / (fwd_ms * 1e-3) / 1e6, "unit": "Mrays/s", "ms": fwd_ms,
                 "fps_per_gpu": 1e3 / fwd_ms, "paper_fps_rtx4090": PAPER_FPS},
         "stages_ms": stage_ms,
+        "refit_ms": refit_ms,
         "e2e": {"value": total_rays / (e2e_ms * 1e-3) / 1e6, "unit": "Mrays/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(tgt_host.numel() * 4), "d2h_bytes_per_step": 4},
         "gpu_launches": int(launches),

@@ -23,4 +23,7 @@ for it in range(3):
     n = cam.n_rays
     print(f"{name} it{it}: build {e0.elapsed_time(e1):.3f} ms  fwd {e1.elapsed_time(e2):.3f} ms "
           f"({n/e1.elapsed_time(e2)/1e3:.1f} Mrays/s)  bwd {e2.elapsed_time(e3):.3f} ms", flush=True)
+e4, e5 = ev(), ev()
+e4.record(); rg.refit_bvh(b, g, cfg); e5.record(); torch.cuda.synchronize()
+print(f"refit {e4.elapsed_time(e5):.3f} ms")
 print(rg.stats_dict(st))
