@@ -1,0 +1,127 @@
+"""Oracle of the training-step neighbours of the hot path (SURVEY.md §8(f)
+NEXT-1): the Adam update with the paper's per-group learning rates, schedule
+and colour unlock, and the parameter activations.  Plain NumPy in float64,
+one step of the algorithm per line, no fusion.
+
+TEST INFRASTRUCTURE ONLY: imported by tests/ (and nothing in the product
+package).  Pinned by tests/test_oracle_train.py.
+
+Citations: P:n = /root/reference/PAPER.md line n.
+  * Adam: Kingma & Ba 2014, Algorithm 1 (cited at P:639): with gradient g_t,
+        m_t = b1 m_{t-1} + (1 - b1) g_t
+        v_t = b2 v_{t-1} + (1 - b2) g_t^2
+        mhat = m_t / (1 - b1^t),  vhat = v_t / (1 - b2^t)
+        theta_t = theta_{t-1} - lr * mhat / (sqrt(vhat) + eps)
+  * learning rates (Blender): density 1.5e-1, constant colour (SH DC)
+    1.3e-3, SH 1.1e-4, SG coefficients 6.0e-4, lobe sharpness 1.0e-1, lobe
+    direction 2.0e-3, scale 1.2e-2, quaternion 3.0e-4, mean exponential decay
+    1.5e-5 -> 2.5e-6 over 30,000 iterations; Mip-NeRF360: density
+    exponential decay 0.5 -> 0.01 over 30,000 iterations.
+  * unlock: SH degrees 0, 1, 2, then the 7 SG, every 1000
+    iterations; a locked coefficient is not updated.
+Readings where the paper is silent (L23-L27): the optimiser holds
+raw parameters; scale = exp(raw), density = exp(raw), quaternion and lobe
+axis = raw / |raw|, everything else the identity; eps = 1e-15, b1 = 0.9,
+b2 = 0.999 (the 3D Gaussian Splatting practice P:224 follows); exponential
+decay is log-linear in the iteration, constant after the last iteration.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+GROUPS = ("mean", "quat", "scale", "density", "sh", "sg_amp", "sg_sharp", "sg_axis")
+
+LR_BLENDER = dict(mean=(1.5e-5, 2.5e-6), quat=3.0e-4, scale=1.2e-2, density=1.5e-1,
+                  sh_dc=1.3e-3, sh_rest=1.1e-4, sg_amp=6.0e-4, sg_sharp=1.0e-1, sg_axis=2.0e-3)
+LR_MIP = dict(LR_BLENDER, density=(0.5, 0.01))
+DECAY_STEPS = 30_000
+
+
+def expon_lr(lr0: float, lr1: float, it: int, steps: int = DECAY_STEPS) -> float:
+    """exponential decay from lr0 at iteration 0 to lr1 at `steps`,
+    log-linear interpolation, constant afterwards"""
+    t = min(max(it / steps, 0.0), 1.0)
+    return float(np.exp(np.log(lr0) * (1.0 - t) + np.log(lr1) * t))
+
+
+def group_lr(lrs: dict, it: int) -> dict:
+    out = {}
+    for k, v in lrs.items():
+        out[k] = expon_lr(v[0], v[1], it) if isinstance(v, tuple) else float(v)
+    return out
+
+
+def unlocked(it: int, every: int = 1000, max_deg: int = 3, max_lobes: int = 7):
+    """(active SH degree, active SG lobes) at iteration `it`: degree 0
+    from the start, one more SH degree every `every` iterations up to 2, then
+    the SG (and the last SH degree if the scene has it)"""
+    stage = it // every
+    deg = min(stage, min(max_deg, 2))
+    lobes = max_lobes if stage >= 3 else 0
+    if stage >= 3 and max_deg == 3:
+        deg = 3
+    return deg, lobes
+
+
+def activate(raw: dict) -> dict:
+    """activated parameters from raw ones (readings L23-L25)"""
+    a = {k: np.asarray(v, np.float64) for k, v in raw.items()}
+    a["scale"] = np.exp(a["scale"])
+    a["density"] = np.exp(a["density"])
+    a["quat"] = a["quat"] / np.linalg.norm(a["quat"], axis=-1, keepdims=True)
+    a["sg_axis"] = a["sg_axis"] / np.linalg.norm(a["sg_axis"], axis=-1, keepdims=True)
+    return a
+
+
+def raw_grad(raw: dict, grad_act: dict) -> dict:
+    """chain rule of `activate`: dL/draw from dL/dactivated"""
+    g = {k: np.asarray(v, np.float64).copy() for k, v in grad_act.items()}
+    g["scale"] = grad_act["scale"] * np.exp(np.asarray(raw["scale"], np.float64))
+    g["density"] = grad_act["density"] * np.exp(np.asarray(raw["density"], np.float64))
+    for k in ("quat", "sg_axis"):
+        r = np.asarray(raw[k], np.float64)
+        nr = np.linalg.norm(r, axis=-1, keepdims=True)
+        u = r / nr
+        ga = np.asarray(grad_act[k], np.float64)
+        g[k] = (ga - u * np.sum(u * ga, axis=-1, keepdims=True)) / nr   # (I - u u^T) g / |r|
+    return g
+
+
+def lr_per_element(raw: dict, lrs: dict, sh_active: int, sg_active: int) -> dict:
+    """learning rate of every raw element (0 for locked colour coefficients)"""
+    out = {}
+    for k in GROUPS:
+        shape = np.asarray(raw[k]).shape
+        if k == "sh":
+            lr = np.full(shape, lrs["sh_rest"])
+            lr[:, 0, :] = lrs["sh_dc"]
+            lr[:, sh_active:, :] = 0.0
+        elif k in ("sg_amp", "sg_sharp", "sg_axis"):
+            lr = np.full(shape, lrs[k])
+            lr[:, sg_active:, ...] = 0.0
+        else:
+            lr = np.full(shape, lrs[k])
+        out[k] = lr
+    return out
+
+
+def adam_step(raw: dict, m: dict, v: dict, grad_act: dict, it: int, *, lrs=LR_BLENDER,
+              sh_active=16, sg_active=7, b1=0.9, b2=0.999, eps=1e-15):
+    """one Adam step (Kingma & Ba Alg. 1) at iteration `it` (t = it + 1) on the
+    raw parameters; returns (raw', m', v', activated')"""
+    t = it + 1
+    g = raw_grad(raw, grad_act)
+    lr = lr_per_element(raw, group_lr(lrs, it), sh_active, sg_active)
+    raw2, m2, v2 = {}, {}, {}
+    for k in GROUPS:
+        th = np.asarray(raw[k], np.float64)
+        live = lr[k] > 0.0                               # locked: no update at all
+        mk = b1 * np.asarray(m[k], np.float64) + (1.0 - b1) * g[k]
+        vk = b2 * np.asarray(v[k], np.float64) + (1.0 - b2) * g[k] * g[k]
+        mhat = mk / (1.0 - b1 ** t)
+        vhat = vk / (1.0 - b2 ** t)
+        upd = th - lr[k] * mhat / (np.sqrt(vhat) + eps)
+        raw2[k] = np.where(live, upd, th)
+        m2[k] = np.where(live, mk, m[k])
+        v2[k] = np.where(live, vk, v[k])
+    return raw2, m2, v2, activate(raw2)
