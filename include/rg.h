@@ -205,6 +205,41 @@ rg_status rg_render_backward(const rg_gaussians* g, const rg_bvh* bvh, const rg_
                              const rg_gaussian_grads* grads, rg_stats* stats, void* ws,
                              size_t ws_bytes, void* stream);
 
+/* ---- training-step neighbours ---------------------- */
+/* Mutable fp32 arrays in the rg_gaussians layouts (raw parameters, Adam moments,
+   activated outputs). */
+typedef rg_gaussian_grads rg_param_arrays;
+
+/* learning-rate slots of rg_adam_config.lr */
+enum { RG_LR_MEAN = 0, RG_LR_QUAT, RG_LR_SCALE, RG_LR_DENSITY, RG_LR_SH_DC, RG_LR_SH_REST,
+       RG_LR_SG_AMP, RG_LR_SG_SHARP, RG_LR_SG_AXIS, RG_LR_COUNT };
+
+typedef struct {
+  int32_t n, sh_degree, sg_count;
+  int32_t step;          /* t >= 1 of Kingma & Ba Alg. 1 (bias corrections 1 - beta^t) */
+  float lr[RG_LR_COUNT]; /* this iteration's learning rates (schedules are the caller's) */
+  float beta1, beta2, eps;   /* in [0,1), [0,1), > 0 */
+  int32_t sh_active;     /* SH coefficients per channel being optimised, 1..(sh_degree+1)^2;
+                            the rest are locked (colour unlock) */
+  int32_t sg_active;     /* SG lobes being optimised, 0..sg_count */
+} rg_adam_config;
+
+/* One fused Adam step over every parameter group (Alg. 3 AdamOptim):
+     g_raw = J_act^T grad_act (activations: scale = exp(raw), density = exp(raw),
+             quat and sg_axis = raw/|raw|, identity otherwise -- DESIGN.md L23-L25);
+     m = b1 m + (1-b1) g_raw;  v = b2 v + (1-b2) g_raw^2;
+     raw -= lr * (m/(1-b1^t)) / (sqrt(v/(1-b2^t)) + eps)      (Kingma & Ba Alg. 1);
+     act_out = act(raw) for every element (locked ones too).
+   raw, m, v are updated in place; grad_act is read (the gradient w.r.t. the
+   activated parameters, e.g. from rg_render_backward); act_out may alias the
+   arrays of the rg_gaussians the next render reads.  Locked colour coefficients
+   keep raw, m and v.  Errors: RG_ERR_INVALID_ARG for NULL arrays (sg_* may be
+   NULL when sg_count == 0), bad sizes, step < 1, out-of-range betas/eps/active
+   counts. */
+rg_status rg_adam_step(const rg_adam_config* cfg, const rg_gaussian_grads* grad_act,
+                       const rg_param_arrays* raw, const rg_param_arrays* m,
+                       const rg_param_arrays* v, const rg_param_arrays* act_out, void* stream);
+
 /* ---- loss helper (for benchmarks; loss itself is outside the paper's path) -- */
 /* L1 loss: loss += scale * sum |rgb - target|, d_rgb = scale * sign(rgb - target)
    over n_values floats (device; loss is one device float, accumulated). */

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libraygauss.so")
-SOURCES = ["rg_build.cu", "rg_render.cu", "rg_api.cu"]
+SOURCES = ["rg_build.cu", "rg_render.cu", "rg_train.cu", "rg_api.cu"]
 HEADERS = ["rg_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -128,6 +128,39 @@ rg_status rg_refit_bvh(const rg_gaussians* g, const rg_config* cfg, void* ws, si
   return e == cudaSuccess ? RG_OK : RG_ERR_CUDA;
 }
 
+namespace {
+bool arrays_ok(const rg_gaussian_grads* a, int32_t n, int32_t G) {
+  if (!a) return false;
+  if (n == 0) return true;
+  if (!a->mean || !a->quat || !a->scale || !a->density || !a->sh) return false;
+  if (G > 0 && (!a->sg_amp || !a->sg_sharp || !a->sg_axis)) return false;
+  return true;
+}
+}  // namespace
+
+rg_status rg_adam_step(const rg_adam_config* cfg, const rg_gaussian_grads* grad_act,
+                       const rg_param_arrays* raw, const rg_param_arrays* m,
+                       const rg_param_arrays* v, const rg_param_arrays* act_out, void* stream) {
+  if (!cfg || cfg->n < 0 || cfg->sh_degree < 0 || cfg->sh_degree > kMaxDeg || cfg->sg_count < 0 ||
+      cfg->sg_count > kMaxLobes || cfg->step < 1)
+    return RG_ERR_INVALID_ARG;
+  if (!(cfg->beta1 >= 0.f && cfg->beta1 < 1.f) || !(cfg->beta2 >= 0.f && cfg->beta2 < 1.f) ||
+      !(cfg->eps > 0.f))
+    return RG_ERR_INVALID_ARG;
+  const int nc = (cfg->sh_degree + 1) * (cfg->sh_degree + 1);
+  if (cfg->sh_active < 1 || cfg->sh_active > nc || cfg->sg_active < 0 ||
+      cfg->sg_active > cfg->sg_count)
+    return RG_ERR_INVALID_ARG;
+  for (int k = 0; k < RG_LR_COUNT; ++k)
+    if (!(cfg->lr[k] >= 0.f) || !isfinite(cfg->lr[k])) return RG_ERR_INVALID_ARG;
+  for (const rg_gaussian_grads* a : {grad_act, raw, m, v, act_out})
+    if (!arrays_ok(a, cfg->n, cfg->sg_count)) return RG_ERR_INVALID_ARG;
+  cudaGetLastError();
+  const cudaError_t e = launch_adam(*cfg, *grad_act, *raw, *m, *v, *act_out,
+                                    static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? RG_OK : RG_ERR_CUDA;
+}
+
 rg_status rg_camera_rays(const rg_camera* cam, float* origin, float* dir, void* stream) {
   if (!cam || !rays_ok(nullptr, cam)) return RG_ERR_INVALID_ARG;
   const int n = (cam->x1 - cam->x0) * (cam->y1 - cam->y0);

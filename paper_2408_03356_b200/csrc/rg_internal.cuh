@@ -253,6 +253,9 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
                          cudaStream_t st);
 cudaError_t launch_refit(const rg_gaussians& g, const rg_config& c, char* ws, const BvhLayout& L,
                          cudaStream_t st);
+cudaError_t launch_adam(const rg_adam_config& c, const rg_gaussian_grads& g,
+                        const rg_gaussian_grads& raw, const rg_gaussian_grads& m,
+                        const rg_gaussian_grads& v, const rg_gaussian_grads& act, cudaStream_t st);
 cudaError_t launch_camera_rays(const rg_camera& cam, float* o, float* d, cudaStream_t st);
 cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,
                            const rg_rays* rays, const rg_camera* cam, float* rgb, float* T,

@@ -45,6 +45,13 @@ class _Config(C.Structure):
                 ("pad_", C.c_int32)]
 
 
+class _AdamConfig(C.Structure):
+    _fields_ = [("n", C.c_int32), ("sh_degree", C.c_int32), ("sg_count", C.c_int32),
+                ("step", C.c_int32), ("lr", C.c_float * 9), ("beta1", C.c_float),
+                ("beta2", C.c_float), ("eps", C.c_float), ("sh_active", C.c_int32),
+                ("sg_active", C.c_int32)]
+
+
 class _Rays(C.Structure):
     _fields_ = [("n", C.c_int32), ("pad_", C.c_int32), ("origin", C.c_void_p), ("dir", C.c_void_p)]
 
@@ -64,7 +71,7 @@ class _BVH(C.Structure):
 
 
 EXPORTS = ("rg_status_string", "rg_version", "rg_kernel_launches", "rg_bvh_workspace_bytes", "rg_build_bvh",
-           "rg_refit_bvh",
+           "rg_refit_bvh", "rg_adam_step",
            "rg_camera_rays", "rg_render_forward", "rg_backward_workspace_bytes",
            "rg_render_backward", "rg_l1_loss_grad", "rg_fetch_log_bytes")
 
@@ -98,6 +105,8 @@ def lib(load_only: bool = False):
     L.rg_build_bvh.argtypes = [P, P, P, SZ, P, P]
     L.rg_refit_bvh.restype = C.c_int
     L.rg_refit_bvh.argtypes = [P, P, P, SZ, P, P]
+    L.rg_adam_step.restype = C.c_int
+    L.rg_adam_step.argtypes = [P, P, P, P, P, P, P]
     L.rg_camera_rays.restype = C.c_int
     L.rg_camera_rays.argtypes = [P, P, P, P]
     L.rg_render_forward.restype = C.c_int
@@ -398,3 +407,66 @@ def new_stats(device="cuda"):
 def stats_dict(t):
     v = t.cpu().tolist()
     return {k: int(v[i]) for i, k in enumerate(STAT_KEYS)}
+
+
+# ---------------------------------------------------------------------------
+# training-step neighbours
+# ---------------------------------------------------------------------------
+
+LR_SLOTS = ("mean", "quat", "scale", "density", "sh_dc", "sh_rest", "sg_amp", "sg_sharp", "sg_axis")
+# P:642 (Blender); tuples are exponential decays (start, end) over 30,000 iterations
+LR_BLENDER = dict(mean=(1.5e-5, 2.5e-6), quat=3.0e-4, scale=1.2e-2, density=1.5e-1,
+                  sh_dc=1.3e-3, sh_rest=1.1e-4, sg_amp=6.0e-4, sg_sharp=1.0e-1, sg_axis=2.0e-3)
+LR_MIP = dict(LR_BLENDER, density=(0.5, 0.01))
+
+
+def learning_rates(it: int, table=LR_BLENDER, decay_steps: int = 30_000):
+    """per-slot learning rates at iteration `it` (exponential decay, log-linear)"""
+    import math
+    f = min(max(it / decay_steps, 0.0), 1.0)
+    out = []
+    for k in LR_SLOTS:
+        x = table[k]
+        out.append(math.exp(math.log(x[0]) * (1 - f) + math.log(x[1]) * f) if isinstance(x, tuple)
+                   else float(x))
+    return out
+
+
+def _arrays(d) -> _Grads:
+    a = _Grads()
+    for k in GROUPS:
+        setattr(a, k, _ptr(d[k]))
+    return a
+
+
+class Adam:
+    """Optimiser state of Alg. 3 (raw parameters + moments, caller layout) and
+    the fused rg_adam_step.  Built from ACTIVATED parameters (inverse of the
+    activations of DESIGN.md L23-L25); `step` writes the activated parameters
+    back into `scene` for the next render."""
+
+    def __init__(self, scene: Gaussians, betas=(0.9, 0.999), eps=1e-15, table=LR_BLENDER):
+        self.scene, self.betas, self.eps, self.table = scene, betas, eps, table
+        self.raw = {k: getattr(scene, k).clone() for k in GROUPS}
+        self.raw["scale"] = torch.log(self.raw["scale"])
+        self.raw["density"] = torch.log(self.raw["density"])
+        self.m = {k: torch.zeros_like(v) for k, v in self.raw.items()}
+        self.v = {k: torch.zeros_like(v) for k, v in self.raw.items()}
+        self.t = 0
+
+    def step(self, grads: dict, it: int = None, lrs=None, sh_active=None, sg_active=None):
+        _require_cuda()
+        sc = self.scene
+        self.t += 1
+        c = _AdamConfig()
+        c.n, c.sh_degree, c.sg_count, c.step = sc.n, sc.sh_degree, sc.sg_count, self.t
+        lr = lrs if lrs is not None else learning_rates(self.t - 1 if it is None else it, self.table)
+        for i in range(9):
+            c.lr[i] = lr[i]
+        c.beta1, c.beta2, c.eps = self.betas[0], self.betas[1], self.eps
+        c.sh_active = (sc.sh_degree + 1) ** 2 if sh_active is None else sh_active
+        c.sg_active = sc.sg_count if sg_active is None else sg_active
+        act = {k: getattr(sc, k) for k in GROUPS}
+        _check(lib().rg_adam_step(C.byref(c), C.byref(_arrays(grads)), C.byref(_arrays(self.raw)),
+                                  C.byref(_arrays(self.m)), C.byref(_arrays(self.v)),
+                                  C.byref(_arrays(act)), _stream()), "rg_adam_step")

@@ -131,3 +131,68 @@ def test_refit_rejects_other_topology():
         rg.refit_bvh(b, rg.Gaussians.from_scene(synth.random_scene(1601, 51)), cfg)
     with pytest.raises(rg.RGError):
         rg.refit_bvh(b, rg.Gaussians.from_scene(synth.random_scene(1602, 50, sh_degree=1)), cfg)
+
+
+# ---------------------------------------------------------------------------
+# fused Adam (rg_adam_step) vs oracle/train.py
+# ---------------------------------------------------------------------------
+
+def _np_raw(sc):
+    raw = {k: np.asarray(v, np.float64) for k, v in zip(rg.GROUPS, sc.arrays())}
+    raw["scale"] = np.log(raw["scale"])
+    raw["density"] = np.log(raw["density"])
+    return raw
+
+
+@pytest.mark.parametrize("n,deg,sg,sh_active,sg_active", [(3000, 3, 7, 16, 7), (777, 2, 7, 4, 0),
+                                                          (500, 0, 0, 1, 0), (1, 1, 2, 4, 1)])
+def test_adam_matches_oracle(n, deg, sg, sh_active, sg_active):
+    from oracle import train as T
+    sc = synth.random_scene(1700 + n, n, sh_degree=deg, sg_count=sg, density_range=(0.5, 40))
+    g = rg.Gaussians.from_scene(sc)
+    opt = rg.Adam(g)
+    raw = _np_raw(sc)
+    # the GPU state starts from fp32 logs: start the oracle from the same fp32 raw values
+    raw = {k: opt.raw[k].cpu().numpy().astype(np.float64) for k in rg.GROUPS}
+    m = {k: np.zeros_like(v) for k, v in raw.items()}
+    v = {k: np.zeros_like(x) for k, x in raw.items()}
+    rng = np.random.default_rng(n)
+    for it in range(5):
+        ga = {k: (rng.normal(size=raw[k].shape) * 10.0 ** rng.uniform(-3, 1)).astype(np.float32)
+              for k in rg.GROUPS}
+        opt.step({k: torch.from_numpy(ga[k]).cuda() for k in rg.GROUPS}, it=it,
+                 sh_active=sh_active, sg_active=sg_active)
+        raw, m, v, act = T.adam_step(raw, m, v, {k: ga[k].astype(np.float64) for k in rg.GROUPS}, it,
+                                     sh_active=sh_active, sg_active=sg_active)
+        torch.cuda.synchronize()
+        for k in rg.GROUPS:
+            if raw[k].size == 0:
+                continue
+            lrmax = max(T.group_lr(T.LR_BLENDER, it).values())
+            # raw: one fp32 rounding of values |x| <= ~40 per step, plus the step's relative error
+            assert np.abs(opt.raw[k].cpu().numpy() - raw[k]).max() <= 4e-6 * (1 + np.abs(raw[k]).max()), k
+            for name, mine, ref in (("m", opt.m[k], m[k]), ("v", opt.v[k], v[k])):
+                sc_ = np.abs(ref).max()
+                if sc_ > 0:
+                    assert np.abs(mine.cpu().numpy() - ref).max() <= 1e-5 * sc_, (k, name)
+            a = getattr(g, k).cpu().numpy()
+            assert np.allclose(a, act[k], rtol=2e-5, atol=1e-7), k
+    # locked coefficients untouched (raw and moments)
+    if sh_active < (deg + 1) ** 2:
+        assert not opt.m["sh"][:, sh_active:].any()
+    if sg_active < sg:
+        assert not opt.v["sg_amp"][:, sg_active:].any()
+
+
+def test_adam_empty_and_validation():
+    sc = synth.random_scene(1800, 0)
+    g = rg.Gaussians.from_scene(sc)
+    opt = rg.Adam(g)
+    opt.step(g.zeros_like_grads())
+    sc = synth.random_scene(1801, 10, sh_degree=1)
+    g = rg.Gaussians.from_scene(sc)
+    opt = rg.Adam(g)
+    with pytest.raises(rg.RGError):
+        opt.step(g.zeros_like_grads(), sh_active=5)       # > (deg+1)^2
+    with pytest.raises(rg.RGError):
+        opt.step(g.zeros_like_grads(), sg_active=1)       # > sg_count
