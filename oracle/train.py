@@ -125,3 +125,60 @@ def adam_step(raw: dict, m: dict, v: dict, grad_act: dict, it: int, *, lrs=LR_BL
         m2[k] = np.where(live, mk, m[k])
         v2[k] = np.where(live, vk, v[k])
     return raw2, m2, v2, activate(raw2)
+
+
+# ---------------------------------------------------------------------------
+# loss: L = (1 - lambda) L1 + lambda DSSIM, following 3D Gaussian
+# Splatting practice: SSIM of Wang et al. 2004 with an 11x11 Gaussian
+# window (sigma 1.5), zero padding ("same" size), C1 = 0.01^2, C2 = 0.03^2,
+# per channel, averaged over pixels and channels; DSSIM = 1 - SSIM;
+# lambda = 0.2 (readings L26-L27).  Images are [H, W, 3] (the ray order of
+# rg_render_forward's camera mode, row-major).
+# ---------------------------------------------------------------------------
+
+SSIM_C1 = 0.01 ** 2
+SSIM_C2 = 0.03 ** 2
+SSIM_WIN = 11
+SSIM_SIGMA = 1.5
+LAMBDA_DSSIM = 0.2
+
+
+def gaussian_window(size=SSIM_WIN, sigma=SSIM_SIGMA):
+    """normalised 1-D Gaussian taps g_k ~ exp(-(k - size//2)^2 / (2 sigma^2))"""
+    k = np.arange(size, dtype=np.float64) - size // 2
+    g = np.exp(-(k * k) / (2.0 * sigma * sigma))
+    return g / g.sum()
+
+
+def _filter(img, g):
+    """zero-padded 'same' correlation of each channel of img [H,W,C] with the
+    separable window g (x) g (the window is symmetric: = convolution)"""
+    import torch
+    t = torch.as_tensor(img, dtype=torch.float64).permute(2, 0, 1).unsqueeze(1)   # [C,1,H,W]
+    w = torch.as_tensor(np.outer(g, g), dtype=torch.float64)[None, None]
+    out = torch.nn.functional.conv2d(t, w, padding=len(g) // 2)
+    return out.squeeze(1).permute(1, 2, 0)
+
+
+def ssim_map(x, y):
+    """per-pixel, per-channel SSIM (Wang et al. 2004 Eq. 13) of torch fp64 [H,W,3]"""
+    import torch
+    g = gaussian_window()
+    mx, my = _filter(x, g), _filter(y, g)
+    sxx = _filter(x * x, g) - mx * mx
+    syy = _filter(y * y, g) - my * my
+    sxy = _filter(x * y, g) - mx * my
+    return ((2 * mx * my + SSIM_C1) * (2 * sxy + SSIM_C2)) / (
+        (mx * mx + my * my + SSIM_C1) * (sxx + syy + SSIM_C2))
+
+
+def l1_dssim_loss_grad(rgb, target, lam=LAMBDA_DSSIM):
+    """(loss, dL/drgb) of L = (1 - lam) mean|rgb - target| + lam (1 - mean SSIM),
+    rgb/target [H,W,3]; the gradient by fp64 autograd of the plain definition"""
+    import torch
+    x = torch.tensor(np.asarray(rgb, np.float64), requires_grad=True)
+    y = torch.tensor(np.asarray(target, np.float64))
+    l1 = torch.mean(torch.abs(x - y))
+    loss = (1.0 - lam) * l1 + lam * (1.0 - torch.mean(ssim_map(x, y)))
+    loss.backward()
+    return float(loss.detach()), x.grad.numpy()

@@ -146,3 +146,77 @@ def test_locked_coefficients_do_not_move():
         assert not np.array_equal(r2[k][:, :1], raw[k][:, :1])
     assert np.allclose(np.linalg.norm(a2["quat"], axis=-1), 1.0)
     assert np.all(a2["scale"] > 0) and np.all(a2["density"] > 0)
+
+
+# ---------------------------------------------------------------------------
+# L1 + DSSIM loss oracle
+# ---------------------------------------------------------------------------
+
+def test_gaussian_window():
+    g = T.gaussian_window()
+    assert len(g) == 11 and g.sum() == pytest.approx(1.0, abs=1e-15)
+    assert np.array_equal(g, g[::-1]) and np.argmax(g) == 5
+    # variance of the taps ~ sigma^2 (truncated at +-5 = 3.33 sigma)
+    k = np.arange(11) - 5
+    assert np.sum(g * k * k) == pytest.approx(1.5 ** 2, rel=0.01)
+
+
+def test_ssim_identical_images_is_one():
+    rng = np.random.default_rng(5)
+    x = rng.uniform(size=(20, 17, 3))
+    import torch
+    s = T.ssim_map(torch.tensor(x), torch.tensor(x)).numpy()
+    assert np.allclose(s, 1.0, atol=1e-12)
+    loss, g = T.l1_dssim_loss_grad(x, x)
+    assert loss == pytest.approx(0.0, abs=1e-12)
+    assert np.abs(g).max() < 1e-9        # L1 subgradient sign(0) = 0, SSIM at its maximum
+
+
+def test_ssim_constant_images_closed_form():
+    """interior of constant images a, b: sigma = 0, SSIM = (2ab + C1) / (a^2 + b^2 + C1)"""
+    import torch
+    a, b = 0.3, 0.7
+    x = np.full((30, 30, 3), a); y = np.full((30, 30, 3), b)
+    s = T.ssim_map(torch.tensor(x), torch.tensor(y)).numpy()
+    inner = s[5:-5, 5:-5]
+    ref = (2 * a * b + 0.01 ** 2) / (a * a + b * b + 0.01 ** 2)
+    assert np.allclose(inner, ref, rtol=1e-12)
+
+
+def test_ssim_matches_direct_windowed_statistics():
+    """a few pixels of the SSIM map recomputed by explicit weighted sums over the
+    zero-padded 11x11 neighbourhood (no convolution routine)"""
+    import torch
+    rng = np.random.default_rng(6)
+    x = rng.uniform(size=(16, 13, 3)); y = rng.uniform(size=(16, 13, 3))
+    s = T.ssim_map(torch.tensor(x), torch.tensor(y)).numpy()
+    g = T.gaussian_window()
+    for (i, j, c) in [(0, 0, 0), (7, 6, 1), (15, 12, 2), (3, 11, 0)]:
+        mx = my = exx = eyy = exy = 0.0
+        for di in range(-5, 6):
+            for dj in range(-5, 6):
+                ii, jj = i + di, j + dj
+                if 0 <= ii < 16 and 0 <= jj < 13:
+                    w = g[di + 5] * g[dj + 5]
+                    xv, yv = x[ii, jj, c], y[ii, jj, c]
+                    mx += w * xv; my += w * yv
+                    exx += w * xv * xv; eyy += w * yv * yv; exy += w * xv * yv
+        sxx, syy, sxy = exx - mx * mx, eyy - my * my, exy - mx * my
+        ref = ((2 * mx * my + 1e-4) * (2 * sxy + 9e-4)) / ((mx * mx + my * my + 1e-4) * (sxx + syy + 9e-4))
+        assert s[i, j, c] == pytest.approx(ref, rel=1e-12)
+
+
+def test_l1_dssim_gradient_finite_differences():
+    rng = np.random.default_rng(7)
+    x = rng.uniform(size=(12, 14, 3)); y = rng.uniform(size=(12, 14, 3))
+    loss, g = T.l1_dssim_loss_grad(x, y)
+    h = 1e-6
+    for (i, j, c) in [(0, 0, 0), (5, 7, 1), (11, 13, 2), (6, 0, 2)]:
+        xp = x.copy(); xp[i, j, c] += h
+        xm = x.copy(); xm[i, j, c] -= h
+        fd = (T.l1_dssim_loss_grad(xp, y)[0] - T.l1_dssim_loss_grad(xm, y)[0]) / (2 * h)
+        assert fd == pytest.approx(g[i, j, c], rel=1e-5, abs=1e-10)
+    # lambda = 0 reduces to the mean L1 with its sign gradient
+    l0, g0 = T.l1_dssim_loss_grad(x, y, lam=0.0)
+    assert l0 == pytest.approx(np.mean(np.abs(x - y)), rel=1e-12)
+    assert np.allclose(g0, np.sign(x - y) / x.size, rtol=1e-12)
