@@ -240,6 +240,23 @@ rg_status rg_adam_step(const rg_adam_config* cfg, const rg_gaussian_grads* grad_
                        const rg_param_arrays* raw, const rg_param_arrays* m,
                        const rg_param_arrays* v, const rg_param_arrays* act_out, void* stream);
 
+/* Workspace bytes of rg_l1_dssim_loss_grad for a width x height image (0 if invalid). */
+size_t rg_dssim_workspace_bytes(int32_t width, int32_t height);
+
+/* Training loss of the paper (3D Gaussian Splatting practice;
+   DESIGN.md L26-L27) and its gradient, fused:
+     L = (1 - lambda) mean|rgb - target| + lambda (1 - mean SSIM(rgb, target)),
+   SSIM (Wang et al. 2004) per pixel and channel from 11x11 Gaussian-window
+   (sigma 1.5) local moments with zero padding, C1 = 0.01^2, C2 = 0.03^2; means
+   over all pixels and the 3 channels.  rgb, target: device [height, width, 3]
+   row-major (rg_render_forward's camera-mode ray order); d_rgb (device, same
+   shape) is WRITTEN with dL/drgb (sign(0) = 0 for the L1 term); *loss (device)
+   is ACCUMULATED with L (may be NULL).  Errors: RG_ERR_INVALID_ARG for NULL
+   images, width/height < 0, lambda outside [0,1]; RG_ERR_WORKSPACE_TOO_SMALL. */
+rg_status rg_l1_dssim_loss_grad(const float* rgb, const float* target, int32_t width,
+                                int32_t height, float lambda, float* d_rgb, float* loss, void* ws,
+                                size_t ws_bytes, void* stream);
+
 /* ---- loss helper (for benchmarks; loss itself is outside the paper's path) -- */
 /* L1 loss: loss += scale * sum |rgb - target|, d_rgb = scale * sign(rgb - target)
    over n_values floats (device; loss is one device float, accumulated). */

@@ -161,6 +161,24 @@ rg_status rg_adam_step(const rg_adam_config* cfg, const rg_gaussian_grads* grad_
   return e == cudaSuccess ? RG_OK : RG_ERR_CUDA;
 }
 
+size_t rg_dssim_workspace_bytes(int32_t width, int32_t height) {
+  if (width < 0 || height < 0) return 0;
+  return dssim_workspace_bytes(height, width);
+}
+
+rg_status rg_l1_dssim_loss_grad(const float* rgb, const float* target, int32_t width,
+                                int32_t height, float lambda, float* d_rgb, float* loss, void* ws,
+                                size_t ws_bytes, void* stream) {
+  if (width < 0 || height < 0 || !(lambda >= 0.f && lambda <= 1.f)) return RG_ERR_INVALID_ARG;
+  if ((size_t)width * height == 0) return RG_OK;
+  if (!rgb || !target || !d_rgb || !ws) return RG_ERR_INVALID_ARG;
+  if (ws_bytes < dssim_workspace_bytes(height, width)) return RG_ERR_WORKSPACE_TOO_SMALL;
+  cudaGetLastError();
+  const cudaError_t e = launch_l1_dssim(rgb, target, height, width, lambda, d_rgb, loss,
+                                        static_cast<float*>(ws), static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? RG_OK : RG_ERR_CUDA;
+}
+
 rg_status rg_camera_rays(const rg_camera* cam, float* origin, float* dir, void* stream) {
   if (!cam || !rays_ok(nullptr, cam)) return RG_ERR_INVALID_ARG;
   const int n = (cam->x1 - cam->x0) * (cam->y1 - cam->y0);

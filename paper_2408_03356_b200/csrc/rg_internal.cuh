@@ -256,6 +256,9 @@ cudaError_t launch_refit(const rg_gaussians& g, const rg_config& c, char* ws, co
 cudaError_t launch_adam(const rg_adam_config& c, const rg_gaussian_grads& g,
                         const rg_gaussian_grads& raw, const rg_gaussian_grads& m,
                         const rg_gaussian_grads& v, const rg_gaussian_grads& act, cudaStream_t st);
+size_t dssim_workspace_bytes(int H, int W);
+cudaError_t launch_l1_dssim(const float* x, const float* y, int H, int W, float lam, float* d,
+                            float* loss, float* ws, cudaStream_t st);
 cudaError_t launch_camera_rays(const rg_camera& cam, float* o, float* d, cudaStream_t st);
 cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,
                            const rg_rays* rays, const rg_camera* cam, float* rgb, float* T,

@@ -148,4 +148,169 @@ cudaError_t launch_adam(const rg_adam_config& c, const rg_gaussian_grads& g,
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Fused L1 + D-SSIM loss gradient (3DGS practice; L26-L27):
+//   L = (1 - lam) mean|x - y| + lam (1 - mean SSIM(x, y)),
+// SSIM per pixel and channel from 11x11 Gaussian-window moments (sigma 1.5,
+// zero padding).  Two tiled passes over 16x16 pixel tiles:
+//   k_dssim_moments: separable filter of (x, y, x^2, y^2, xy) -> S and the
+//     partials G1 = dS/dmu_x, G2 = dS/dE[x^2], G3 = dS/dE[xy] per pixel
+//     (workspace, 9 planes), block sums of S and |x - y| -> loss;
+//   k_dssim_grad: adjoint filter of (G1, G2, G3) and
+//     dL/dx = (1-lam) sign(x-y)/N - lam/N (wG1 + 2 x wG2 + y wG3),  N = 3 H W.
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kT = 16, kHalo = 5, kE = kT + 2 * kHalo;   // tile, halo, extended tile
+constexpr float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
+
+struct SsimArgs {
+  const float* x;
+  const float* y;
+  float* d;
+  float* loss;
+  float* gmap;     // [9][H*W]: (channel, G1..G3) planes
+  int H, W;
+  float lam, invN;
+  float w[11];
+};
+
+__global__ void __launch_bounds__(256) k_dssim_moments(const SsimArgs A) {
+  __shared__ float sx[kE][kE], sy[kE][kE];
+  __shared__ float hs[5][kE][kT];
+  __shared__ float red[2][8];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int X0 = blockIdx.x * kT, Y0 = blockIdx.y * kT;
+  const int px = X0 + tx, py = Y0 + ty;
+  const bool in = px < A.W && py < A.H;
+  float s_sum = 0.f, l1_sum = 0.f;
+  for (int c = 0; c < 3; ++c) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < kE * kE; k += 256) {
+      const int ex = k % kE, ey = k / kE;
+      const int gx = X0 - kHalo + ex, gy = Y0 - kHalo + ey;
+      const bool ok = gx >= 0 && gx < A.W && gy >= 0 && gy < A.H;
+      const size_t gi = 3 * ((size_t)gy * A.W + gx) + c;
+      sx[ey][ex] = ok ? A.x[gi] : 0.f;
+      sy[ey][ex] = ok ? A.y[gi] : 0.f;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < kE * kT; k += 256) {      // horizontal pass
+      const int ox = k % kT, ey = k / kT;
+      float a = 0.f, b = 0.f, aa = 0.f, bb = 0.f, ab = 0.f;
+#pragma unroll
+      for (int t = 0; t < 11; ++t) {
+        const float u = sx[ey][ox + t], v = sy[ey][ox + t], w = A.w[t];
+        a = fmaf(w, u, a); b = fmaf(w, v, b);
+        aa = fmaf(w, u * u, aa); bb = fmaf(w, v * v, bb); ab = fmaf(w, u * v, ab);
+      }
+      hs[0][ey][ox] = a; hs[1][ey][ox] = b; hs[2][ey][ox] = aa; hs[3][ey][ox] = bb; hs[4][ey][ox] = ab;
+    }
+    __syncthreads();
+    float mx = 0.f, my = 0.f, exx = 0.f, eyy = 0.f, exy = 0.f;   // vertical pass
+#pragma unroll
+    for (int t = 0; t < 11; ++t) {
+      const float w = A.w[t];
+      mx = fmaf(w, hs[0][ty + t][tx], mx); my = fmaf(w, hs[1][ty + t][tx], my);
+      exx = fmaf(w, hs[2][ty + t][tx], exx); eyy = fmaf(w, hs[3][ty + t][tx], eyy);
+      exy = fmaf(w, hs[4][ty + t][tx], exy);
+    }
+    if (in) {
+      const float sxx = exx - mx * mx, syy = eyy - my * my, sxy = exy - mx * my;
+      const float N1 = 2.f * mx * my + kC1, N2 = 2.f * sxy + kC2;
+      const float D1 = mx * mx + my * my + kC1, D2 = sxx + syy + kC2;
+      const float D = D1 * D2;
+      const float S = N1 * N2 / D;
+      const size_t p = (size_t)py * A.W + px, HW = (size_t)A.H * A.W;
+      A.gmap[(3 * c + 0) * HW + p] = (2.f * my * (N2 - N1) - 2.f * mx * S * (D2 - D1)) / D;
+      A.gmap[(3 * c + 1) * HW + p] = -S / D2;
+      A.gmap[(3 * c + 2) * HW + p] = 2.f * N1 / D;
+      s_sum += S;
+      l1_sum += fabsf(sx[ty + kHalo][tx + kHalo] - sy[ty + kHalo][tx + kHalo]);
+    }
+  }
+  // block sums -> loss += (1-lam) L1/N - lam S/N  (+ lam once)
+  for (int o = 16; o > 0; o >>= 1) {
+    s_sum += __shfl_xor_sync(0xffffffffu, s_sum, o);
+    l1_sum += __shfl_xor_sync(0xffffffffu, l1_sum, o);
+  }
+  if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = s_sum; red[1][threadIdx.x >> 5] = l1_sum; }
+  __syncthreads();
+  if (threadIdx.x == 0 && A.loss) {
+    float s = 0.f, l = 0.f;
+    for (int k = 0; k < 8; ++k) { s += red[0][k]; l += red[1][k]; }
+    float v = ((1.f - A.lam) * l - A.lam * s) * A.invN;
+    if (blockIdx.x == 0 && blockIdx.y == 0) v += A.lam;
+    atomicAdd(A.loss, v);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_dssim_grad(const SsimArgs A) {
+  __shared__ float sg[3][kE][kE];
+  __shared__ float hs[3][kE][kT];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int X0 = blockIdx.x * kT, Y0 = blockIdx.y * kT;
+  const int px = X0 + tx, py = Y0 + ty;
+  const bool in = px < A.W && py < A.H;
+  const size_t HW = (size_t)A.H * A.W;
+  for (int c = 0; c < 3; ++c) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < kE * kE; k += 256) {
+      const int ex = k % kE, ey = k / kE;
+      const int gx = X0 - kHalo + ex, gy = Y0 - kHalo + ey;
+      const bool ok = gx >= 0 && gx < A.W && gy >= 0 && gy < A.H;
+      const size_t p = (size_t)gy * A.W + gx;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) sg[j][ey][ex] = ok ? A.gmap[(3 * c + j) * HW + p] : 0.f;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < kE * kT; k += 256) {
+      const int ox = k % kT, ey = k / kT;
+      float a = 0.f, b = 0.f, e = 0.f;
+#pragma unroll
+      for (int t = 0; t < 11; ++t) {
+        const float w = A.w[t];
+        a = fmaf(w, sg[0][ey][ox + t], a); b = fmaf(w, sg[1][ey][ox + t], b);
+        e = fmaf(w, sg[2][ey][ox + t], e);
+      }
+      hs[0][ey][ox] = a; hs[1][ey][ox] = b; hs[2][ey][ox] = e;
+    }
+    __syncthreads();
+    float a = 0.f, b = 0.f, e = 0.f;
+#pragma unroll
+    for (int t = 0; t < 11; ++t) {
+      const float w = A.w[t];
+      a = fmaf(w, hs[0][ty + t][tx], a); b = fmaf(w, hs[1][ty + t][tx], b);
+      e = fmaf(w, hs[2][ty + t][tx], e);
+    }
+    if (in) {
+      const size_t gi = 3 * ((size_t)py * A.W + px) + c;
+      const float x = A.x[gi], y = A.y[gi];
+      const float sgn = x > y ? 1.f : (x < y ? -1.f : 0.f);
+      A.d[gi] = ((1.f - A.lam) * sgn - A.lam * (a + 2.f * x * b + y * e)) * A.invN;
+    }
+  }
+}
+
+}  // namespace
+
+size_t dssim_workspace_bytes(int H, int W) { return sizeof(float) * 9 * (size_t)H * (size_t)W; }
+
+cudaError_t launch_l1_dssim(const float* x, const float* y, int H, int W, float lam, float* d,
+                            float* loss, float* ws, cudaStream_t st) {
+  if ((size_t)H * W == 0) return cudaSuccess;
+  SsimArgs A{};
+  A.x = x; A.y = y; A.d = d; A.loss = loss; A.gmap = ws;
+  A.H = H; A.W = W; A.lam = lam;
+  A.invN = (float)(1.0 / (3.0 * (double)H * (double)W));
+  double g[11], s = 0.0;
+  for (int k = 0; k < 11; ++k) { g[k] = exp(-((k - 5) * (k - 5)) / (2.0 * 1.5 * 1.5)); s += g[k]; }
+  for (int k = 0; k < 11; ++k) A.w[k] = (float)(g[k] / s);
+  const dim3 grid((W + kT - 1) / kT, (H + kT - 1) / kT);
+  k_dssim_moments<<<grid, 256, 0, st>>>(A);
+  k_dssim_grad<<<grid, 256, 0, st>>>(A);
+  count_launches(2);
+  return cudaGetLastError();
+}
+
 }  // namespace rg

@@ -71,7 +71,7 @@ class _BVH(C.Structure):
 
 
 EXPORTS = ("rg_status_string", "rg_version", "rg_kernel_launches", "rg_bvh_workspace_bytes", "rg_build_bvh",
-           "rg_refit_bvh", "rg_adam_step",
+           "rg_refit_bvh", "rg_adam_step", "rg_dssim_workspace_bytes", "rg_l1_dssim_loss_grad",
            "rg_camera_rays", "rg_render_forward", "rg_backward_workspace_bytes",
            "rg_render_backward", "rg_l1_loss_grad", "rg_fetch_log_bytes")
 
@@ -107,6 +107,10 @@ def lib(load_only: bool = False):
     L.rg_refit_bvh.argtypes = [P, P, P, SZ, P, P]
     L.rg_adam_step.restype = C.c_int
     L.rg_adam_step.argtypes = [P, P, P, P, P, P, P]
+    L.rg_dssim_workspace_bytes.restype = SZ
+    L.rg_dssim_workspace_bytes.argtypes = [I32, I32]
+    L.rg_l1_dssim_loss_grad.restype = C.c_int
+    L.rg_l1_dssim_loss_grad.argtypes = [P, P, I32, I32, C.c_float, P, P, P, SZ, P]
     L.rg_camera_rays.restype = C.c_int
     L.rg_camera_rays.argtypes = [P, P, P, P]
     L.rg_render_forward.restype = C.c_int
@@ -470,3 +474,23 @@ class Adam:
         _check(lib().rg_adam_step(C.byref(c), C.byref(_arrays(grads)), C.byref(_arrays(self.raw)),
                                   C.byref(_arrays(self.m)), C.byref(_arrays(self.v)),
                                   C.byref(_arrays(act)), _stream()), "rg_adam_step")
+
+
+def l1_dssim_loss_grad(rgb, target, width: int, height: int, lam: float = 0.2, d_rgb=None,
+                       loss=None, ws=None):
+    """fused L = (1-lam) L1 + lam DSSIM and dL/drgb (rg_l1_dssim_loss_grad);
+    rgb/target [height*width, 3] (camera-mode order).  Returns (d_rgb, loss)."""
+    _require_cuda()
+    L = lib()
+    rgb, target = rgb.contiguous(), target.contiguous()
+    if d_rgb is None:
+        d_rgb = torch.empty_like(rgb)
+    if loss is None:
+        loss = torch.zeros(1, dtype=torch.float32, device=rgb.device)
+    nb = int(L.rg_dssim_workspace_bytes(width, height))
+    if ws is None:
+        ws = torch.empty(max(nb // 4, 1), dtype=torch.float32, device=rgb.device)
+    _check(L.rg_l1_dssim_loss_grad(_ptr(rgb), _ptr(target), width, height, lam, _ptr(d_rgb),
+                                   _ptr(loss), _ptr(ws), ws.numel() * 4, _stream()),
+           "rg_l1_dssim_loss_grad")
+    return d_rgb, loss

@@ -199,3 +199,45 @@ def test_adam_empty_and_validation():
         opt.step(g.zeros_like_grads(), sh_active=5)       # > (deg+1)^2
     with pytest.raises(rg.RGError):
         opt.step(g.zeros_like_grads(), sg_active=1)       # > sg_count
+
+
+# ---------------------------------------------------------------------------
+# fused L1 + D-SSIM loss gradient vs oracle/train.py
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("H,W,lam", [(64, 64, 0.2), (37, 53, 0.2), (1, 9, 0.2), (20, 30, 0.0),
+                                     (16, 16, 1.0)])
+def test_l1_dssim_matches_oracle(H, W, lam):
+    from oracle import train as T
+    rng = np.random.default_rng(H * 1000 + W)
+    y = rng.uniform(size=(H, W, 3)).astype(np.float32)
+    x = np.clip(y + rng.normal(0, 0.1, size=y.shape), 0, 1).astype(np.float32)
+    x[0, :2] = y[0, :2]                     # exact ties: sign(0) = 0
+    d, loss = rg.l1_dssim_loss_grad(torch.from_numpy(x.reshape(-1, 3)).cuda(),
+                                    torch.from_numpy(y.reshape(-1, 3)).cuda(), W, H, lam)
+    torch.cuda.synchronize()
+    ref_loss, ref_g = T.l1_dssim_loss_grad(x.astype(np.float64), y.astype(np.float64), lam=lam)
+    assert float(loss.item()) == pytest.approx(ref_loss, rel=1e-5, abs=1e-6)
+    dg = d.cpu().numpy().reshape(H, W, 3).astype(np.float64)
+    assert np.abs(dg - ref_g).max() <= 1e-3 * np.abs(ref_g).max()
+
+
+def test_l1_dssim_full_frame_sampled():
+    """the bench's 800x800 frame: loss vs the oracle on the full image, gradient
+    compared everywhere (the fp64 oracle handles a frame in seconds)"""
+    from oracle import train as T
+    wl = synth.workload("blender")
+    sc, cam, p = wl.scene, wl.cameras[0], wl.params
+    g = rg.Gaussians.from_scene(sc)
+    cfg = rg.Config.of(p)
+    b = rg.build_bvh(g, cfg)
+    x = rg.render_forward(g, b, cfg, camera=cam)["rgb"]
+    y = torch.clamp(x + 0.05 * torch.randn_like(x), 0, 1)
+    d, loss = rg.l1_dssim_loss_grad(x, y, cam.width, cam.height)
+    torch.cuda.synchronize()
+    H, W = cam.height, cam.width
+    ref_loss, ref_g = T.l1_dssim_loss_grad(x.cpu().numpy().reshape(H, W, 3).astype(np.float64),
+                                           y.cpu().numpy().reshape(H, W, 3).astype(np.float64))
+    assert float(loss.item()) == pytest.approx(ref_loss, rel=1e-4)
+    dg = d.cpu().numpy().reshape(H, W, 3)
+    assert np.abs(dg - ref_g).max() <= 1e-3 * np.abs(ref_g).max()
