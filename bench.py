@@ -337,6 +337,53 @@ def run_ours(args):
     e7.record(stream)
     torch.cuda.synchronize()
     refit_ms = max_over_ranks(e6.elapsed_time(e7) / args.steps)
+    # ---- the other NEXT-1 kernels, each timed alone on the same workload
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        a, b_ = ev(), ev()
+        a.record(stream)
+        for _ in range(args.steps):
+            fn()
+        b_.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b_) / args.steps
+    ga = rg.Gaussians(*[t.clone() for t in g.tensors()], sh_degree=g.sh_degree, sg_count=g.sg_count)
+    opt = rg.Adam(ga)
+    adam_ms = timed(lambda: opt.step(gb.views, it=0))
+    n_el = sum(int(t.numel()) for t in g.tensors())
+    adam_bytes = 32 * n_el          # read raw, m, v, grad; write raw, m, v, activated (fp32)
+    ssim_d = torch.empty(R, 3, device=dev)
+    ssim_ws = torch.empty(int(rg.lib().rg_dssim_workspace_bytes(cam.width, cam.height)) // 4,
+                          device=dev)
+    ssim_loss = torch.zeros(1, device=dev)
+    ssim_ms = timed(lambda: rg.l1_dssim_loss_grad(fo["rgb"], tgt_dev, cam.width, cam.height,
+                                                  d_rgb=ssim_d, loss=ssim_loss, ws=ssim_ws))
+    hbm = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                      "MEASURED_PEAKS.json"))).get("hbm_gbs", 6547.8) \
+        if os.path.exists(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                       "MEASURED_PEAKS.json")) else 6547.8
+    # one full optimisation iteration of Alg. 3: UpdateBVH (rebuild),
+    # RayCast, Loss (L1 + D-SSIM), backward, AdamOptim -- on its own scene copy
+    def full_iteration():
+        bv = rg.build_bvh(ga, cfg, ws=bws)
+        f_ = rg.render_forward(ga, bv, cfg, camera=cam, out=fo, log=flog)
+        ssim_loss.zero_()
+        rg.l1_dssim_loss_grad(f_["rgb"], tgt_dev, cam.width, cam.height, d_rgb=ssim_d,
+                              loss=ssim_loss, ws=ssim_ws)
+        gb.zero_()
+        rg.render_backward(ga, bv, cfg, f_, ssim_d, camera=cam, grads=gb.views, ws=gws)
+        opt.step(gb.views, it=0)
+    iter_ms = timed(full_iteration)
+    next_rows = {
+        "alg3_iteration_ms": iter_ms,
+        "refit_bvh_ms": refit_ms,
+        "adam": {"ms": adam_ms, "elements": n_el, "bytes": adam_bytes,
+                 "achieved_gbs": adam_bytes / (adam_ms * 1e-3) / 1e9, "peak_gbs": hbm,
+                 "frac": adam_bytes / (adam_ms * 1e-3) / 1e9 / hbm, "bound": "hbm"},
+        "l1_dssim_ms": ssim_ms,
+    }
     # ---- end to end through the public API with host buffers
     for _ in range(args.warmup):
         tgt_dev.copy_(tgt_host, non_blocking=True); step(tgt_dev); loss_host.copy_(loss, non_blocking=True)
@@ -386,7 +433,7 @@ def run_ours(args):
         "fwd": {"value": world * R / (fwd_ms * 1e-3) / 1e6, "unit": "Mrays/s", "ms": fwd_ms,
                 "fps_per_gpu": 1e3 / fwd_ms, "paper_fps_rtx4090": PAPER_FPS},
         "stages_ms": stage_ms,
-        "refit_ms": refit_ms,
+        "next": next_rows,
         "e2e": {"value": total_rays / (e2e_ms * 1e-3) / 1e6, "unit": "Mrays/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(tgt_host.numel() * 4), "d2h_bytes_per_step": 4},
         "gpu_launches": int(launches),
