@@ -33,9 +33,9 @@ __device__ __forceinline__ float adam1(float th, float& m, float& v, float g, fl
 }
 
 // element-wise groups with identity or exp activation
-template <bool EXP>
+template <bool EXP, typename I>
 __device__ __forceinline__ void step_elem(float* raw, float* m, float* v, const float* g, float* act,
-                                          int64_t i, float lr, const AdamArgs& A) {
+                                          I i, float lr, const AdamArgs& A) {
   const float r = raw[i];
   float gi = g[i];
   if (EXP) gi *= expf(r);                      // d exp(r)/dr = exp(r)
@@ -45,9 +45,9 @@ __device__ __forceinline__ void step_elem(float* raw, float* m, float* v, const 
   act[i] = EXP ? expf(r2) : r2;
 }
 
-template <int D>
+template <int D, typename I>
 __device__ __forceinline__ void step_unit(float* raw, float* m, float* v, const float* g, float* act,
-                                          int64_t i, float lr, bool live, const AdamArgs& A) {
+                                          I i, float lr, bool live, const AdamArgs& A) {
   float r[D], gr[D];
   float nn = 0.f, ug = 0.f;
 #pragma unroll
@@ -74,45 +74,49 @@ __device__ __forceinline__ void step_unit(float* raw, float* m, float* v, const 
   for (int k = 0; k < D; ++k) act[D * i + k] = r2[k] / inv;
 }
 
+// 32-bit item indices (the launcher falls back to the 64-bit instantiation
+// above 2^31 items): the segment decode is then a few compares and 32-bit
+// divisions by small constants
+template <typename I>
 __global__ void __launch_bounds__(256) k_adam(const AdamArgs A) {
-  const int64_t total = A.seg[8];
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    if (t < A.seg[1]) {                                   // mean [n,3]
+  const I total = (I)A.seg[8];
+  const I s1 = (I)A.seg[1], s2 = (I)A.seg[2], s3 = (I)A.seg[3], s4 = (I)A.seg[4], s5 = (I)A.seg[5],
+          s6 = (I)A.seg[6], s7 = (I)A.seg[7];
+  const I nc = (I)A.nc, G = (I)(A.G > 0 ? A.G : 1);
+  for (I t = blockIdx.x * (I)blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
+    if (t < s1) {                                         // mean [n,3]
       step_elem<false>(A.raw.mean, A.m.mean, A.v.mean, A.g.mean, A.act.mean, t, A.lr[0], A);
-    } else if (t < A.seg[2]) {                            // quat [n,4] as units
-      step_unit<4>(A.raw.quat, A.m.quat, A.v.quat, A.g.quat, A.act.quat, t - A.seg[1], A.lr[1],
-                   true, A);
-    } else if (t < A.seg[3]) {                            // scale [n,3]
-      step_elem<true>(A.raw.scale, A.m.scale, A.v.scale, A.g.scale, A.act.scale, t - A.seg[2],
-                      A.lr[2], A);
-    } else if (t < A.seg[4]) {                            // density [n]
-      step_elem<true>(A.raw.density, A.m.density, A.v.density, A.g.density, A.act.density,
-                      t - A.seg[3], A.lr[3], A);
-    } else if (t < A.seg[5]) {                            // sh [n,nc,3]
-      const int64_t i = t - A.seg[4];
-      const int c = (int)((i / 3) % A.nc);
-      if (c < A.sh_active)
+    } else if (t < s2) {                                  // quat [n,4] as units
+      step_unit<4>(A.raw.quat, A.m.quat, A.v.quat, A.g.quat, A.act.quat, t - s1, A.lr[1], true, A);
+    } else if (t < s3) {                                  // scale [n,3]
+      step_elem<true>(A.raw.scale, A.m.scale, A.v.scale, A.g.scale, A.act.scale, t - s2, A.lr[2], A);
+    } else if (t < s4) {                                  // density [n]
+      step_elem<true>(A.raw.density, A.m.density, A.v.density, A.g.density, A.act.density, t - s3,
+                      A.lr[3], A);
+    } else if (t < s5) {                                  // sh [n,nc,3]
+      const I i = t - s4;
+      const I c = (i / 3) % nc;
+      if (c < (I)A.sh_active)
         step_elem<false>(A.raw.sh, A.m.sh, A.v.sh, A.g.sh, A.act.sh, i, c == 0 ? A.lr[4] : A.lr[5], A);
       else
         A.act.sh[i] = A.raw.sh[i];
-    } else if (t < A.seg[6]) {                            // sg_amp [n,G,3]
-      const int64_t i = t - A.seg[5];
-      if ((int)((i / 3) % A.G) < A.sg_active)
+    } else if (t < s6) {                                  // sg_amp [n,G,3]
+      const I i = t - s5;
+      if ((i / 3) % G < (I)A.sg_active)
         step_elem<false>(A.raw.sg_amp, A.m.sg_amp, A.v.sg_amp, A.g.sg_amp, A.act.sg_amp, i, A.lr[6], A);
       else
         A.act.sg_amp[i] = A.raw.sg_amp[i];
-    } else if (t < A.seg[7]) {                            // sg_sharp [n,G]
-      const int64_t i = t - A.seg[6];
-      if ((int)(i % A.G) < A.sg_active)
+    } else if (t < s7) {                                  // sg_sharp [n,G]
+      const I i = t - s6;
+      if (i % G < (I)A.sg_active)
         step_elem<false>(A.raw.sg_sharp, A.m.sg_sharp, A.v.sg_sharp, A.g.sg_sharp, A.act.sg_sharp, i,
                          A.lr[7], A);
       else
         A.act.sg_sharp[i] = A.raw.sg_sharp[i];
     } else {                                              // sg_axis [n,G,3] as units
-      const int64_t i = t - A.seg[7];
+      const I i = t - s7;
       step_unit<3>(A.raw.sg_axis, A.m.sg_axis, A.v.sg_axis, A.g.sg_axis, A.act.sg_axis, i, A.lr[8],
-                   (int)(i % A.G) < A.sg_active, A);
+                   i % G < (I)A.sg_active, A);
     }
   }
 }
@@ -143,7 +147,8 @@ cudaError_t launch_adam(const rg_adam_config& c, const rg_gaussian_grads& g,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t want = (A.seg[8] + 255) / 256;
   const int blocks = (int)(want < (int64_t)sms * 16 ? want : (int64_t)sms * 16);
-  k_adam<<<blocks, 256, 0, st>>>(A);
+  if (A.seg[8] < ((int64_t)1 << 31)) k_adam<uint32_t><<<blocks, 256, 0, st>>>(A);
+  else k_adam<int64_t><<<blocks, 256, 0, st>>>(A);
   count_launches(1);
   return cudaGetLastError();
 }
