@@ -78,7 +78,7 @@ __device__ __forceinline__ void step_unit(float* raw, float* m, float* v, const 
 // above 2^31 items): the segment decode is then a few compares and 32-bit
 // divisions by small constants
 template <typename I>
-__global__ void __launch_bounds__(256) k_adam(const AdamArgs A) {
+__global__ void __launch_bounds__(256, 8) k_adam(const AdamArgs A) {
   const I total = (I)A.seg[8];
   const I s1 = (I)A.seg[1], s2 = (I)A.seg[2], s3 = (I)A.seg[3], s4 = (I)A.seg[4], s5 = (I)A.seg[5],
           s6 = (I)A.seg[6], s7 = (I)A.seg[7];
