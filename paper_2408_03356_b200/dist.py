@@ -81,3 +81,88 @@ class GradBuffer:
     @property
     def nbytes(self):
         return self.flat.numel() * self.flat.element_size()
+
+
+class ShardedAdam:
+    """Reduce-scatter -> sharded Adam -> all-gather: each
+    rank owns the Gaussian rows [rank*s, (rank+1)*s) of every parameter group
+    (s = ceil(n / world)); the summed gradient of its rows arrives by one
+    reduce-scatter per group, its Adam state is 1/world of the full one, and the
+    updated activated parameters are all-gathered back into the replicated scene
+    the renderer reads.  Group arrays keep the rg.h caller layouts (row slices of
+    padded [n_pad, ...] storage), so the same kernels run on a shard.
+
+    `make_local(act_shard: dict) -> obj with .step(grads: dict, it)` builds the
+    per-shard optimiser that updates `act_shard` in place (rg.Adam on the GPU)."""
+
+    PAD_ROW = dict(quat=(1.0, 0.0, 0.0, 0.0))
+
+    def __init__(self, scene, make_local, group=None):
+        from . import rg
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        n = scene.n
+        self.n = n
+        self.s = -(-n // self.world) if n > 0 else 0
+        n_pad = self.s * self.world
+        self.full, self.grad = {}, {}
+        for k in GROUPS:
+            t = getattr(scene, k)
+            buf = torch.zeros((n_pad,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            buf[:n] = t
+            if n_pad > n:          # valid dummy rows: zero gradient keeps them fixed
+                if k == "quat":
+                    buf[n:, 0] = 1.0
+                elif k == "sg_axis":
+                    buf[n:, ..., 2] = 1.0
+                elif k in ("scale", "density"):
+                    buf[n:] = 1.0
+            self.full[k] = buf
+            self.grad[k] = torch.zeros_like(buf)
+        self.scene = rg.Gaussians(*[self.full[k][:n] for k in GROUPS], sh_degree=scene.sh_degree,
+                                  sg_count=scene.sg_count)
+        self.grad_views = {k: self.grad[k][:n] for k in GROUPS}
+        lo, hi = self.rank * self.s, (self.rank + 1) * self.s
+        self.act_shard = {k: self.full[k][lo:hi].clone() for k in GROUPS}
+        self.grad_shard = {k: torch.zeros_like(self.act_shard[k]) for k in GROUPS}
+        self.local = make_local(self.act_shard)
+
+    def zero_grad(self):
+        for k in GROUPS:
+            self.grad[k].zero_()
+
+    def step(self, it=None):
+        multi = dist.is_initialized() and self.world > 1
+        for k in GROUPS:
+            if self.grad[k].numel() == 0:
+                continue
+            if multi:
+                dist.reduce_scatter_tensor(self.grad_shard[k].view(-1), self.grad[k].view(-1),
+                                           op=dist.ReduceOp.SUM, group=self.group)
+            else:
+                self.grad_shard[k].copy_(self.grad[k])
+        self.local.step(self.grad_shard, it)
+        for k in GROUPS:
+            if self.full[k].numel() == 0:
+                continue
+            if multi:
+                dist.all_gather_into_tensor(self.full[k].view(-1), self.act_shard[k].view(-1),
+                                            group=self.group)
+            else:
+                self.full[k].copy_(self.act_shard[k])
+
+    @staticmethod
+    def gpu_local(sh_degree, sg_count, **adam_kw):
+        """factory of the production per-shard optimiser (fused rg_adam_step)"""
+        from . import rg
+
+        class _Local:
+            def __init__(self, act):
+                self.scene = rg.Gaussians(*[act[k] for k in GROUPS], sh_degree=sh_degree,
+                                          sg_count=sg_count)
+                self.opt = rg.Adam(self.scene, **adam_kw)
+
+            def step(self, grads, it):
+                self.opt.step(grads, it=it)
+        return _Local

@@ -94,3 +94,88 @@ def test_shard_helpers():
     assert gb.flat.sum() == 30.0 and gb.nbytes == 8 * 15 * 4
     gb.all_reduce()   # world size 1: no-op
     assert gb.flat.sum() == 30.0
+
+
+# ---------------------------------------------------------------------------
+# reduce-scatter -> sharded Adam -> all-gather (dist.ShardedAdam), host logic with
+# the oracle's Adam as the per-shard step
+# ---------------------------------------------------------------------------
+
+class _OracleLocal:
+    def __init__(self, act):
+        from oracle import train as T
+        self.T, self.act = T, act
+        self.raw = {k: act[k].numpy().astype(np.float64) for k in rgd.GROUPS}
+        self.raw["scale"] = np.log(self.raw["scale"])
+        self.raw["density"] = np.log(self.raw["density"])
+        self.m = {k: np.zeros_like(v) for k, v in self.raw.items()}
+        self.v = {k: np.zeros_like(v) for k, v in self.raw.items()}
+
+    def step(self, grads, it):
+        g = {k: grads[k].numpy().astype(np.float64) for k in rgd.GROUPS}
+        self.raw, self.m, self.v, a = self.T.adam_step(self.raw, self.m, self.v, g, it)
+        for k in rgd.GROUPS:
+            self.act[k].copy_(torch.from_numpy(a[k]).float())
+
+
+def _sharded_adam_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    try:
+        from paper_2408_03356_b200 import rg
+        rgd.init("gloo")
+        sc = synth.random_scene(91, 31, sh_degree=2, sg_count=3)     # 31 rows: padding
+        g = rg.Gaussians(*[torch.from_numpy(a.copy()) for a in sc.arrays()],
+                         sh_degree=sc.sh_degree, sg_count=sc.sg_count)
+        sa = rgd.ShardedAdam(g, _OracleLocal)
+        assert sa.s == 16 and sa.full["mean"].shape[0] == 32
+        for it in range(3):
+            sa.zero_grad()
+            rng = np.random.default_rng(1000 * it + rank)   # each rank its own gradient
+            for k in rgd.GROUPS:
+                sa.grad_views[k].copy_(torch.from_numpy(
+                    rng.normal(size=tuple(sa.grad_views[k].shape)).astype(np.float32)))
+            sa.step(it)
+        q.put((rank, {k: getattr(sa.scene, k).numpy().copy() for k in rgd.GROUPS}))
+    except Exception as e:  # noqa: BLE001
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_sharded_adam_equals_full_adam():
+    from oracle import train as T
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_sharded_adam_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+    # reference: the unsharded oracle step on the summed gradient, from the same fp32 start
+    sc = synth.random_scene(91, 31, sh_degree=2, sg_count=3)
+    raw = {k: np.asarray(a, np.float64) for k, a in zip(rgd.GROUPS, sc.arrays())}
+    raw["scale"] = np.log(np.asarray(sc.scale, np.float32).astype(np.float64))
+    raw["density"] = np.log(np.asarray(sc.density, np.float32).astype(np.float64))
+    m = {k: np.zeros_like(v) for k, v in raw.items()}
+    v = {k: np.zeros_like(x) for k, x in raw.items()}
+    for it in range(3):
+        gsum = {k: np.zeros_like(raw[k]) for k in rgd.GROUPS}
+        for r in range(world):                      # the workers' draws: one generator per
+            rng = np.random.default_rng(1000 * it + r)   # (iteration, rank), groups in order
+            for k in rgd.GROUPS:
+                gsum[k] += rng.normal(size=raw[k].shape).astype(np.float32).astype(np.float64)
+        raw, m, v, act = T.adam_step(raw, m, v, gsum, it)
+        # the sharded path rounds the activated values to fp32 each step and
+        # re-derives nothing from them (raw stays fp64 in the oracle local), so
+        # only the final fp32 rounding differs
+    for r in range(world):
+        for k in rgd.GROUPS:
+            assert np.allclose(res[r][k], act[k], rtol=2e-6, atol=1e-7), (r, k)
+    assert all(np.array_equal(res[0][k], res[1][k]) for k in rgd.GROUPS)   # replicas identical

@@ -241,3 +241,26 @@ def test_l1_dssim_full_frame_sampled():
     assert float(loss.item()) == pytest.approx(ref_loss, rel=1e-4)
     dg = d.cpu().numpy().reshape(H, W, 3)
     assert np.abs(dg - ref_g).max() <= 1e-3 * np.abs(ref_g).max()
+
+
+def test_sharded_adam_gpu_local_equals_adam():
+    """dist.ShardedAdam with the fused kernel as the per-shard step (world 1 on
+    the box; the multi-rank host logic is covered by tests/test_dist_gloo.py)"""
+    from paper_2408_03356_b200 import dist as rgd
+    sc = synth.random_scene(1900, 1001, sh_degree=3, sg_count=7)
+    g1 = rg.Gaussians.from_scene(sc)
+    g2 = rg.Gaussians.from_scene(sc)
+    sa = rgd.ShardedAdam(g1, rgd.ShardedAdam.gpu_local(3, 7))
+    opt = rg.Adam(g2)
+    rng = np.random.default_rng(0)
+    for it in range(3):
+        gr = {k: torch.from_numpy(rng.normal(size=tuple(getattr(g2, k).shape)).astype(np.float32)).cuda()
+              for k in rg.GROUPS}
+        sa.zero_grad()
+        for k in rg.GROUPS:
+            sa.grad_views[k].copy_(gr[k])
+        sa.step(it)
+        opt.step(gr, it=it)
+    torch.cuda.synchronize()
+    for k in rg.GROUPS:
+        assert torch.equal(getattr(sa.scene, k), getattr(g2, k)), k
