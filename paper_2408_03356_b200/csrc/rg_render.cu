@@ -456,19 +456,17 @@ __device__ __forceinline__ void grad_range(const WarpMem& M, WarpAcc& A, int e0,
         const float4 s0 = A.s0[j];
         const float tk = s0.x;
         if (a.x <= tk && tk <= a.y) {
-          const float4 s1 = A.s1[j];
-          if (s1.w != 0.f) {
-            const float tau = tk - a.z;
-            const float w = ex2_approx(fmaf(tau, fmaf(q.y, tau, q.x), a.w));
-            const float dldw = s0.y + (s0.z * q.z + s0.w * q.w + s1.x * cb - s1.y) * s1.z;
-            const float wd = w * dldw, wi = w * s1.z;
-            a0 += wd;
-            a1 = fmaf(wd, tau, a1);
-            a2 = fmaf(wd * tau, tau, a2);
-            a3 = fmaf(wi, s0.z, a3);
-            a4 = fmaf(wi, s0.w, a4);
-            a5 = fmaf(wi, s1.x, a5);
-          }
+          const float b2 = A.s1[j].x;
+          const float tau = tk - a.z;
+          const float w = ex2_approx(fmaf(tau, fmaf(q.y, tau, q.x), a.w));
+          const float dldw = fmaf(s0.z, q.z, fmaf(s0.w, q.w, fmaf(b2, cb, s0.y)));
+          const float wd = w * dldw;
+          a0 += wd;
+          a1 = fmaf(wd, tau, a1);
+          a2 = fmaf(wd * tau, tau, a2);
+          a3 = fmaf(w, s0.z, a3);
+          a4 = fmaf(w, s0.w, a4);
+          a5 = fmaf(w, b2, a5);
         }
       }
       float4 v = A.a[e];
@@ -956,8 +954,10 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
               H.gc = H.dc0 * cr + H.dc1 * cg + H.dc2 * cb;
               H.inv = inv_s;
             }
-            A.s0[lane] = make_float4(tk, H.dls, H.dc0, H.dc1);
-            A.s1[lane] = make_float4(H.dc2, H.gc, H.inv, live ? 1.f : 0.f);
+            // dL/dw_e = (dls - gc/sigma) + <dc, c_e>/sigma: per-sample coefficients
+            // (zero for dead samples, so the member loop needs no liveness test)
+            A.s0[lane] = make_float4(tk, H.dls - H.gc * H.inv, H.dc0 * H.inv, H.dc1 * H.inv);
+            A.s1[lane] = make_float4(H.dc2 * H.inv, 0.f, 0.f, 0.f);
             __syncwarp();
             // lane = (member, part): P2 members per pass, each member's window samples
             // split into 32/P2 parts of P2 samples; parts reduced by xor shuffles
@@ -976,23 +976,22 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
                 int kh = (int)ceilf((a.y - t0) / c.dt - kf) + 1;
                 kl = max(kl, part0);
                 kh = min(kh, min(last, part0 + P2 - 1));
+#pragma unroll 2
                 for (int k = kl; k <= kh; ++k) {
                   const float4 s0 = A.s0[k];
                   const float tkk = s0.x;
                   if (a.x <= tkk && tkk <= a.y) {
-                    const float4 s1 = A.s1[k];
-                    if (s1.w != 0.f) {
-                      const float tau_ = tkk - a.z;
-                      const float w = ex2_approx(fmaf(tau_, fmaf(q.y, tau_, q.x), a.w));
-                      const float dldw = s0.y + (s0.z * q.z + s0.w * q.w + s1.x * cbv - s1.y) * s1.z;
-                      const float wd = w * dldw, wi = w * s1.z;
-                      a0 += wd;
-                      a1 = fmaf(wd, tau_, a1);
-                      a2 = fmaf(wd * tau_, tau_, a2);
-                      a3 = fmaf(wi, s0.z, a3);
-                      a4 = fmaf(wi, s0.w, a4);
-                      a5 = fmaf(wi, s1.x, a5);
-                    }
+                    const float b2 = A.s1[k].x;
+                    const float tau_ = tkk - a.z;
+                    const float w = ex2_approx(fmaf(tau_, fmaf(q.y, tau_, q.x), a.w));
+                    const float dldw = fmaf(s0.z, q.z, fmaf(s0.w, q.w, fmaf(b2, cbv, s0.y)));
+                    const float wd = w * dldw;
+                    a0 += wd;
+                    a1 = fmaf(wd, tau_, a1);
+                    a2 = fmaf(wd * tau_, tau_, a2);
+                    a3 = fmaf(w, s0.z, a3);
+                    a4 = fmaf(w, s0.w, a4);
+                    a5 = fmaf(w, b2, a5);
                   }
                 }
               }
@@ -1121,8 +1120,8 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             H.inv = inv_s;
           }
           if (L.esub == 0) {
-            A.s0[L.j] = make_float4(tk, H.dls, H.dc0, H.dc1);
-            A.s1[L.j] = make_float4(H.dc2, H.gc, H.inv, live ? 1.f : 0.f);
+            A.s0[L.j] = make_float4(tk, H.dls - H.gc * H.inv, H.dc0 * H.inv, H.dc1 * H.inv);
+            A.s1[L.j] = make_float4(H.dc2 * H.inv, 0.f, 0.f, 0.f);
           }
         }
         const float tot_x = __shfl_sync(kFull, incl, GW - 1, GW);
