@@ -574,6 +574,56 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WarpMem&
     atomicAdd(row + 2, make_float4(dM[4], dM[5], dM[6], dM[7]));
     atomicAdd(row + 3, make_float4(dM[8], 0.f, 0.f, 0.f));
   }
+#ifndef RG_SERIAL_SG
+  // SG lobes: lane = (pair, lobe, half) item, so several pairs' record loads are in
+  // flight per instruction (the per-pair loop below waits on one pair at a time)
+  if (S.lobes > 0) {
+    const int per = 2 * S.lobes;
+    const int nitems = (32 - __clz(mask)) * per;
+    const int c0 = am.nchunks - per;                  // first SG chunk of the row
+    for (int it = (int)lane; it - (int)lane < nitems; it += 32) {
+      const int b = it / per;
+      const int c = it - b * per;
+      if (it < nitems && ((mask >> b) & 1u)) {
+        const int e = base + b;
+        const float4 acc = A.a[e];
+        const float2 acb = A.b[e];
+        const float d0 = acc.w, d1 = acb.x, d2 = acb.y;
+        const int pos = __float_as_int(M.e2[e].y);
+        const float* q = S.app + (size_t)pos * S.app_stride + kShFloats + 7 * (c >> 1);
+        const float lam = __ldg(q + 3);
+        const float dpm = R.d.x * __ldg(q + 4) + R.d.y * __ldg(q + 5) + R.d.z * __ldg(q + 6) - 1.0f;
+        const float ej = ex2_approx(lam * dpm * kLog2e);
+        const float kd = (d0 * __ldg(q) + d1 * __ldg(q + 1) + d2 * __ldg(q + 2)) * ej;
+        float4 v;
+        if ((c & 1) == 0) {
+          v = make_float4(d0 * ej, d1 * ej, d2 * ej, kd * dpm);
+        } else {
+          const float kdl = kd * lam;
+          v = make_float4(kdl * R.d.x, kdl * R.d.y, kdl * R.d.z, 0.f);
+        }
+        atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + c0 + c, v);
+      }
+    }
+  }
+  // SH: one coalesced burst per pair, lane = (channel, 4 coefficients)
+  while (mask) {
+    const int b = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const int e = base + b;
+    const float4 acc = A.a[e];
+    const float2 acb = A.b[e];
+    const float d0 = acc.w, d1 = acb.x, d2 = acb.y;
+    const int pos = __float_as_int(M.e2[e].y);
+    if (am.ch >= 0) {
+      const float dsel = am.ch == 0 ? d0 : (am.ch == 1 ? d1 : d2);
+      atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + lane,
+                make_float4(dsel * am.y.x, dsel * am.y.y, dsel * am.y.z, dsel * am.y.w));
+    }
+  }
+}
+
+#else
   while (mask) {
     const int b = __ffs(mask) - 1;
     mask &= mask - 1;
@@ -603,6 +653,8 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WarpMem&
       atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + lane, v);
   }
 }
+
+#endif
 
 __device__ __forceinline__ int skip_to(float te, int s, int B, float dt, float t0, float t1) {
   int est = (int)((te - t0) / ((float)B * dt));
