@@ -89,7 +89,7 @@ struct WarpMem {
   uint16_t stn[kStk];  // their boxes' entry distances as 16-bit order keys (fp16 rounded
                        // down): pop-time selection and pruning
   uint32_t lq[64];     // fetch: queued leaves awaiting the exact test
-  float Y[16];
+  alignas(16) float Y[16];   // Y(d) of the ray (zero past the degree), read as float4 by the scatter
 };
 struct WarpAcc {
   float4 a[kSlots];    // Sw, Sw1, Sw2, dc_r
@@ -480,39 +480,6 @@ __device__ __forceinline__ void grad_range(const WarpMem& M, WarpAcc& A, int e0,
   __syncwarp();
 }
 
-// Per-lane map of the appearance part of a gradient row (rg_internal.cuh
-// grad_stride): lane c owns float4 chunk 4 + c.  SH chunks: channel `ch`,
-// coefficients 4q..4q+3 (their Y(d) values precomputed per ray in y);
-// SG chunks: lobe `lobe`, half 0 = (k0, k1, k2, lambda), half 1 = (p0, p1, p2, -).
-struct AppMap {
-  float4 y;          // SH: Y(d) of the lane's 4 coefficients (0 past nc)
-  int ch;            // SH channel (0..2), -1 otherwise
-  int lobe;          // SG lobe, -1 otherwise
-  int half;          // SG half
-  int nchunks;
-};
-__device__ __forceinline__ AppMap app_map(const SceneView& S, const float* Y) {
-  AppMap m;
-  const int c = (int)lane_id();
-  const int nc = (S.deg + 1) * (S.deg + 1);
-  const int qsh = sh_pad(S.deg) / 4;
-  m.nchunks = 3 * qsh + 2 * S.lobes;
-  m.y = make_float4(0.f, 0.f, 0.f, 0.f);
-  m.ch = -1; m.lobe = -1; m.half = 0;
-  if (c < 3 * qsh) {
-    m.ch = c / qsh;
-    const int q = c % qsh;
-    m.y.x = 4 * q + 0 < nc ? Y[4 * q + 0] : 0.f;
-    m.y.y = 4 * q + 1 < nc ? Y[4 * q + 1] : 0.f;
-    m.y.z = 4 * q + 2 < nc ? Y[4 * q + 2] : 0.f;
-    m.y.w = 4 * q + 3 < nc ? Y[4 * q + 3] : 0.f;
-  } else if (c < m.nchunks) {
-    m.lobe = (c - 3 * qsh) >> 1;
-    m.half = (c - 3 * qsh) & 1;
-  }
-  return m;
-}
-
 // Gradient scatter of the slots in `mask` (relative to `base`), warp-cooperative:
 //  geometry: each lane owning a slot computes its 13 values, 4 float4 atomics;
 //  appearance: per slot, lane c writes chunk 4 + c (one coalesced burst).
@@ -520,9 +487,10 @@ __device__ __forceinline__ AppMap app_map(const SceneView& S, const float* Y) {
 //  Sw2 = sum w dL/dw tau^2:  dL/dmu = M^T (Sw u + Sw1 d_l),
 //  dL/dM = -(Sw u x'^T + Sw1 (u d^T + d_l x'^T) + Sw2 d_l d^T),  dL/dsigma~ = Sw / sigma~.
 __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WarpMem& M, const WarpAcc& A,
-                                           int base, unsigned mask, const Ray& R, const AppMap& am,
+                                           int base, unsigned mask, const Ray& R,
                                            float* gbuf, int gstride) {
   const unsigned lane = lane_id();
+  const int qsh = sh_pad(S.deg) / 4;   // float4 chunks per SH channel
   // drop slots with all-zero moments (never contributed)
   {
     bool nz = false;
@@ -574,13 +542,12 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WarpMem&
     atomicAdd(row + 2, make_float4(dM[4], dM[5], dM[6], dM[7]));
     atomicAdd(row + 3, make_float4(dM[8], 0.f, 0.f, 0.f));
   }
-#ifndef RG_SERIAL_SG
   // SG lobes: lane = (pair, lobe, half) item, so several pairs' record loads are in
   // flight per instruction (the per-pair loop below waits on one pair at a time)
   if (S.lobes > 0) {
     const int per = 2 * S.lobes;
     const int nitems = (32 - __clz(mask)) * per;
-    const int c0 = am.nchunks - per;                  // first SG chunk of the row
+    const int c0 = 3 * qsh;                           // first SG chunk of the row
     for (int it = (int)lane; it - (int)lane < nitems; it += 32) {
       const int b = it / per;
       const int c = it - b * per;
@@ -606,55 +573,27 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WarpMem&
       }
     }
   }
-  // SH: one coalesced burst per pair, lane = (channel, 4 coefficients)
-  while (mask) {
-    const int b = __ffs(mask) - 1;
-    mask &= mask - 1;
-    const int e = base + b;
-    const float4 acc = A.a[e];
-    const float2 acb = A.b[e];
-    const float d0 = acc.w, d1 = acb.x, d2 = acb.y;
-    const int pos = __float_as_int(M.e2[e].y);
-    if (am.ch >= 0) {
-      const float dsel = am.ch == 0 ? d0 : (am.ch == 1 ? d1 : d2);
-      atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + lane,
-                make_float4(dsel * am.y.x, dsel * am.y.y, dsel * am.y.z, dsel * am.y.w));
-    }
-  }
-}
-
-#else
-  while (mask) {
-    const int b = __ffs(mask) - 1;
-    mask &= mask - 1;
-    const int e = base + b;
-    const float4 acc = A.a[e];
-    const float2 acb = A.b[e];
-    const float d0 = acc.w, d1 = acb.x, d2 = acb.y;
-    const int pos = __float_as_int(M.e2[e].y);
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (am.ch >= 0) {            // SH: dc[ch] * Y(d) of 4 coefficients
-      const float dsel = am.ch == 0 ? d0 : (am.ch == 1 ? d1 : d2);
-      v = make_float4(dsel * am.y.x, dsel * am.y.y, dsel * am.y.z, dsel * am.y.w);
-    } else if (am.lobe >= 0) {   // SG lobe j: e = exp(lambda (d.p - 1)), kd = <dc, k> e
-      const float* q = S.app + (size_t)pos * S.app_stride + kShFloats + 7 * am.lobe;
-      const float lam = __ldg(q + 3);
-      const float dpm = R.d.x * __ldg(q + 4) + R.d.y * __ldg(q + 5) + R.d.z * __ldg(q + 6) - 1.0f;
-      const float ej = ex2_approx(lam * dpm * kLog2e);
-      if (am.half == 0) {
-        const float kd = (d0 * __ldg(q) + d1 * __ldg(q + 1) + d2 * __ldg(q + 2)) * ej;
-        v = make_float4(d0 * ej, d1 * ej, d2 * ej, kd * dpm);
-      } else {
-        const float kdl = (d0 * __ldg(q) + d1 * __ldg(q + 1) + d2 * __ldg(q + 2)) * ej * lam;
-        v = make_float4(kdl * R.d.x, kdl * R.d.y, kdl * R.d.z, 0.f);
+  // SH: lane = (pair, channel, 4 coefficients) item: dL/dc~_m = dc[ch] Y_m(d),
+  // Y(d) from shared memory (zero past the degree)
+  {
+    const int per = 3 * qsh;
+    const int nitems = (32 - __clz(mask)) * per;
+    for (int it = (int)lane; it - (int)lane < nitems; it += 32) {
+      const int b = it / per;
+      const int c = it - b * per;
+      if (it < nitems && ((mask >> b) & 1u)) {
+        const int e = base + b;
+        const int ch = c / qsh, qq = c - ch * qsh;
+        const float dsel = ch == 0 ? A.a[e].w : (ch == 1 ? A.b[e].x : A.b[e].y);
+        const int pos = __float_as_int(M.e2[e].y);
+        const float4 y = *reinterpret_cast<const float4*>(&M.Y[4 * qq]);
+        atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + c,
+                  make_float4(dsel * y.x, dsel * y.y, dsel * y.z, dsel * y.w));
       }
     }
-    if ((int)lane < am.nchunks)
-      atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + lane, v);
   }
 }
 
-#endif
 
 __device__ __forceinline__ int skip_to(float te, int s, int B, float dt, float t0, float t1) {
   int est = (int)((te - t0) / ((float)B * dt));
@@ -758,7 +697,6 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
   if (hit && !(BWD && gr0 == 0.f && gr1 == 0.f && gr2 == 0.f)) {
     R.inv = make_float3(1.0f / R.d.x, 1.0f / R.d.y, 1.0f / R.d.z);
     R.oinv = make_float3(R.o.x * R.inv.x, R.o.y * R.inv.y, R.o.z * R.inv.z);
-    AppMap am;
     {   // Y(d) once per ray (zero past the degree): colour set-up and SH gradients
       float Y[16];
       sh_basis(P.S.deg, R.d.x, R.d.y, R.d.z, Y);
@@ -766,7 +704,6 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
 #pragma unroll
       for (int m = 0; m < 16; ++m)
         if ((int)lane == m) M.Y[m] = m < nc ? Y[m] : 0.f;
-      if (BWD) am = app_map(P.S, Y);
       __syncwarp();
     }
     Lanes<GW> L;
@@ -800,7 +737,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
               const unsigned gm = h ? gone1 : gone0;
               if (!gm) continue;
               if (nret + __popc(gm) > 32) {
-                scatter_batch(P.S, M, A, kRet, nret >= 32 ? kFull : ((1u << nret) - 1u), R, am,
+                scatter_batch(P.S, M, A, kRet, nret >= 32 ? kFull : ((1u << nret) - 1u), R,
                               P.gbuf, P.gstride);
                 nret = 0;
                 __syncwarp();
@@ -1204,7 +1141,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
               }
               __syncwarp();
               grad_range<GW>(M, A, kA, kA + got);
-              scatter_batch(P.S, M, A, kA, got >= 32 ? kFull : ((1u << got) - 1u), R, am, P.gbuf,
+              scatter_batch(P.S, M, A, kA, got >= 32 ? kFull : ((1u << got) - 1u), R, P.gbuf,
                             P.gstride);
               remaining -= got;
               if (got > 0) cur2 = shfl64(key, got - 1);
@@ -1226,9 +1163,9 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
     if (BWD) {
       const unsigned m0 = count >= 32 ? kFull : ((1u << count) - 1u);
       const unsigned m1 = count >= 64 ? kFull : (count > 32 ? ((1u << (count - 32)) - 1u) : 0u);
-      scatter_batch(P.S, M, A, 0, m0, R, am, P.gbuf, P.gstride);
-      scatter_batch(P.S, M, A, 32, m1, R, am, P.gbuf, P.gstride);
-      scatter_batch(P.S, M, A, kRet, nret >= 32 ? kFull : ((1u << nret) - 1u), R, am, P.gbuf,
+      scatter_batch(P.S, M, A, 0, m0, R, P.gbuf, P.gstride);
+      scatter_batch(P.S, M, A, 32, m1, R, P.gbuf, P.gstride);
+      scatter_batch(P.S, M, A, kRet, nret >= 32 ? kFull : ((1u << nret) - 1u), R, P.gbuf,
                     P.gstride);
     } else if (lg != nullptr && lane == 0) {
       lg[0] = log_ok ? lp : -1;
