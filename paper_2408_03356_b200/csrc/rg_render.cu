@@ -573,27 +573,23 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WarpMem&
       }
     }
   }
-  // SH: lane = (pair, channel, 4 coefficients) item: dL/dc~_m = dc[ch] Y_m(d),
-  // Y(d) from shared memory (zero past the degree)
-  {
-    const int per = 3 * qsh;
-    const int nitems = (32 - __clz(mask)) * per;
-    for (int it = (int)lane; it - (int)lane < nitems; it += 32) {
-      const int b = it / per;
-      const int c = it - b * per;
-      if (it < nitems && ((mask >> b) & 1u)) {
-        const int e = base + b;
-        const int ch = c / qsh, qq = c - ch * qsh;
-        const float dsel = ch == 0 ? A.a[e].w : (ch == 1 ? A.b[e].x : A.b[e].y);
-        const int pos = __float_as_int(M.e2[e].y);
-        const float4 y = *reinterpret_cast<const float4*>(&M.Y[4 * qq]);
-        atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + c,
-                  make_float4(dsel * y.x, dsel * y.y, dsel * y.z, dsel * y.w));
-      }
+  // SH: one coalesced burst per pair, lane = (channel, 4 coefficients):
+  // dL/dc~_m = dc[ch] Y_m(d), Y(d) from shared memory (zero past the degree)
+  const int ch = (int)lane < 3 * qsh ? (int)lane / qsh : -1;
+  float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (ch >= 0) y = *reinterpret_cast<const float4*>(&M.Y[4 * ((int)lane - ch * qsh)]);
+  while (mask) {
+    const int b = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const int e = base + b;
+    const int pos = __float_as_int(M.e2[e].y);
+    if (ch >= 0) {
+      const float dsel = ch == 0 ? A.a[e].w : (ch == 1 ? A.b[e].x : A.b[e].y);
+      atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + lane,
+                make_float4(dsel * y.x, dsel * y.y, dsel * y.z, dsel * y.w));
     }
   }
 }
-
 
 __device__ __forceinline__ int skip_to(float te, int s, int B, float dt, float t0, float t1) {
   int est = (int)((te - t0) / ((float)B * dt));
