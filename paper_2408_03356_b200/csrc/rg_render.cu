@@ -231,16 +231,17 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
     int node;
     {
       const int nwin = min(sp, 32);
-      const unsigned k16 = (int)lane < nwin ? (unsigned)M.stn[sp - 1 - (int)lane] : 0xFFFFu;
+      unsigned k16 = 0xFFFFu, nid = 0;
+      if ((int)lane < nwin) { k16 = M.stn[sp - 1 - (int)lane]; nid = M.stk[sp - 1 - (int)lane]; }
       const unsigned kmin = __reduce_min_sync(kFull, k16);
       if (stn_dec(kmin) > te_lim + slack) {
         sp -= nwin;
         continue;
       }
-      const int si = sp - 1 - (__ffs(__ballot_sync(kFull, k16 == kmin)) - 1);
-      node = (int)M.stk[si];
-      __syncwarp();
-      if (lane == 0 && si != sp - 1) { M.stk[si] = M.stk[sp - 1]; M.stn[si] = M.stn[sp - 1]; }
+      const int src = __ffs(__ballot_sync(kFull, k16 == kmin)) - 1;
+      node = (int)__shfl_sync(kFull, nid, src);
+      // lane 0 holds the top entry: it fills the winner's hole
+      if (lane == 0 && src != 0) { M.stk[sp - 1 - src] = nid; M.stn[sp - 1 - src] = (uint16_t)k16; }
       --sp;
       __syncwarp();
     }
