@@ -46,7 +46,7 @@ constexpr int kTrans = kA;             // transient chunk slots (slab sets > kA)
 constexpr int kRet = kA + 32;          // retired (expired, not yet scattered) slots, backward
 constexpr int kSlots = kA + 64;
 static_assert(kA == 64, "expire/n_in handle two 32-slot chunks");
-constexpr int kStk = 240;              // traversal stack (wide nodes; max depth seen: C1 56, C3 149)
+constexpr int kStk = 216;              // traversal stack (wide nodes; max depth seen: C1 56, C3 149)
 constexpr unsigned kFull = 0xffffffffu;
 
 struct Counters {
@@ -88,7 +88,7 @@ struct WarpMem {
   uint32_t stk[kStk];  // stacked wide node ids
   uint16_t stn[kStk];  // their boxes' entry distances as 16-bit order keys (fp16 rounded
                        // down): pop-time selection and pruning
-  uint32_t lq[64];     // fetch: queued leaves awaiting the exact test
+  uint32_t lq[96];     // fetch: queued leaves awaiting the exact test (< 32 + 2 x 32)
   alignas(16) float Y[16];   // Y(d) of the ray (zero past the degree), read as float4 by the scatter
 };
 struct WarpAcc {
@@ -224,11 +224,12 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
       te_lim = fkey_inv((uint32_t)(kth >> 32));
     }
   };
+  // Best-first-ish DFS: each iteration pops the two nodes with the smallest entry
+  // distances among the top 32 stack entries and visits both (their 14 child-box
+  // loads per lane are in flight together); when even the nearest lies beyond the
+  // k-th key, all 32 are dropped.  Pushes are unordered (the pop selects).
   while (sp > 0) {
-#ifndef RG_NEAREST_TOP
-    // pop the node with the smallest entry distance among the top 32 (approximately
-    // best-first); when even that one lies beyond the k-th key, drop all 32
-    int node;
+    int nodeA, nodeB = -1;
     {
       const int nwin = min(sp, 32);
       unsigned k16 = 0xFFFFu, nid = 0;
@@ -238,52 +239,80 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
         sp -= nwin;
         continue;
       }
-      const int src = __ffs(__ballot_sync(kFull, k16 == kmin)) - 1;
-      node = (int)__shfl_sync(kFull, nid, src);
-      // lane 0 holds the top entry: it fills the winner's hole
-      if (lane == 0 && src != 0) { M.stk[sp - 1 - src] = nid; M.stn[sp - 1 - src] = (uint16_t)k16; }
-      --sp;
+      const int srcA = __ffs(__ballot_sync(kFull, k16 == kmin)) - 1;
+      nodeA = (int)__shfl_sync(kFull, nid, srcA);
+      int srcB = -1;
+#ifndef RG_ONE_NODE
+      const unsigned k16b = (int)lane == srcA ? 0xFFFFu : k16;
+      const unsigned kmin2 = __reduce_min_sync(kFull, k16b);
+      if (kmin2 != 0xFFFFu && stn_dec(kmin2) <= te_lim + slack) {
+        srcB = __ffs(__ballot_sync(kFull, k16b == kmin2)) - 1;
+        nodeB = (int)__shfl_sync(kFull, nid, srcB);
+      }
+#endif
+      // remove the popped entries: the surviving top entries (lanes 0, 1) fill the
+      // holes the popped ones leave further down
+      if (srcB < 0) {
+        if (lane == 0 && srcA != 0) { M.stk[sp - 1 - srcA] = nid; M.stn[sp - 1 - srcA] = (uint16_t)k16; }
+        sp -= 1;
+      } else {
+        const bool m0 = srcA != 0 && srcB != 0, m1 = srcA != 1 && srcB != 1;
+        const int h1 = srcA >= 2 ? srcA : srcB, h2 = srcA >= 2 ? srcB : srcA;   // holes (>= 2 first)
+        int hole = -1;
+        if (lane == 0 && m0) hole = h1;
+        if (lane == 1 && m1) hole = m0 ? h2 : h1;
+        if (hole >= 2) { M.stk[sp - 1 - hole] = nid; M.stn[sp - 1 - hole] = (uint16_t)k16; }
+        sp -= 2;
+      }
       __syncwarp();
     }
-#else
-    const int node = (int)M.stk[sp - 1];
-    const float ntn = stn_dec(M.stn[sp - 1]);
-    --sp;
-    if (ntn > te_lim + slack) continue;   // the k-buffer filled since it was pushed
-#endif
-    if (lane == 0) cnt.nodes++;
-    const WideNode& W = S.wide[node];
-    const int child = __ldg(&W.child[lane]);
-    float tn, tf;
-    box_t(__ldg(&W.lox[lane]), __ldg(&W.loy[lane]), __ldg(&W.loz[lane]), __ldg(&W.hix[lane]),
-          __ldg(&W.hiy[lane]), __ldg(&W.hiz[lane]), R.inv, R.oinv, tn, tf);
-    const bool hit = child != kWideEmpty && tn <= tf && tf >= lo_s && tn <= hi_s &&
-                     tn <= te_lim + slack;
-    // queue box-passing leaves
+    if (lane == 0) cnt.nodes += nodeB >= 0 ? 2 : 1;
+    const bool two = nodeB >= 0;
+    const WideNode& WA = S.wide[nodeA];
+    const WideNode& WB = S.wide[two ? nodeB : nodeA];
+    const int childA = __ldg(&WA.child[lane]);
+    const float alx = __ldg(&WA.lox[lane]), aly = __ldg(&WA.loy[lane]), alz = __ldg(&WA.loz[lane]);
+    const float ahx = __ldg(&WA.hix[lane]), ahy = __ldg(&WA.hiy[lane]), ahz = __ldg(&WA.hiz[lane]);
+    int childB = kWideEmpty;
+    float blx = 0.f, bly = 0.f, blz = 0.f, bhx = 0.f, bhy = 0.f, bhz = 0.f;
+    if (two) {
+      childB = __ldg(&WB.child[lane]);
+      blx = __ldg(&WB.lox[lane]); bly = __ldg(&WB.loy[lane]); blz = __ldg(&WB.loz[lane]);
+      bhx = __ldg(&WB.hix[lane]); bhy = __ldg(&WB.hiy[lane]); bhz = __ldg(&WB.hiz[lane]);
+    }
+    float tnA, tfA, tnB, tfB;
+    box_t(alx, aly, alz, ahx, ahy, ahz, R.inv, R.oinv, tnA, tfA);
+    box_t(blx, bly, blz, bhx, bhy, bhz, R.inv, R.oinv, tnB, tfB);
+    const bool hitA = childA != kWideEmpty && tnA <= tfA && tfA >= lo_s && tnA <= hi_s &&
+                      tnA <= te_lim + slack;
+    const bool hitB = childB != kWideEmpty && tnB <= tfB && tfB >= lo_s && tnB <= hi_s &&
+                      tnB <= te_lim + slack;
+    // queue box-passing leaves (A's, then B's)
     {
-      const unsigned lm = __ballot_sync(kFull, hit && child < 0);
-      if (lm) {
+      const unsigned lmA = __ballot_sync(kFull, hitA && childA < 0);
+      const unsigned lmB = __ballot_sync(kFull, hitB && childB < 0);
+      if (lmA | lmB) {
         __syncwarp();
-        if (hit && child < 0) M.lq[qn + __popc(lm & lt_mask)] = (uint32_t)(~child);
-        qn += __popc(lm);
+        if (hitA && childA < 0) M.lq[qn + __popc(lmA & lt_mask)] = (uint32_t)(~childA);
+        if (hitB && childB < 0) M.lq[qn + __popc(lmA) + __popc(lmB & lt_mask)] = (uint32_t)(~childB);
+        qn += __popc(lmA) + __popc(lmB);
       }
     }
-    // internal children
-    const unsigned im = __ballot_sync(kFull, hit && child >= 0);
-    if (im) {
-#ifndef RG_NEAREST_TOP   // any order: the pop selects
-      const unsigned k16 = stn_enc(tn);
-      const int rank = __popc(im & lt_mask);
-#else                     // the nearest child on top, the rest in lane order below it
-      const unsigned k16 = (hit && child >= 0) ? stn_enc(tn) : 0xFFFFu;
-      const unsigned kmin = __reduce_min_sync(kFull, k16);
-      const int first = __ffs(__ballot_sync(kFull, k16 == kmin)) - 1;
-      const int rank = (int)lane == first ? __popc(im) - 1 : __popc(im & lt_mask & ~(1u << first));
-#endif
-      const int np = __popc(im);
+    // internal children, any order (the pop selects)
+    const unsigned imA = __ballot_sync(kFull, hitA && childA >= 0);
+    const unsigned imB = __ballot_sync(kFull, hitB && childB >= 0);
+    if (imA | imB) {
+      const int npA = __popc(imA), np = npA + __popc(imB);
       __syncwarp();
       if (sp + np <= kStk) {
-        if (hit && child >= 0) { M.stk[sp + rank] = (uint32_t)child; M.stn[sp + rank] = (uint16_t)k16; }
+        if (hitA && childA >= 0) {
+          const int r = sp + __popc(imA & lt_mask);
+          M.stk[r] = (uint32_t)childA; M.stn[r] = stn_enc(tnA);
+        }
+        if (hitB && childB >= 0) {
+          const int r = sp + npA + __popc(imB & lt_mask);
+          M.stk[r] = (uint32_t)childB; M.stn[r] = stn_enc(tnB);
+        }
         sp += np;
 #ifdef RG_STACK_PROBE
         if (lane == 0 && (uint32_t)sp > cnt.stackov) cnt.stackov = sp;   // max depth, not overflows
@@ -293,7 +322,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
       }
       __syncwarp();
     }
-    if (qn >= 32) flush(32);
+    while (qn >= 32) flush(32);
   }
   while (qn > 0) flush(min(qn, 32));
   return nk;
