@@ -181,10 +181,12 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
       }
     }
     // drop the consumed queue entries
-    const int rem = qn - n;
+    const int rem = qn - n;   // < 64 left over (two nodes' leaves per iteration)
     const uint32_t mv = (int)lane < rem ? M.lq[n + lane] : 0u;
+    const uint32_t mv2 = (int)lane + 32 < rem ? M.lq[n + 32 + lane] : 0u;
     __syncwarp();
     if ((int)lane < rem) M.lq[lane] = mv;
+    if ((int)lane + 32 < rem) M.lq[32 + lane] = mv2;
     qn = rem;
     const unsigned cmask = __ballot_sync(kFull, cand);
     if (!cmask) return;
