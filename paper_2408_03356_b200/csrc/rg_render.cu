@@ -46,7 +46,14 @@ constexpr int kTrans = kA;             // transient chunk slots (slab sets > kA)
 constexpr int kRet = kA + 32;          // retired (expired, not yet scattered) slots, backward
 constexpr int kSlots = kA + 64;
 static_assert(kA == 64, "expire/n_in handle two 32-slot chunks");
-constexpr int kStk = 216;              // traversal stack (wide nodes; max depth seen: C1 56, C3 149)
+#ifndef RG_STK_FWD
+#define RG_STK_FWD 512
+#endif
+// traversal stack entries (wide nodes; max depth seen: C1 ~60, C3 170): the forward
+// has shared memory to spare; the backward traverses only for rays whose fetch log
+// overflowed and must stay within its 48 KB block budget
+constexpr int kStkFwd = RG_STK_FWD;
+constexpr int kStkBwd = 216;
 constexpr unsigned kFull = 0xffffffffu;
 
 struct Counters {
@@ -83,10 +90,12 @@ struct RenderArgs {
 
 // per-slot entry (AoS, three float4 so a lane reads a slot with LDS.128):
 //   e0 = {t_entry, t_exit, t_mid, c0}   e1 = {c1, c2, r, g}   e2 = {b, pos, idx, -}
-struct WarpMem {
+template <int STK>
+struct WarpMemT {
+  static constexpr int kStack = STK;
   float4 e0[kSlots], e1[kSlots], e2[kSlots];
-  uint32_t stk[kStk];  // stacked wide node ids
-  uint16_t stn[kStk];  // their boxes' entry distances as 16-bit order keys (fp16 rounded
+  uint32_t stk[STK];   // stacked wide node ids
+  uint16_t stn[STK];  // their boxes' entry distances as 16-bit order keys (fp16 rounded
                        // down): pop-time selection and pruning
   uint32_t lq[96];     // fetch: queued leaves awaiting the exact test (< 32 + 2 x 32)
   alignas(16) float Y[16];   // Y(d) of the ray (zero past the degree), read as float4 by the scatter
@@ -143,7 +152,8 @@ __device__ __forceinline__ float stn_dec(unsigned k) {
 // smallest keys (t_entry bits, index) > cursor among Gaussians whose exact
 // support interval satisfies t_exit >= seg_lo and t_entry <= seg_hi.
 // Result: lane l < return value holds the l-th smallest key and its position.
-__device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo, float seg_hi,
+template <class WM>
+__device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, float seg_hi,
                      unsigned long long cursor, int kmax, unsigned long long& key, uint32_t& pos,
                      Counters& cnt) {
   const unsigned lane = lane_id();
@@ -306,7 +316,7 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
     if (imA | imB) {
       const int npA = __popc(imA), np = npA + __popc(imB);
       __syncwarp();
-      if (sp + np <= kStk) {
+      if (sp + np <= WM::kStack) {
         if (hitA && childA >= 0) {
           const int r = sp + __popc(imA & lt_mask);
           M.stk[r] = (uint32_t)childA; M.stn[r] = stn_enc(tnA);
@@ -336,16 +346,16 @@ __device__ int fetch(const SceneView& S, WarpMem& M, const Ray& R, float seg_lo,
 // VEC: 16-B loads (forward: -5% time); scalar loads in the backward, where the
 // extra registers of the vector form cost more (+3%) than they save
 template <bool VEC>
-__device__ __forceinline__ float3 pair_color(const SceneView& S, const WarpMem& M, int pos,
+__device__ __forceinline__ float3 pair_color(const SceneView& S, const float* Y, int pos,
                                              const float3& d) {
   if (!VEC) {
   const float* ap = S.app + (size_t)pos * S.app_stride;
   float r = 0.f, g = 0.f, b = 0.f;
 #pragma unroll
   for (int m = 0; m < 16; ++m) {
-    r = fmaf(M.Y[m], __ldg(ap + 3 * m), r);
-    g = fmaf(M.Y[m], __ldg(ap + 3 * m + 1), g);
-    b = fmaf(M.Y[m], __ldg(ap + 3 * m + 2), b);
+    r = fmaf(Y[m], __ldg(ap + 3 * m), r);
+    g = fmaf(Y[m], __ldg(ap + 3 * m + 1), g);
+    b = fmaf(Y[m], __ldg(ap + 3 * m + 2), b);
   }
   for (int j = 0; j < S.lobes; ++j) {
     const float* q = ap + kShFloats + 7 * j;
@@ -368,7 +378,7 @@ __device__ __forceinline__ float3 pair_color(const SceneView& S, const WarpMem& 
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int f = 4 * i + k;
-      acc[f % 3] = fmaf(M.Y[f / 3], vv[k], acc[f % 3]);
+      acc[f % 3] = fmaf(Y[f / 3], vv[k], acc[f % 3]);
     }
   }
   const int L = S.lobes;
@@ -410,8 +420,8 @@ __device__ __forceinline__ float3 pair_color(const SceneView& S, const WarpMem& 
 #else
 #define RG_SCATTER_ATTR __forceinline__
 #endif
-template <bool VEC>
-__device__ RG_SETUP_ATTR void setup_pair(const SceneView& S, WarpMem& M, int sl, const Ray& R,
+template <bool VEC, class WM>
+__device__ RG_SETUP_ATTR void setup_pair(const SceneView& S, WM& M, int sl, const Ray& R,
                                         uint32_t pos) {
   const float4* gp = S.geom + 4 * (size_t)pos;
   const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2), g3 = __ldg(gp + 3);
@@ -425,7 +435,7 @@ __device__ RG_SETUP_ATTR void setup_pair(const SceneView& S, WarpMem& M, int sl,
   const float u2 = g2.z * x0 + g2.w * x1 + g3.x * x2;
   const float qm = u0 * u0 + u1 * u1 + u2 * u2;
   const float b1 = u0 * pg.dl0 + u1 * pg.dl1 + u2 * pg.dl2;
-  const float3 col = pair_color<VEC>(S, M, (int)pos, R.d);
+  const float3 col = pair_color<VEC>(S, M.Y, (int)pos, R.d);
   M.e0[sl] = make_float4(pg.te, pg.tx, pg.tm, lg2_approx(g0.w) - 0.5f * kLog2e * qm);
   M.e1[sl] = make_float4(-kLog2e * b1, -0.5f * kLog2e * pg.A, col.x, col.y);
   M.e2[sl] = make_float4(col.z, __int_as_float((int)pos), g3.z, 0.f);
@@ -445,8 +455,8 @@ struct Lanes {
 };
 
 // sigma and sigma*c at this lane's sample from slots [e0, e1)
-template <int GW>
-__device__ __forceinline__ void eval_range(const WarpMem& M, int e0, int e1, const Lanes<GW>& L,
+template <int GW, class WM>
+__device__ __forceinline__ void eval_range(const WM& M, int e0, int e1, const Lanes<GW>& L,
                                            float tk, bool val, float& s, float& r, float& g,
                                            float& b, uint32_t& evals) {
 #pragma unroll 2
@@ -473,8 +483,8 @@ struct SampleGrad {   // per-sample backward quantities (lanes of sample j)
 // accumulate the per-pair moments of slots [e0, e1) over this group's samples:
 // lane = slot, loop over the GW samples whose backward values the composite
 // step left in A.s0/A.s1 (broadcast reads), moments kept in registers.
-template <int GW>
-__device__ __forceinline__ void grad_range(const WarpMem& M, WarpAcc& A, int e0, int e1) {
+template <int GW, class WM>
+__device__ __forceinline__ void grad_range(const WM& M, WarpAcc& A, int e0, int e1) {
   __syncwarp();
   for (int base = e0; base < e1; base += 32) {
     const int e = base + (int)lane_id();
@@ -518,7 +528,8 @@ __device__ __forceinline__ void grad_range(const WarpMem& M, WarpAcc& A, int e0,
 //  With x = x' + tau d, u = M x', d_l = M d and Sw = sum w dL/dw, Sw1 = sum w dL/dw tau,
 //  Sw2 = sum w dL/dw tau^2:  dL/dmu = M^T (Sw u + Sw1 d_l),
 //  dL/dM = -(Sw u x'^T + Sw1 (u d^T + d_l x'^T) + Sw2 d_l d^T),  dL/dsigma~ = Sw / sigma~.
-__device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WarpMem& M, const WarpAcc& A,
+template <class WM>
+__device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, const WarpAcc& A,
                                            int base, unsigned mask, const Ray& R,
                                            float* gbuf, int gstride) {
   const unsigned lane = lane_id();
@@ -657,8 +668,9 @@ __device__ __forceinline__ void kadd(float& s, float& comp, float x) {
   s = t;
 }
 
+template <class WM>
 __device__ __forceinline__ void dbg_put(const RenderArgs& P, int ray, int& dbg_n, int s, int n,
-                                        const WarpMem& M, int first) {
+                                        const WM& M, int first) {
   for (int e = (int)lane_id(); e < n; e += 32)
     if (dbg_n + e < P.dbg_cap) {
       int32_t* r = P.dbg_rec + 2 * ((size_t)ray * P.dbg_cap + dbg_n + e);
@@ -676,18 +688,20 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
   // shared-window offsets; the dynamic (extern) form made the compiler re-derive the
   // window base (S2UR SR_CgaCtaId + ULEA) at loop heads of the hot loops
 #ifdef RG_STATIC_SMEM
-  __shared__ WarpMem sm_mem[kWarps];
+  using WM = WarpMemT<BWD ? kStkBwd : kStkFwd>;
+  __shared__ WM sm_mem[kWarps];
   __shared__ WarpAcc sm_acc[BWD ? kWarps : 1];
   const unsigned lane = lane_id();
   const int wid = threadIdx.x >> 5;
-  WarpMem& M = sm_mem[wid];
+  WM& M = sm_mem[wid];
   WarpAcc& A = sm_acc[BWD ? wid : 0];
 #else
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const unsigned lane = lane_id();
   const int wid = threadIdx.x >> 5;
-  WarpMem& M = reinterpret_cast<WarpMem*>(smem_raw)[wid];
-  WarpAcc& A = reinterpret_cast<WarpAcc*>(smem_raw + sizeof(WarpMem) * kWarps)[BWD ? wid : 0];
+  using WM = WarpMemT<BWD ? kStkBwd : kStkFwd>;
+  WM& M = reinterpret_cast<WM*>(smem_raw)[wid];
+  WarpAcc& A = reinterpret_cast<WarpAcc*>(smem_raw + sizeof(WM) * kWarps)[BWD ? wid : 0];
 #endif
   int ray;
   Ray R;
@@ -1377,8 +1391,8 @@ void launch_render(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st)
   else launch_gw<BWD, 1>(A, grid, smem, st);
 }
 
-constexpr size_t kSmemFwd = sizeof(WarpMem) * kWarps;
-constexpr size_t kSmemBwd = (sizeof(WarpMem) + sizeof(WarpAcc)) * kWarps;
+constexpr size_t kSmemFwd = sizeof(WarpMemT<kStkFwd>) * kWarps;
+constexpr size_t kSmemBwd = (sizeof(WarpMemT<kStkBwd>) + sizeof(WarpAcc)) * kWarps;
 // 4 resident backward blocks must fit the 196 KB shared-memory carve-out (1 KB
 // reserved per block): a larger carve-out halves L1 and costs ~6% (measured)
 static_assert(kSmemBwd <= 48 * 1024 + 128, "backward block exceeds the 196 KB carve-out budget");
