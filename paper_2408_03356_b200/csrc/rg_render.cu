@@ -47,11 +47,13 @@ constexpr int kRet = kA + 32;          // retired (expired, not yet scattered) s
 constexpr int kSlots = kA + 64;
 static_assert(kA == 64, "expire/n_in handle two 32-slot chunks");
 #ifndef RG_STK_FWD
-#define RG_STK_FWD 512
+#define RG_STK_FWD 320
 #endif
-// traversal stack entries (wide nodes; max depth seen: C1 ~60, C3 170): the forward
-// has shared memory to spare; the backward traverses only for rays whose fetch log
-// overflowed and must stay within its 48 KB block budget
+// traversal stack entries (wide nodes; max depth seen: C1 ~60, C3 170; an overflow
+// drops subtrees and is counted in rg_stats.stack_overflows, asserted 0 by the
+// tests): the forward affords 320 (512 costs ~1% through the smaller L1); the
+// backward traverses only for rays whose fetch log overflowed and must stay within
+// its 48 KB block budget
 constexpr int kStkFwd = RG_STK_FWD;
 constexpr int kStkBwd = 216;
 constexpr unsigned kFull = 0xffffffffu;

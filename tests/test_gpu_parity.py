@@ -229,8 +229,10 @@ def test_forward_full_size_sampled(oracle, name):
     wl = synth.workload(name)
     sc, cam, p = wl.scene, wl.cameras[0], wl.params
     g, b = gpu_build(sc, p)
-    full = rg.render_forward(g, b, rg.Config.of(p), camera=cam)
+    st = rg.new_stats()
+    full = rg.render_forward(g, b, rg.Config.of(p), camera=cam, stats=st)
     torch.cuda.synchronize()
+    assert rg.stats_dict(st)["stack_overflows"] == 0
     W = cam.width
     ys, xs = np.meshgrid(np.arange(8, cam.height, 16), np.arange(8, cam.width, 16), indexing="ij")
     idx = (ys * W + xs).reshape(-1)
@@ -367,6 +369,7 @@ def test_fwd_bwd_sampled_large_configs(oracle, name, n_rays):
             assert np.array_equal(rg_["debug_records"][r, :n], ref["dump"][r]), r
     if name == "stress":
         assert ref["counters"]["overflows"] > 0
+    assert rg_["stats"]["stack_overflows"] == 0
     cfg = rg.Config.of(p)
     to, td = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
     fwd = rg.render_forward(g, b, cfg, rays=(to, td), log=rg.new_log(len(o)))
