@@ -451,9 +451,9 @@ def run_ours(args):
         from oracle import oracle as O
         O.build()
         tgt_np = tgt.cpu().numpy().astype(np.float64)
-        n, s = oracle_step(sc, p, cam, tgt_np, 6)
+        n, s = oracle_step(sc, p, cam, tgt_np, 4)
         line["cpu_baseline"] = {"value": n / s / 1e6, "unit": "Mrays/s", "cores": 1, "kind": "oracle",
-                                "sample": f"{n} stratified rays (every 6th pixel) of the 800x800 view: "
+                                "sample": f"{n} stratified rays (every 4th pixel) of the 800x800 view: "
                                           f"oracle BVH build + fwd + L1 grad + bwd, {s:.1f} s",
                                 "cpu": cpu_model(), "nproc": os.cpu_count()}
     print(json.dumps(line), flush=True)
