@@ -76,6 +76,9 @@ def lib():
         _lib.og_camera_rays.argtypes = [C.c_int32, C.c_int32, C.c_float, C.c_float, C.c_float,
                                         C.c_float, P, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_int32, P, P]
+        _lib.og_camera_rays_spp.argtypes = [C.c_int32, C.c_int32, C.c_float, C.c_float, C.c_float,
+                                            C.c_float, P, C.c_int32, C.c_int32, C.c_int32,
+                                            C.c_int32, C.c_int32, P, P]
         _lib.og_clip.restype = C.c_int32
         _lib.og_clip.argtypes = [P, P, P, C.c_float, P, P]
         _lib.og_color.argtypes = [P, C.c_int32, P, P]
@@ -150,6 +153,17 @@ def camera_rays(cam):
     c2w = np.ascontiguousarray(cam.c2w, np.float32)
     lib().og_camera_rays(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, _p(c2w),
                          x0, y0, x1, y1, _p(o), _p(d))
+    return o, d
+
+
+def camera_rays_spp(cam, spp):
+    """RayGauss4x rays: spp per pixel, pixel-major (og_camera_rays_spp)"""
+    x0, y0, x1, y1 = cam.x0y0x1y1
+    n = (x1 - x0) * (y1 - y0) * spp
+    o = np.zeros((n, 3), np.float32); d = np.zeros((n, 3), np.float32)
+    c2w = np.ascontiguousarray(cam.c2w, np.float32)
+    lib().og_camera_rays_spp(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, _p(c2w),
+                             x0, y0, x1, y1, spp, _p(o), _p(d))
     return o, d
 
 

@@ -312,6 +312,29 @@ void og_camera_rays(int32_t width, int32_t height, float fx, float fy, float cx,
     }
 }
 
+void og_camera_rays_spp(int32_t width, int32_t height, float fx, float fy, float cx, float cy,
+                        const float* c2w, int32_t x0, int32_t y0, int32_t x1, int32_t y1,
+                        int32_t spp, float* o, float* d) {
+  (void)width; (void)height;
+  const int w = x1 - x0;
+  for (int py = y0; py < y1; ++py)
+    for (int px = x0; px < x1; ++px)
+      for (int s = 0; s < spp; ++s) {
+        const size_t r = ((size_t)(py - y0) * w + (px - x0)) * (size_t)spp + (size_t)s;
+        const float ox = spp == 1 ? 0.5f : 0.25f + 0.5f * (float)(s & 1);
+        const float oy = spp == 1 ? 0.5f : 0.25f + 0.5f * (float)(s >> 1);
+        const float xc = (((float)px + ox) - cx) / fx;
+        const float yc = (((float)py + oy) - cy) / fy;
+        float dw[3];
+        for (int a = 0; a < 3; ++a) dw[a] = (c2w[4 * a + 0] * xc + c2w[4 * a + 1] * yc) + c2w[4 * a + 2];
+        const float nrm = sqrtf((dw[0] * dw[0] + dw[1] * dw[1]) + dw[2] * dw[2]);
+        for (int a = 0; a < 3; ++a) {
+          d[3 * r + a] = dw[a] / nrm;
+          o[3 * r + a] = c2w[4 * a + 3];
+        }
+      }
+}
+
 /* ------------------------------------------------------------------------ */
 /* ARITH-8  IntersectBBox (Alg. 2 line 2), t0 clipped at t_near (L13)  */
 /* ------------------------------------------------------------------------ */

@@ -83,6 +83,12 @@ void og_refit(int32_t n, const int32_t* left, const int32_t* right,
 void og_camera_rays(int32_t width, int32_t height, float fx, float fy, float cx, float cy,
                     const float* c2w, int32_t x0, int32_t y0, int32_t x1, int32_t y1,
                     float* o, float* d);
+/* RayGauss4x (L29): spp rays per pixel, spp = 1 (the centre,
+   identical to og_camera_rays) or 4 (2x2 grid at offsets 1/4, 3/4 of the pixel);
+   ray index = pixel index * spp + s, s = sx + 2 sy */
+void og_camera_rays_spp(int32_t width, int32_t height, float fx, float fy, float cx, float cy,
+                        const float* c2w, int32_t x0, int32_t y0, int32_t x1, int32_t y1,
+                        int32_t spp, float* o, float* d);
 /* scene-bbox clip (ARITH-8): returns 1 if t0 < t1 */
 int32_t og_clip(const float box[6], const float o[3], const float d[3], float t_near,
                 float* t0, float* t1);

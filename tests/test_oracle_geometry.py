@@ -292,6 +292,27 @@ def test_camera_rays(oracle):
     assert np.array_equal(d3.reshape(12, 20, 3), d.reshape(48, 64, 3)[5:17, 10:30])
 
 
+def test_camera_rays_4x(oracle):
+    """RayGauss4x rays: spp = 1 is the centre ray bit for bit; for
+    the principal-point pixel the 4 subrays are mirror images about the forward
+    axis, each at angle atan(0.25 sqrt(2) / f) from it (square pixels), and the
+    rays of pixel p are 4p .. 4p+3"""
+    cam = synth.orbit_camera(3.0, 30, 20, 16, 12, 50.0)
+    o1, d1 = oracle.camera_rays(cam)
+    o, d = oracle.camera_rays_spp(cam, 1)
+    assert np.array_equal(d, d1) and np.array_equal(o, o1)
+    c2 = synth.Camera(17, 13, 40.0, 40.0, 8.5, 6.5, cam.c2w)          # pixel (8, 6) centred
+    o4, d4 = oracle.camera_rays_spp(c2, 4)
+    assert d4.shape == (17 * 13 * 4, 3)
+    sub = d4.reshape(13, 17, 4, 3)[6, 8].astype(np.float64)
+    fwd, right, down = cam.c2w[:, 2], cam.c2w[:, 0], cam.c2w[:, 1]
+    ang = np.arctan2(np.linalg.norm(np.cross(sub, fwd), axis=1), sub @ fwd)
+    assert np.allclose(ang, np.arctan(0.25 * np.sqrt(2) / 40.0), rtol=1e-4)
+    sx = np.sign(sub @ right); sy = np.sign(sub @ down)
+    assert list(sx) == [-1, 1, -1, 1] and list(sy) == [-1, -1, 1, 1]   # s = sx + 2 sy
+    assert np.allclose(sub.sum(0) / np.linalg.norm(sub.sum(0)), fwd, atol=1e-6)
+
+
 def test_bbox_clip(oracle):
     ex = GOLD["bbox"][0]
     hit, t0, t1 = oracle.clip(ex["box"], ex["o"], ex["d"])
