@@ -91,6 +91,11 @@ typedef struct {
   int32_t width, height, x0, y0, x1, y1;
   float fx, fy, cx, cy;
   float c2w[12];
+  int32_t spp;           /* rays per pixel: 1 (the pixel centre) or 4 (RayGauss4x, P:775:
+                            a 2x2 grid at offsets 1/4, 3/4; L29).  Rays are
+                            numbered pixel * spp + (sx + 2 sy); rg_supersample_resolve /
+                            rg_supersample_spread map between rays and pixels. */
+  int32_t pad_;
 } rg_camera;
 
 /* BVH handle filled by rg_build_bvh: device pointers into the caller's
@@ -256,6 +261,15 @@ size_t rg_dssim_workspace_bytes(int32_t width, int32_t height);
 rg_status rg_l1_dssim_loss_grad(const float* rgb, const float* target, int32_t width,
                                 int32_t height, float lambda, float* d_rgb, float* loss, void* ws,
                                 size_t ws_bytes, void* stream);
+
+/* RayGauss4x pixel <-> ray maps for spp rays per pixel (device, [n_pixels*spp,3]
+   rays, [n_pixels,3] pixels): resolve writes rgb_px = mean of the pixel's spp ray
+   colours (box filter); spread writes d_rays = d_px / spp (its adjoint).  Errors:
+   RG_ERR_INVALID_ARG for NULL pointers with n_pixels > 0, spp < 1. */
+rg_status rg_supersample_resolve(const float* rgb_rays, int64_t n_pixels, int32_t spp,
+                                 float* rgb_px, void* stream);
+rg_status rg_supersample_spread(const float* d_px, int64_t n_pixels, int32_t spp, float* d_rays,
+                                void* stream);
 
 /* ---- loss helper (for benchmarks; loss itself is outside the paper's path) -- */
 /* L1 loss: loss += scale * sum |rgb - target|, d_rgb = scale * sign(rgb - target)

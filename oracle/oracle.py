@@ -147,6 +147,8 @@ def clip(box, o, d, t_near=0.0):
 
 
 def camera_rays(cam):
+    if getattr(cam, "spp", 1) != 1:
+        return camera_rays_spp(cam, cam.spp)
     x0, y0, x1, y1 = cam.x0y0x1y1
     n = (x1 - x0) * (y1 - y0)
     o = np.zeros((n, 3), np.float32); d = np.zeros((n, 3), np.float32)

@@ -52,6 +52,7 @@ bool rays_ok(const rg_rays* r, const rg_camera* cam) {
   if (r) return r->n >= 0 && (r->n == 0 || (r->origin && r->dir));
   if (cam->x0 < 0 || cam->y0 < 0 || cam->x1 < cam->x0 || cam->y1 < cam->y0) return false;
   if (!(cam->fx != 0.0f) || !(cam->fy != 0.0f)) return false;
+  if (cam->spp != 1 && cam->spp != 4) return false;
   return true;
 }
 
@@ -177,6 +178,22 @@ rg_status rg_l1_dssim_loss_grad(const float* rgb, const float* target, int32_t w
   const cudaError_t e = launch_l1_dssim(rgb, target, height, width, lambda, d_rgb, loss,
                                         static_cast<float*>(ws), static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? RG_OK : RG_ERR_CUDA;
+}
+
+rg_status rg_supersample_resolve(const float* rgb_rays, int64_t n_pixels, int32_t spp,
+                                 float* rgb_px, void* stream) {
+  if (n_pixels < 0 || spp < 1 || (n_pixels > 0 && (!rgb_rays || !rgb_px))) return RG_ERR_INVALID_ARG;
+  cudaGetLastError();
+  return launch_ss_resolve(rgb_rays, n_pixels, spp, rgb_px, static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess ? RG_OK : RG_ERR_CUDA;
+}
+
+rg_status rg_supersample_spread(const float* d_px, int64_t n_pixels, int32_t spp, float* d_rays,
+                                void* stream) {
+  if (n_pixels < 0 || spp < 1 || (n_pixels > 0 && (!d_px || !d_rays))) return RG_ERR_INVALID_ARG;
+  cudaGetLastError();
+  return launch_ss_spread(d_px, n_pixels, spp, d_rays, static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess ? RG_OK : RG_ERR_CUDA;
 }
 
 rg_status rg_camera_rays(const rg_camera* cam, float* origin, float* dir, void* stream) {

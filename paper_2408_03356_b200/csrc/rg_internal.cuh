@@ -187,10 +187,14 @@ __device__ __forceinline__ bool clip_exact(const float* box, const float3& o, co
 }
 
 // ARITH-7: pinhole ray through pixel centre
-__device__ __forceinline__ void camera_ray(const rg_camera& cam, int px, int py, float3& o,
-                                           float3& d) {
-  const float xc = div_(sub_(add_((float)px, 0.5f), cam.cx), cam.fx);
-  const float yc = div_(sub_(add_((float)py, 0.5f), cam.cy), cam.fy);
+// subsample s of a pixel: the centre for spp = 1, the 2x2 grid at 1/4, 3/4 for spp = 4
+__device__ __forceinline__ float sub_off(int spp, int s_axis) {
+  return spp == 1 ? 0.5f : 0.25f + 0.5f * (float)s_axis;
+}
+__device__ __forceinline__ void camera_ray(const rg_camera& cam, int px, int py, float ox, float oy,
+                                           float3& o, float3& d) {
+  const float xc = div_(sub_(add_((float)px, ox), cam.cx), cam.fx);
+  const float yc = div_(sub_(add_((float)py, oy), cam.cy), cam.fy);
   const float* M = cam.c2w;
   const float dw0 = add_(add_(mul_(M[0], xc), mul_(M[1], yc)), M[2]);
   const float dw1 = add_(add_(mul_(M[4], xc), mul_(M[5], yc)), M[6]);
@@ -259,6 +263,8 @@ cudaError_t launch_adam(const rg_adam_config& c, const rg_gaussian_grads& g,
 size_t dssim_workspace_bytes(int H, int W);
 cudaError_t launch_l1_dssim(const float* x, const float* y, int H, int W, float lam, float* d,
                             float* loss, float* ws, cudaStream_t st);
+cudaError_t launch_ss_resolve(const float* r, int64_t n, int spp, float* px, cudaStream_t st);
+cudaError_t launch_ss_spread(const float* dpx, int64_t n, int spp, float* dr, cudaStream_t st);
 cudaError_t launch_camera_rays(const rg_camera& cam, float* o, float* d, cudaStream_t st);
 cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,
                            const rg_rays* rays, const rg_camera* cam, float* rgb, float* T,

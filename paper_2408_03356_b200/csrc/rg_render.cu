@@ -40,6 +40,7 @@ namespace {
 #define RG_MIN_BLOCKS_FWD RG_MIN_BLOCKS   // forward (no WarpAcc: smem allows more blocks)
 #endif
 constexpr int kWarps = 4;              // rays (warps) per block
+static_assert(kWarps == 4, "camera mode: a block is a 2x2 pixel tile, or one pixel's 4 subsamples");
 constexpr int kBlock = 32 * kWarps;
 constexpr int kA = 64;                 // persistent active-list capacity
 constexpr int kTrans = kA;             // transient chunk slots (slab sets > kA)
@@ -709,11 +710,18 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
   Ray R;
   if (P.cam_mode) {
     const int tile = blockIdx.x;
-    const int px = 2 * (tile % P.tiles_x) + (wid & 1);
-    const int py = 2 * (tile / P.tiles_x) + (wid >> 1);
-    if (px >= P.rw || py >= P.rh) return;
-    ray = py * P.rw + px;
-    camera_ray(P.cam, P.cam.x0 + px, P.cam.y0 + py, R.o, R.d);
+    if (P.cam.spp == 1) {         // block = 2x2 pixel tile, warp = pixel
+      const int px = 2 * (tile % P.tiles_x) + (wid & 1);
+      const int py = 2 * (tile / P.tiles_x) + (wid >> 1);
+      if (px >= P.rw || py >= P.rh) return;
+      ray = py * P.rw + px;
+      camera_ray(P.cam, P.cam.x0 + px, P.cam.y0 + py, 0.5f, 0.5f, R.o, R.d);
+    } else {                      // RayGauss4x: block = pixel, warp = one of its 4 subsamples
+      const int px = tile % P.rw, py = tile / P.rw;
+      ray = tile * 4 + wid;
+      camera_ray(P.cam, P.cam.x0 + px, P.cam.y0 + py, sub_off(4, wid & 1), sub_off(4, wid >> 1),
+                 R.o, R.d);
+    }
   } else {
     ray = blockIdx.x * kWarps + wid;
     if (ray >= P.n_rays) return;
@@ -1309,9 +1317,11 @@ __global__ void __launch_bounds__(256) k_finalize_app(const float* gbuf, int gst
 __global__ void k_camera_rays(const rg_camera cam, float* o, float* d) {
   const int rw = cam.x1 - cam.x0, rh = cam.y1 - cam.y0;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rw * rh) return;
+  if (r >= rw * rh * cam.spp) return;
+  const int pix = r / cam.spp, s = r - pix * cam.spp;
   float3 oo, dd;
-  camera_ray(cam, cam.x0 + r % rw, cam.y0 + r / rw, oo, dd);
+  camera_ray(cam, cam.x0 + pix % rw, cam.y0 + pix / rw, sub_off(cam.spp, s & 1),
+             sub_off(cam.spp, s >> 1), oo, dd);
   o[3 * r] = oo.x; o[3 * r + 1] = oo.y; o[3 * r + 2] = oo.z;
   d[3 * r] = dd.x; d[3 * r + 1] = dd.y; d[3 * r + 2] = dd.z;
 }
@@ -1349,9 +1359,10 @@ void ray_grid(RenderArgs& A, const rg_rays* rays, const rg_camera* cam, dim3& gr
     A.cam = *cam;
     A.rw = cam->x1 - cam->x0;
     A.rh = cam->y1 - cam->y0;
-    A.n_rays = A.rw * A.rh;
+    A.n_rays = A.rw * A.rh * cam->spp;
     A.tiles_x = (A.rw + 1) / 2;
-    grid = dim3((unsigned)(A.tiles_x * ((A.rh + 1) / 2)));
+    grid = cam->spp == 1 ? dim3((unsigned)(A.tiles_x * ((A.rh + 1) / 2)))
+                         : dim3((unsigned)(A.rw * A.rh));     // spp = 4: one block per pixel
   } else {
     A.cam_mode = 0;
     A.ro = rays->origin;
@@ -1413,7 +1424,7 @@ void set_log(RenderArgs& A, const void* log, size_t log_bytes, int n_rays) {
 }  // namespace
 
 cudaError_t launch_camera_rays(const rg_camera& cam, float* o, float* d, cudaStream_t st) {
-  const int n = (cam.x1 - cam.x0) * (cam.y1 - cam.y0);
+  const int n = (cam.x1 - cam.x0) * (cam.y1 - cam.y0) * cam.spp;
   if (n > 0) { k_camera_rays<<<(n + 255) / 256, 256, 0, st>>>(cam, o, d); count_launches(1); }
   return cudaGetLastError();
 }

@@ -318,4 +318,38 @@ cudaError_t launch_l1_dssim(const float* x, const float* y, int H, int W, float 
   return cudaGetLastError();
 }
 
+// RayGauss4x pixel <-> ray maps: resolve = box-filter mean of a pixel's spp
+// rays, spread = its adjoint (d_ray = d_px / spp)
+namespace {
+__global__ void k_ss_resolve(const float* r, int64_t n, int spp, float* px) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;   // (pixel, channel)
+  if (i >= 3 * n) return;
+  const int64_t p = i / 3, c = i - 3 * p;
+  float s = 0.f;
+  for (int k = 0; k < spp; ++k) s += r[3 * (p * spp + k) + c];
+  px[i] = s / (float)spp;
+}
+__global__ void k_ss_spread(const float* dpx, int64_t n, int spp, float* dr) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;   // (ray, channel)
+  if (i >= 3 * n * spp) return;
+  const int64_t ray = i / 3, c = i - 3 * ray;
+  dr[i] = dpx[3 * (ray / spp) + c] / (float)spp;
+}
+}  // namespace
+
+cudaError_t launch_ss_resolve(const float* r, int64_t n, int spp, float* px, cudaStream_t st) {
+  if (n > 0) {
+    k_ss_resolve<<<(unsigned)((3 * n + 255) / 256), 256, 0, st>>>(r, n, spp, px);
+    count_launches(1);
+  }
+  return cudaGetLastError();
+}
+cudaError_t launch_ss_spread(const float* dpx, int64_t n, int spp, float* dr, cudaStream_t st) {
+  if (n > 0) {
+    k_ss_spread<<<(unsigned)((3 * n * spp + 255) / 256), 256, 0, st>>>(dpx, n, spp, dr);
+    count_launches(1);
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace rg

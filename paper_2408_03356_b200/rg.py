@@ -59,7 +59,8 @@ class _Rays(C.Structure):
 class _Camera(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("x0", C.c_int32), ("y0", C.c_int32),
                 ("x1", C.c_int32), ("y1", C.c_int32), ("fx", C.c_float), ("fy", C.c_float),
-                ("cx", C.c_float), ("cy", C.c_float), ("c2w", C.c_float * 12)]
+                ("cx", C.c_float), ("cy", C.c_float), ("c2w", C.c_float * 12),
+                ("spp", C.c_int32), ("pad_", C.c_int32)]
 
 
 class _BVH(C.Structure):
@@ -72,6 +73,7 @@ class _BVH(C.Structure):
 
 EXPORTS = ("rg_status_string", "rg_version", "rg_kernel_launches", "rg_bvh_workspace_bytes", "rg_build_bvh",
            "rg_refit_bvh", "rg_adam_step", "rg_dssim_workspace_bytes", "rg_l1_dssim_loss_grad",
+           "rg_supersample_resolve", "rg_supersample_spread",
            "rg_camera_rays", "rg_render_forward", "rg_backward_workspace_bytes",
            "rg_render_backward", "rg_l1_loss_grad", "rg_fetch_log_bytes")
 
@@ -111,6 +113,10 @@ def lib(load_only: bool = False):
     L.rg_dssim_workspace_bytes.argtypes = [I32, I32]
     L.rg_l1_dssim_loss_grad.restype = C.c_int
     L.rg_l1_dssim_loss_grad.argtypes = [P, P, I32, I32, C.c_float, P, P, P, SZ, P]
+    L.rg_supersample_resolve.restype = C.c_int
+    L.rg_supersample_resolve.argtypes = [P, C.c_int64, I32, P, P]
+    L.rg_supersample_spread.restype = C.c_int
+    L.rg_supersample_spread.argtypes = [P, C.c_int64, I32, P, P]
     L.rg_camera_rays.restype = C.c_int
     L.rg_camera_rays.argtypes = [P, P, P, P]
     L.rg_render_forward.restype = C.c_int
@@ -299,6 +305,7 @@ def camera_struct(cam) -> _Camera:
     flat = [float(v) for v in cam.c2w.reshape(-1)]
     for i in range(12):
         s.c2w[i] = flat[i]
+    s.spp = int(getattr(cam, "spp", 1))
     return s
 
 
@@ -494,3 +501,23 @@ def l1_dssim_loss_grad(rgb, target, width: int, height: int, lam: float = 0.2, d
                                    _ptr(loss), _ptr(ws), ws.numel() * 4, _stream()),
            "rg_l1_dssim_loss_grad")
     return d_rgb, loss
+
+
+def supersample_resolve(rgb_rays, spp: int, out=None):
+    """RayGauss4x: [n_px*spp, 3] ray colours -> [n_px, 3] pixels (box-filter mean)"""
+    _require_cuda()
+    n = rgb_rays.shape[0] // spp
+    out = torch.empty(n, 3, dtype=torch.float32, device=rgb_rays.device) if out is None else out
+    _check(lib().rg_supersample_resolve(_ptr(rgb_rays.contiguous()), n, spp, _ptr(out), _stream()),
+           "rg_supersample_resolve")
+    return out
+
+
+def supersample_spread(d_px, spp: int, out=None):
+    """adjoint of supersample_resolve: d_rays = d_px / spp per subsample"""
+    _require_cuda()
+    n = d_px.shape[0]
+    out = torch.empty(n * spp, 3, dtype=torch.float32, device=d_px.device) if out is None else out
+    _check(lib().rg_supersample_spread(_ptr(d_px.contiguous()), n, spp, _ptr(out), _stream()),
+           "rg_supersample_spread")
+    return out

@@ -69,6 +69,7 @@ class Camera:
     cy: float
     c2w: np.ndarray                 # [3,4] f32
     rect: tuple | None = None       # (x0, y0, x1, y1) pixel rectangle, default full
+    spp: int = 1                    # rays per pixel: 1, or 4 (RayGauss4x)
 
     @property
     def x0y0x1y1(self):
@@ -77,7 +78,7 @@ class Camera:
     @property
     def n_rays(self) -> int:
         x0, y0, x1, y1 = self.x0y0x1y1
-        return (x1 - x0) * (y1 - y0)
+        return (x1 - x0) * (y1 - y0) * self.spp
 
 
 @dataclass

@@ -66,7 +66,7 @@ def test_struct_sizes_match_header():
     from paper_2408_03356_b200 import rg
     assert C.sizeof(rg._Gaussians) == 16 + 8 * 8
     assert C.sizeof(rg._Config) == 48
-    assert C.sizeof(rg._Camera) == 24 + 16 + 48
+    assert C.sizeof(rg._Camera) == 24 + 16 + 48 + 8
     assert C.sizeof(rg._BVH) == 16 + 10 * 8
 
 
