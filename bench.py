@@ -376,6 +376,23 @@ def run_ours(args):
         rg.render_backward(ga, bv, cfg, f_, ssim_d, camera=cam, grads=gb.views, ws=gws)
         opt.step(gb.views, it=0)
     iter_ms = timed(full_iteration)
+    # NEXT-2: RayGauss4x (P:775, 4 rays per pixel) and uncorrelated ray batches
+    # mixing the 8 training views, forward only, BVH built once
+    import dataclasses
+    bvh = rg.build_bvh(g, cfg, ws=bws)
+    cam4 = dataclasses.replace(cam, spp=4)
+    fo4 = dict(rgb=torch.empty(4 * R, 3, device=dev), T=torch.empty(4 * R, device=dev),
+               replay=torch.empty(4 * R, dtype=torch.int32, device=dev))
+    fwd4_ms = timed(lambda: rg.render_forward(g, bvh, cfg, camera=cam4, out=fo4))
+    mix_o, mix_d = [], []
+    for c in wl.cameras:
+        o_, d_ = rg.camera_rays(c, device=dev)
+        mix_o.append(o_); mix_d.append(d_)
+    perm = torch.randperm(len(wl.cameras) * R, device=dev,
+                          generator=torch.Generator(device=dev).manual_seed(7))[:R]
+    mo, md = torch.cat(mix_o)[perm].contiguous(), torch.cat(mix_d)[perm].contiguous()
+    del mix_o, mix_d
+    mix_ms = timed(lambda: rg.render_forward(g, bvh, cfg, rays=(mo, md), out=fo))
     next_rows = {
         "alg3_iteration_ms": iter_ms,
         "refit_bvh_ms": refit_ms,
@@ -383,6 +400,11 @@ def run_ours(args):
                  "achieved_gbs": adam_bytes / (adam_ms * 1e-3) / 1e9, "peak_gbs": hbm,
                  "frac": adam_bytes / (adam_ms * 1e-3) / 1e9 / hbm, "bound": "hbm"},
         "l1_dssim_ms": ssim_ms,
+        "raygauss4x": {"fwd_ms": fwd4_ms, "rays": 4 * R, "cost_vs_1x": fwd4_ms / fwd_ms,
+                       "paper": "about 3x (P:775)"},
+        "uncorrelated_rays": {"fwd_ms": mix_ms, "rays": R,
+                              "mrays_s": R / (mix_ms * 1e-3) / 1e6,
+                              "what": "random sample of the rays of the 8 training views, shuffled"},
     }
     # ---- end to end through the public API with host buffers
     for _ in range(args.warmup):

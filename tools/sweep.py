@@ -1,0 +1,57 @@
+"""Delta-t and sigma_eps sweeps of the forward: the
+throughput TRENDS of the paper's Tables 5-6 on the synthetic C1
+view, with the paper's RTX 4090 FPS beside them (context, different scene).
+
+usage: python tools/sweep.py [out.json]"""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2408_03356_b200 import rg, synth  # noqa: E402
+
+PAPER_DT = {1.25e-4: 17.4, 2.5e-4: 25.8, 5e-4: 42.8, 1e-3: 54.7}      # Table 5, FPS 800x800
+PAPER_SE = {1.0: 29.4, 0.1: 25.8, 0.01: 23.5}                          # Table 6
+
+
+def fwd_ms(g, cfg, cam, reps=5):
+    b = rg.build_bvh(g, cfg)
+    for _ in range(2):
+        rg.render_forward(g, b, cfg, camera=cam)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        rg.render_forward(g, b, cfg, camera=cam)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def main():
+    wl = synth.workload("blender")
+    sc, cam, p = wl.scene, wl.cameras[0], wl.params
+    g = rg.Gaussians.from_scene(sc)
+    rows = {"dt": [], "sigma_eps": []}
+    for dt, fps in PAPER_DT.items():
+        cfg = rg.Config.of(p)
+        cfg.dt = dt
+        ms = fwd_ms(g, cfg, cam)
+        rows["dt"].append({"dt": dt, "fwd_ms": ms, "fps": 1e3 / ms, "paper_fps_rtx4090": fps})
+    for se, fps in PAPER_SE.items():
+        cfg = rg.Config.of(p)
+        cfg.sigma_eps = se
+        ms = fwd_ms(g, cfg, cam)
+        rows["sigma_eps"].append({"sigma_eps": se, "fwd_ms": ms, "fps": 1e3 / ms,
+                                  "paper_fps_rtx4090": fps})
+    out = {"workload": "C1 800x800 view, 300k Gaussians SH3+7SG (synthetic)", **rows}
+    txt = json.dumps(out, indent=1)
+    print(txt)
+    if len(sys.argv) > 1:
+        open(sys.argv[1], "w").write(txt)
+
+
+if __name__ == "__main__":
+    main()
