@@ -182,3 +182,82 @@ def l1_dssim_loss_grad(rgb, target, lam=LAMBDA_DSSIM):
     loss = (1.0 - lam) * l1 + lam * (1.0 - torch.mean(ssim_map(x, y)))
     loss.backward()
     return float(loss.detach()), x.grad.numpy()
+
+
+# ---------------------------------------------------------------------------
+# adaptive density control (Alg. 3): the 3D Gaussian
+# Splatting heuristic the paper follows, with the mean-gradient criterion
+# grad_mu > grad_eps and pruning of sigma~ < sigma_eps.  Readings L30-L32:
+#   * statistic: per Gaussian, the mean over iterations of ||dL/dmu|| (fp32
+#     accumulation acc += ||g||, cnt += (||g|| > 0), average acc / cnt);
+#   * densify if avg >= grad_eps (cnt > 0): CLONE (copy) when
+#     max(scale) <= percent_dense * extent, else SPLIT into 2 children at
+#     mu + R(q) (s * z_k), z_k ~ N(0, I) (passed in), scale s / 1.6, other
+#     parameters copied, parent removed; PRUNE sigma~ < sigma_eps (a pruned
+#     Gaussian is neither cloned nor split);
+#   * output order: surviving originals (index order), then clones (index
+#     order), then split children (parent index order, child 0 then 1).
+# Decisions are taken in fp32 (the kernel's precision); the split positions and
+# scales are computed in fp64.
+# ---------------------------------------------------------------------------
+
+PERCENT_DENSE = 0.01
+SPLIT_N = 2
+SPLIT_SCALE = 1.6          # 0.8 * N
+
+
+def densify_accumulate(acc, cnt, grad_mean):
+    """acc += ||g|| (fp32), cnt += (||g|| > 0) for one iteration's dL/dmu [n,3]"""
+    g = np.asarray(grad_mean, np.float32)
+    nrm = np.sqrt((g[:, 0] * g[:, 0] + g[:, 1] * g[:, 1]) + g[:, 2] * g[:, 2]).astype(np.float32)
+    return (np.asarray(acc, np.float32) + nrm).astype(np.float32), \
+        np.asarray(cnt, np.int32) + (nrm > 0).astype(np.int32)
+
+
+def densify_plan(scene_act, acc, cnt, grad_eps, extent, sigma_eps, percent_dense=PERCENT_DENSE):
+    """per Gaussian action: 0 keep, 1 clone, 2 split, 3 prune (fp32 decisions)"""
+    acc = np.asarray(acc, np.float32); cnt = np.asarray(cnt, np.int32)
+    avg = np.where(cnt > 0, acc / np.maximum(cnt, 1).astype(np.float32), np.float32(0)).astype(np.float32)
+    dens = avg >= np.float32(grad_eps)
+    smax = np.max(np.asarray(scene_act["scale"], np.float32), axis=1)
+    small = smax <= np.float32(np.float32(percent_dense) * np.float32(extent))
+    prune = np.asarray(scene_act["density"], np.float32) < np.float32(sigma_eps)
+    act = np.zeros(len(acc), np.int32)
+    act[dens & small] = 1
+    act[dens & ~small] = 2
+    act[prune] = 3
+    return act
+
+
+def rotation64(q):
+    """R(q) of unit-normalised (w,x,y,z) quaternions, fp64 (Hamilton)"""
+    q = np.asarray(q, np.float64)
+    q = q / np.linalg.norm(q, axis=1, keepdims=True)
+    w, x, y, z = q[:, 0], q[:, 1], q[:, 2], q[:, 3]
+    R = np.empty((len(q), 3, 3))
+    R[:, 0, 0] = 1 - 2 * (y * y + z * z); R[:, 0, 1] = 2 * (x * y - w * z); R[:, 0, 2] = 2 * (x * z + w * y)
+    R[:, 1, 0] = 2 * (x * y + w * z); R[:, 1, 1] = 1 - 2 * (x * x + z * z); R[:, 1, 2] = 2 * (y * z - w * x)
+    R[:, 2, 0] = 2 * (x * z - w * y); R[:, 2, 1] = 2 * (y * z + w * x); R[:, 2, 2] = 1 - 2 * (x * x + y * y)
+    return R
+
+
+def densify_apply(scene_act, action, z):
+    """new activated parameter arrays (dict) in the output order above;
+    z [n, 2, 3] standard normal draws (only split rows are used)"""
+    action = np.asarray(action)
+    keep = np.nonzero((action == 0) | (action == 1))[0]
+    clone = np.nonzero(action == 1)[0]
+    split = np.nonzero(action == 2)[0]
+    src = np.concatenate([keep, clone, np.repeat(split, SPLIT_N)]).astype(np.int64)
+    out = {k: np.asarray(v)[src].astype(np.float64) for k, v in scene_act.items()}
+    ns = len(split)
+    if ns:
+        mu = np.asarray(scene_act["mean"], np.float64)[split]
+        s = np.asarray(scene_act["scale"], np.float64)[split]
+        R = rotation64(np.asarray(scene_act["quat"])[split])
+        zz = np.asarray(z, np.float64)[split]                       # [ns, 2, 3]
+        child_mu = mu[:, None, :] + np.einsum("nab,nkb->nka", R, s[:, None, :] * zz)
+        base = len(keep) + len(clone)
+        out["mean"][base:] = child_mu.reshape(-1, 3)
+        out["scale"][base:] = np.repeat(s / SPLIT_SCALE, SPLIT_N, axis=0)
+    return out, src

@@ -220,3 +220,70 @@ def test_l1_dssim_gradient_finite_differences():
     l0, g0 = T.l1_dssim_loss_grad(x, y, lam=0.0)
     assert l0 == pytest.approx(np.mean(np.abs(x - y)), rel=1e-12)
     assert np.allclose(g0, np.sign(x - y) / x.size, rtol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# adaptive density control oracle
+# ---------------------------------------------------------------------------
+
+def _act_scene(rng, n):
+    q = rng.normal(size=(n, 4))
+    return dict(mean=rng.normal(size=(n, 3)).astype(np.float32),
+                quat=(q / np.linalg.norm(q, axis=1, keepdims=True)).astype(np.float32),
+                scale=np.exp(rng.normal(-4, 1, size=(n, 3))).astype(np.float32),
+                density=np.exp(rng.normal(0, 1.5, size=n)).astype(np.float32),
+                sh=rng.normal(size=(n, 4, 3)).astype(np.float32),
+                sg_amp=rng.normal(size=(n, 1, 3)).astype(np.float32),
+                sg_sharp=rng.uniform(1, 9, size=(n, 1)).astype(np.float32),
+                sg_axis=rng.normal(size=(n, 1, 3)).astype(np.float32))
+
+
+def test_densify_statistic_and_decisions():
+    acc = np.zeros(4, np.float32); cnt = np.zeros(4, np.int32)
+    acc, cnt = T.densify_accumulate(acc, cnt, [[3, 4, 0], [0, 0, 0], [1e-5, 0, 0], [0, 0, 1]])
+    acc, cnt = T.densify_accumulate(acc, cnt, [[0, 0, 0], [0, 0, 0], [3e-5, 0, 0], [0, 0, 1]])
+    assert list(acc) == [5.0, 0.0, np.float32(np.float32(1e-5) + np.float32(3e-5)), 2.0]
+    assert list(cnt) == [1, 0, 2, 2]                     # invisible iterations do not count
+    sc = dict(scale=np.array([[0.001] * 3, [0.5] * 3, [0.02, 0.001, 0.001], [0.05] * 3], np.float32),
+              density=np.array([1.0, 1.0, 1.0, 0.05], np.float32))
+    act = T.densify_plan(sc, acc, cnt, grad_eps=2e-5, extent=1.5, sigma_eps=0.1)
+    # avg 5 -> clone (0.001 <= 0.015); never seen -> keep; avg 2e-5 >= 2e-5 and
+    # max scale 0.02 > 0.015 -> split; low density -> prune (overrides densify)
+    assert list(act) == [1, 0, 2, 3]
+
+
+def test_densify_apply_order_and_split_geometry():
+    rng = np.random.default_rng(8)
+    sc = _act_scene(rng, 6)
+    action = np.array([0, 1, 2, 3, 1, 2])
+    z = rng.normal(size=(6, 2, 3))
+    out, src = T.densify_apply(sc, action, z)
+    assert list(src) == [0, 1, 4, 1, 4, 2, 2, 5, 5]      # survivors, clones, split children
+    assert out["mean"].shape == (9, 3)
+    for k in sc:                                          # clones are exact copies
+        assert np.array_equal(out[k][3], np.asarray(sc[k][1], np.float64))
+    # split children: mean + R diag(s) z, i.e. the child offset in the Gaussian's own
+    # frame is s * z (invert with R^T), scale / 1.6, everything else copied
+    for j, (p, k) in enumerate([(2, 0), (2, 1), (5, 0), (5, 1)]):
+        row = 5 + j
+        R = T.rotation64(sc["quat"][p:p + 1])[0]
+        local = R.T @ (out["mean"][row] - sc["mean"][p])
+        assert np.allclose(local, sc["scale"][p] * z[p, k], rtol=1e-9, atol=1e-12)
+        assert np.allclose(out["scale"][row], sc["scale"][p] / 1.6, rtol=1e-12)
+        assert np.array_equal(out["sh"][row], sc["sh"][p].astype(np.float64))
+    # the split offsets have the Gaussian's covariance: E[(x-mu)(x-mu)^T] = R S^2 R^T
+    zz = rng.normal(size=(1, 200000, 3))
+    sc1 = {k: v[2:3] for k, v in sc.items()}
+    R = T.rotation64(sc1["quat"])[0]
+    offs = np.einsum("ab,nb->na", R, sc1["scale"][0].astype(np.float64) * zz[0])
+    cov = offs.T @ offs / len(offs)
+    ref = R @ np.diag(sc1["scale"][0].astype(np.float64) ** 2) @ R.T
+    assert np.allclose(cov, ref, rtol=0.05, atol=0.02 * ref.max())
+
+
+def test_rotation64_closed_forms():
+    c = np.cos(np.pi / 4); s = np.sin(np.pi / 4)
+    R = T.rotation64(np.array([[c, 0, 0, s], [1, 0, 0, 0], [c, s, 0, 0]]))
+    assert np.allclose(R[0], [[0, -1, 0], [1, 0, 0], [0, 0, 1]], atol=1e-15)   # 90 deg about z
+    assert np.allclose(R[1], np.eye(3), atol=1e-15)
+    assert np.allclose(R[2], [[1, 0, 0], [0, 0, -1], [0, 1, 0]], atol=1e-15)   # 90 deg about x
