@@ -271,6 +271,33 @@ rg_status rg_supersample_resolve(const float* rgb_rays, int64_t n_pixels, int32_
 rg_status rg_supersample_spread(const float* d_px, int64_t n_pixels, int32_t spp, float* d_rays,
                                 void* stream);
 
+/* ---- adaptive density control (Alg. 3; L30-L32) -- */
+/* Statistic: acc[i] += ||grad_mean[i]||, cnt[i] += (||grad_mean[i]|| > 0) (device, fp32 /
+   int32, [n]); call once per iteration with the step's dL/dmu [n,3]. */
+rg_status rg_densify_accumulate(const float* grad_mean, int32_t n, float* acc, int32_t* cnt,
+                                void* stream);
+/* Workspace bytes of rg_densify_plan / _apply for n Gaussians. */
+size_t rg_densify_workspace_bytes(int32_t n);
+/* Decisions (fp32): avg = acc/cnt (0 if cnt = 0); PRUNE if density < sigma_eps; else
+   if avg >= grad_eps: CLONE if max(scale) <= percent_dense * extent, else SPLIT; else
+   KEEP.  Writes action[i] (0 keep, 1 clone, 2 split, 3 prune), the output order into
+   ws, and device counts[4] = {survivors (keep + clone originals), clones, splits,
+   n_out = survivors + clones + 2 splits}.  Output order: survivors (index order),
+   clones (index order), split children (parent order, child 0 then 1). */
+rg_status rg_densify_plan(const rg_gaussians* g, const float* acc, const int32_t* cnt,
+                          float grad_eps, float extent, float sigma_eps, float percent_dense,
+                          int32_t* action, void* ws, size_t ws_bytes, int32_t* counts,
+                          void* stream);
+/* Writes the n_out output rows of one array set (device, caller layouts, out sized
+   counts[3] rows).  mode 0: the activated parameters of `g` (in = NULL or g's
+   arrays): split children get mean + R(q) (scale * z_k) and scale / 1.6;
+   mode 1: raw optimiser parameters `in` (rg_adam_step's raw): split children get the
+   same child mean and raw scale - ln 1.6; mode 2: Adam moments `in`: new rows
+   (clones, children) are zero.  z: device [n, 2, 3] standard normal draws. */
+rg_status rg_densify_apply(const rg_gaussians* g, const rg_param_arrays* in,
+                           const int32_t* action, const void* ws, const int32_t* counts,
+                           const float* z, int32_t mode, const rg_param_arrays* out, void* stream);
+
 /* ---- loss helper (for benchmarks; loss itself is outside the paper's path) -- */
 /* L1 loss: loss += scale * sum |rgb - target|, d_rgb = scale * sign(rgb - target)
    over n_values floats (device; loss is one device float, accumulated). */

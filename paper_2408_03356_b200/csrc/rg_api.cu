@@ -196,6 +196,52 @@ rg_status rg_supersample_spread(const float* d_px, int64_t n_pixels, int32_t spp
                  cudaSuccess ? RG_OK : RG_ERR_CUDA;
 }
 
+rg_status rg_densify_accumulate(const float* grad_mean, int32_t n, float* acc, int32_t* cnt,
+                                void* stream) {
+  if (n < 0 || (n > 0 && (!grad_mean || !acc || !cnt))) return RG_ERR_INVALID_ARG;
+  cudaGetLastError();
+  return launch_dens_acc(grad_mean, n, acc, cnt, static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? RG_OK : RG_ERR_CUDA;
+}
+
+size_t rg_densify_workspace_bytes(int32_t n) { return n < 0 ? 0 : densify_workspace_bytes(n); }
+
+rg_status rg_densify_plan(const rg_gaussians* g, const float* acc, const int32_t* cnt,
+                          float grad_eps, float extent, float sigma_eps, float percent_dense,
+                          int32_t* action, void* ws, size_t ws_bytes, int32_t* counts,
+                          void* stream) {
+  if (!gaussians_ok(g) || !counts || !ws) return RG_ERR_INVALID_ARG;
+  if (g->n > 0 && (!acc || !cnt || !action)) return RG_ERR_INVALID_ARG;
+  if (!isfinite(grad_eps) || !(extent >= 0.f) || !isfinite(sigma_eps) || !(percent_dense >= 0.f))
+    return RG_ERR_INVALID_ARG;
+  if (ws_bytes < densify_workspace_bytes(g->n)) return RG_ERR_WORKSPACE_TOO_SMALL;
+  cudaGetLastError();
+  return launch_dens_plan(*g, acc, cnt, grad_eps, extent, sigma_eps, percent_dense, action,
+                          static_cast<char*>(ws), counts, static_cast<cudaStream_t>(stream)) ==
+                 cudaSuccess ? RG_OK : RG_ERR_CUDA;
+}
+
+rg_status rg_densify_apply(const rg_gaussians* g, const rg_param_arrays* in,
+                           const int32_t* action, const void* ws, const int32_t* counts,
+                           const float* z, int32_t mode, const rg_param_arrays* out, void* stream) {
+  if (!gaussians_ok(g) || !out || !ws || !counts || mode < 0 || mode > 2) return RG_ERR_INVALID_ARG;
+  if (g->n > 0 && (!action || !z)) return RG_ERR_INVALID_ARG;
+  rg_gaussian_grads src;
+  if (in) {
+    src = *in;
+  } else {
+    if (mode != 0) return RG_ERR_INVALID_ARG;
+    src = rg_gaussian_grads{const_cast<float*>(g->mean), const_cast<float*>(g->quat),
+                            const_cast<float*>(g->scale), const_cast<float*>(g->density),
+                            const_cast<float*>(g->sh), const_cast<float*>(g->sg_amp),
+                            const_cast<float*>(g->sg_sharp), const_cast<float*>(g->sg_axis)};
+  }
+  if (!arrays_ok(&src, g->n, g->sg_count) || !arrays_ok(out, 1, g->sg_count)) return RG_ERR_INVALID_ARG;
+  cudaGetLastError();
+  return launch_dens_apply(*g, src, *out, action, static_cast<const char*>(ws), counts, z, mode,
+                           static_cast<cudaStream_t>(stream)) == cudaSuccess ? RG_OK : RG_ERR_CUDA;
+}
+
 rg_status rg_camera_rays(const rg_camera* cam, float* origin, float* dir, void* stream) {
   if (!cam || !rays_ok(nullptr, cam)) return RG_ERR_INVALID_ARG;
   const int n = (cam->x1 - cam->x0) * (cam->y1 - cam->y0);

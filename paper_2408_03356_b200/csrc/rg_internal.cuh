@@ -265,6 +265,14 @@ cudaError_t launch_l1_dssim(const float* x, const float* y, int H, int W, float 
                             float* loss, float* ws, cudaStream_t st);
 cudaError_t launch_ss_resolve(const float* r, int64_t n, int spp, float* px, cudaStream_t st);
 cudaError_t launch_ss_spread(const float* dpx, int64_t n, int spp, float* dr, cudaStream_t st);
+size_t densify_workspace_bytes(int n);
+cudaError_t launch_dens_acc(const float* g, int n, float* acc, int* cnt, cudaStream_t st);
+cudaError_t launch_dens_plan(const rg_gaussians& g, const float* acc, const int* cnt, float grad_eps,
+                             float extent, float sigma_eps, float percent_dense, int* action,
+                             char* ws, int* counts, cudaStream_t st);
+cudaError_t launch_dens_apply(const rg_gaussians& g, const rg_gaussian_grads& in,
+                              const rg_gaussian_grads& out, const int* action, const char* ws,
+                              const int* counts, const float* z, int mode, cudaStream_t st);
 cudaError_t launch_camera_rays(const rg_camera& cam, float* o, float* d, cudaStream_t st);
 cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_config& c,
                            const rg_rays* rays, const rg_camera* cam, float* rgb, float* T,

@@ -352,4 +352,215 @@ cudaError_t launch_ss_spread(const float* dpx, int64_t n, int spp, float* dr, cu
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Adaptive density control (Alg. 3; readings L30-L32):
+//   k_dens_acc:   acc += ||dL/dmu||, cnt += (||dL/dmu|| > 0) per Gaussian (fp32);
+//   k_dens_plan:  action 0 keep / 1 clone / 2 split / 3 prune (fp32 decisions) and the
+//                 three output-order flags, block-scanned;  k_dens_scan: block totals;
+//   k_dens_apply: per input Gaussian, write its output rows (survivors in index
+//                 order, then clones, then 2 split children per split parent).
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kDensT = 256;
+
+__global__ void k_dens_acc(const float* g, int n, float* acc, int* cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float x = g[3 * i], y = g[3 * i + 1], z = g[3 * i + 2];
+  const float nrm = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(x, x), __fmul_rn(y, y)), __fmul_rn(z, z)));
+  acc[i] = __fadd_rn(acc[i], nrm);
+  cnt[i] += nrm > 0.f ? 1 : 0;
+}
+
+// action + inclusive block scans of (survivor, clone, split) flags; block totals
+__global__ void __launch_bounds__(kDensT) k_dens_plan(rg_gaussians g, const float* acc, const int* cnt,
+                                                      float grad_eps, float small_lim, float sigma_eps,
+                                                      int* action, int4* scan, int4* block_tot) {
+  __shared__ int3 sh[kDensT];
+  const int i = blockIdx.x * kDensT + threadIdx.x;
+  int3 f = make_int3(0, 0, 0);
+  if (i < g.n) {
+    const float avg = cnt[i] > 0 ? __fdiv_rn(acc[i], (float)cnt[i]) : 0.f;
+    const bool dens = avg >= grad_eps;
+    const float* sc = g.scale + 3 * (size_t)i;
+    const bool small = fmaxf(fmaxf(sc[0], sc[1]), sc[2]) <= small_lim;
+    const bool prune = g.density[i] < sigma_eps;
+    const int a = prune ? 3 : (dens ? (small ? 1 : 2) : 0);
+    action[i] = a;
+    f = make_int3(a <= 1 ? 1 : 0, a == 1 ? 1 : 0, a == 2 ? 1 : 0);
+  }
+  sh[threadIdx.x] = f;
+  __syncthreads();
+  for (int off = 1; off < kDensT; off <<= 1) {        // Hillis-Steele inclusive scan
+    int3 v = make_int3(0, 0, 0);
+    if ((int)threadIdx.x >= off) v = sh[threadIdx.x - off];
+    __syncthreads();
+    sh[threadIdx.x].x += v.x; sh[threadIdx.x].y += v.y; sh[threadIdx.x].z += v.z;
+    __syncthreads();
+  }
+  if (i < g.n) {
+    const int3 v = sh[threadIdx.x];
+    scan[i] = make_int4(v.x - f.x, v.y - f.y, v.z - f.z, 0);   // exclusive within the block
+  }
+  if (threadIdx.x == kDensT - 1) {
+    const int3 v = sh[kDensT - 1];
+    block_tot[blockIdx.x] = make_int4(v.x, v.y, v.z, 0);
+  }
+}
+
+// exclusive scan of the block totals (one block, looping) and the grand totals
+__global__ void k_dens_scan(int4* block_tot, int nb, int* counts) {
+  __shared__ int3 carry;
+  if (threadIdx.x == 0) carry = make_int3(0, 0, 0);
+  __syncthreads();
+  for (int base = 0; base < nb; base += 1024) {
+    const int k = base + threadIdx.x;
+    int4 v = k < nb ? block_tot[k] : make_int4(0, 0, 0, 0);
+    // warp-level inclusive scans then across warps via shared memory
+    __shared__ int3 wsum[32];
+    int3 x = make_int3(v.x, v.y, v.z);
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ax = __shfl_up_sync(0xffffffffu, x.x, o), ay = __shfl_up_sync(0xffffffffu, x.y, o),
+                az = __shfl_up_sync(0xffffffffu, x.z, o);
+      if ((threadIdx.x & 31) >= o) { x.x += ax; x.y += ay; x.z += az; }
+    }
+    if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int3 w = wsum[threadIdx.x];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ax = __shfl_up_sync(0xffffffffu, w.x, o), ay = __shfl_up_sync(0xffffffffu, w.y, o),
+                  az = __shfl_up_sync(0xffffffffu, w.z, o);
+        if (threadIdx.x >= (unsigned)o) { w.x += ax; w.y += ay; w.z += az; }
+      }
+      wsum[threadIdx.x] = w;
+    }
+    __syncthreads();
+    const int3 wp = (threadIdx.x >> 5) ? wsum[(threadIdx.x >> 5) - 1] : make_int3(0, 0, 0);
+    const int3 c = carry;
+    if (k < nb)
+      block_tot[k] = make_int4(c.x + wp.x + x.x - v.x, c.y + wp.y + x.y - v.y, c.z + wp.z + x.z - v.z, 0);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int3 t = wsum[31];
+      carry = make_int3(c.x + t.x, c.y + t.y, c.z + t.z);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    counts[0] = carry.x; counts[1] = carry.y; counts[2] = carry.z;
+    counts[3] = carry.x + carry.y + 2 * carry.z;      // output Gaussians
+  }
+}
+
+struct DensArgs {
+  rg_gaussians g;          // activated input (geometry of the split)
+  rg_gaussian_grads in;    // rows to move (mode 0: the activated arrays themselves)
+  rg_gaussian_grads out;
+  const int* action;
+  const int4* scan;
+  const int4* block_tot;
+  const int* counts;
+  const float* z;          // [n, 2, 3] standard normal draws
+  int nc, G, mode;         // 0 activated, 1 raw optimiser parameters, 2 moments (new rows zero)
+};
+
+__device__ __forceinline__ void copy_row(const float* a, float* b, int64_t src, int64_t dst, int w,
+                                         bool zero) {
+  for (int k = 0; k < w; ++k) b[dst * w + k] = zero ? 0.f : a[src * w + k];
+}
+
+__global__ void __launch_bounds__(kDensT) k_dens_apply(const DensArgs A) {
+  const int i = blockIdx.x * kDensT + threadIdx.x;
+  if (i >= A.g.n) return;
+  const int a = A.action[i];
+  if (a == 3) return;
+  const int4 sc = A.scan[i], bt = A.block_tot[blockIdx.x];
+  const int nkeep = A.counts[0], nclone = A.counts[1];
+  const int w[8] = {3, 4, 3, 1, 3 * A.nc, 3 * A.G, A.G, 3 * A.G};
+  const float* src[8] = {A.in.mean, A.in.quat, A.in.scale, A.in.density, A.in.sh, A.in.sg_amp,
+                         A.in.sg_sharp, A.in.sg_axis};
+  float* dst[8] = {A.out.mean, A.out.quat, A.out.scale, A.out.density, A.out.sh, A.out.sg_amp,
+                   A.out.sg_sharp, A.out.sg_axis};
+  if (a <= 1) {                                       // survivor (original row)
+    const int64_t o = sc.x + bt.x;
+    for (int k = 0; k < 8; ++k)
+      if (w[k]) copy_row(src[k], dst[k], i, o, w[k], false);
+  }
+  if (a == 1) {                                       // clone: a copy after the survivors
+    const int64_t o = nkeep + sc.y + bt.y;
+    for (int k = 0; k < 8; ++k)
+      if (w[k]) copy_row(src[k], dst[k], i, o, w[k], A.mode == 2);
+  }
+  if (a == 2) {                                       // split: two children
+    const float* q = A.g.quat + 4 * (size_t)i;
+    const float* s = A.g.scale + 3 * (size_t)i;
+    const float* mu = A.g.mean + 3 * (size_t)i;
+    const float nq = sqrtf(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    const float qw = q[0] / nq, qx = q[1] / nq, qy = q[2] / nq, qz = q[3] / nq;
+    const float R[9] = {1.f - 2.f * (qy * qy + qz * qz), 2.f * (qx * qy - qw * qz), 2.f * (qx * qz + qw * qy),
+                        2.f * (qx * qy + qw * qz), 1.f - 2.f * (qx * qx + qz * qz), 2.f * (qy * qz - qw * qx),
+                        2.f * (qx * qz - qw * qy), 2.f * (qy * qz + qw * qx), 1.f - 2.f * (qx * qx + qy * qy)};
+    for (int c = 0; c < 2; ++c) {
+      const int64_t o = nkeep + nclone + 2 * (int64_t)(sc.z + bt.z) + c;
+      for (int k = 0; k < 8; ++k)
+        if (w[k]) copy_row(src[k], dst[k], i, o, w[k], A.mode == 2);
+      if (A.mode == 2) continue;
+      const float* zz = A.z + 6 * (size_t)i + 3 * c;
+      const float l0 = s[0] * zz[0], l1 = s[1] * zz[1], l2 = s[2] * zz[2];
+      for (int r = 0; r < 3; ++r)                      // identity activation: raw mean = mean
+        dst[0][3 * o + r] = mu[r] + (R[3 * r] * l0 + R[3 * r + 1] * l1 + R[3 * r + 2] * l2);
+      for (int r = 0; r < 3; ++r)
+        dst[2][3 * o + r] = A.mode == 0 ? s[r] / 1.6f : src[2][3 * (size_t)i + r] - 0.47000362924573558f;
+    }
+  }
+}
+
+}  // namespace
+
+size_t densify_workspace_bytes(int n) {
+  const size_t nb = (size_t)(n + kDensT - 1) / kDensT;
+  return 16 * (size_t)(n > 0 ? n : 1) + 16 * (nb > 0 ? nb : 1) + 16;
+}
+
+cudaError_t launch_dens_acc(const float* g, int n, float* acc, int* cnt, cudaStream_t st) {
+  if (n > 0) { k_dens_acc<<<(n + 255) / 256, 256, 0, st>>>(g, n, acc, cnt); count_launches(1); }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dens_plan(const rg_gaussians& g, const float* acc, const int* cnt, float grad_eps,
+                             float extent, float sigma_eps, float percent_dense, int* action,
+                             char* ws, int* counts, cudaStream_t st) {
+  const int n = g.n;
+  const int nb = (n + kDensT - 1) / kDensT;
+  int4* scan = reinterpret_cast<int4*>(ws);
+  int4* bt = reinterpret_cast<int4*>(ws + 16 * (size_t)(n > 0 ? n : 1));
+  if (n == 0) {
+    cudaMemsetAsync(counts, 0, 16, st);
+    return cudaGetLastError();
+  }
+  const float small_lim = percent_dense * extent;     // fp32 product (as the oracle)
+  k_dens_plan<<<nb, kDensT, 0, st>>>(g, acc, cnt, grad_eps, small_lim, sigma_eps, action, scan, bt);
+  k_dens_scan<<<1, 1024, 0, st>>>(bt, nb, counts);
+  count_launches(2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dens_apply(const rg_gaussians& g, const rg_gaussian_grads& in,
+                              const rg_gaussian_grads& out, const int* action, const char* ws,
+                              const int* counts, const float* z, int mode, cudaStream_t st) {
+  const int n = g.n;
+  if (n == 0) return cudaSuccess;
+  DensArgs A{};
+  A.g = g; A.in = in; A.out = out; A.action = action;
+  A.scan = reinterpret_cast<const int4*>(ws);
+  A.block_tot = reinterpret_cast<const int4*>(ws + 16 * (size_t)n);
+  A.counts = counts; A.z = z;
+  A.nc = (g.sh_degree + 1) * (g.sh_degree + 1); A.G = g.sg_count; A.mode = mode;
+  k_dens_apply<<<(n + kDensT - 1) / kDensT, kDensT, 0, st>>>(A);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
 }  // namespace rg

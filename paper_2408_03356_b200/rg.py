@@ -73,7 +73,8 @@ class _BVH(C.Structure):
 
 EXPORTS = ("rg_status_string", "rg_version", "rg_kernel_launches", "rg_bvh_workspace_bytes", "rg_build_bvh",
            "rg_refit_bvh", "rg_adam_step", "rg_dssim_workspace_bytes", "rg_l1_dssim_loss_grad",
-           "rg_supersample_resolve", "rg_supersample_spread",
+           "rg_supersample_resolve", "rg_supersample_spread", "rg_densify_accumulate",
+           "rg_densify_workspace_bytes", "rg_densify_plan", "rg_densify_apply",
            "rg_camera_rays", "rg_render_forward", "rg_backward_workspace_bytes",
            "rg_render_backward", "rg_l1_loss_grad", "rg_fetch_log_bytes")
 
@@ -117,6 +118,14 @@ def lib(load_only: bool = False):
     L.rg_supersample_resolve.argtypes = [P, C.c_int64, I32, P, P]
     L.rg_supersample_spread.restype = C.c_int
     L.rg_supersample_spread.argtypes = [P, C.c_int64, I32, P, P]
+    L.rg_densify_accumulate.restype = C.c_int
+    L.rg_densify_accumulate.argtypes = [P, I32, P, P, P]
+    L.rg_densify_workspace_bytes.restype = SZ
+    L.rg_densify_workspace_bytes.argtypes = [I32]
+    L.rg_densify_plan.restype = C.c_int
+    L.rg_densify_plan.argtypes = [P, P, P, C.c_float, C.c_float, C.c_float, C.c_float, P, P, SZ, P, P]
+    L.rg_densify_apply.restype = C.c_int
+    L.rg_densify_apply.argtypes = [P, P, P, P, P, P, I32, P, P]
     L.rg_camera_rays.restype = C.c_int
     L.rg_camera_rays.argtypes = [P, P, P, P]
     L.rg_render_forward.restype = C.c_int
@@ -521,3 +530,62 @@ def supersample_spread(d_px, spp: int, out=None):
     _check(lib().rg_supersample_spread(_ptr(d_px.contiguous()), n, spp, _ptr(out), _stream()),
            "rg_supersample_spread")
     return out
+
+
+# ---------------------------------------------------------------------------
+# adaptive density control (Alg. 3)
+# ---------------------------------------------------------------------------
+
+class DensityStats:
+    """per-Gaussian accumulated ||dL/dmu|| and visible-iteration count"""
+
+    def __init__(self, n, device="cuda"):
+        self.acc = torch.zeros(n, dtype=torch.float32, device=device)
+        self.cnt = torch.zeros(n, dtype=torch.int32, device=device)
+
+    def accumulate(self, grad_mean):
+        _check(lib().rg_densify_accumulate(_ptr(grad_mean.contiguous()), self.acc.numel(),
+                                           _ptr(self.acc), _ptr(self.cnt), _stream()),
+               "rg_densify_accumulate")
+
+
+def densify(scene: Gaussians, stats: DensityStats, grad_eps: float, extent: float,
+            sigma_eps: float, percent_dense: float = 0.01, z=None, adam: "Adam" = None,
+            generator=None):
+    """One adaptive-density-control step: returns (new Gaussians, action tensor);
+    if `adam` is given its raw parameters and moments are carried over in place
+    (new rows: moments zero).  z: [n,2,3] normal draws (sampled if None)."""
+    _require_cuda()
+    L = lib()
+    n, dev = scene.n, scene.mean.device
+    if z is None:
+        z = torch.randn(n, 2, 3, device=dev, generator=generator)
+    ws = torch.empty(max(int(L.rg_densify_workspace_bytes(n)), 16), dtype=torch.uint8, device=dev)
+    action = torch.empty(n, dtype=torch.int32, device=dev)
+    counts = torch.zeros(4, dtype=torch.int32, device=dev)
+    gs = scene.struct()
+    _check(L.rg_densify_plan(C.byref(gs), _ptr(stats.acc), _ptr(stats.cnt), grad_eps, extent,
+                             sigma_eps, percent_dense, _ptr(action), _ptr(ws), ws.numel(),
+                             _ptr(counts), _stream()), "rg_densify_plan")
+    n_out = int(counts[3].item())
+
+    def alloc():
+        return {k: torch.empty((n_out,) + tuple(getattr(scene, k).shape[1:]), dtype=torch.float32,
+                               device=dev) for k in GROUPS}
+
+    def apply(src, mode):
+        out = alloc()
+        if n_out > 0:
+            _check(L.rg_densify_apply(C.byref(gs), None if src is None else C.byref(_arrays(src)),
+                                      _ptr(action), _ptr(ws), _ptr(counts), _ptr(z.contiguous()),
+                                      mode, C.byref(_arrays(out)), _stream()), "rg_densify_apply")
+        return out
+    new = apply(None, 0)
+    if adam is not None:
+        adam.raw = apply(adam.raw, 1)
+        adam.m = apply(adam.m, 2)
+        adam.v = apply(adam.v, 2)
+    g2 = Gaussians(*[new[k] for k in GROUPS], sh_degree=scene.sh_degree, sg_count=scene.sg_count)
+    if adam is not None:
+        adam.scene = g2
+    return g2, action

@@ -316,3 +316,76 @@ def test_raygauss4x_backward(oracle):
     up = np.repeat(d_px.astype(np.float64) / 4, 4, axis=0)
     ref = oracle.backward(sc, p, ro, rd, up, mode=2)
     grad_check(grads, ref)
+
+
+# ---------------------------------------------------------------------------
+# adaptive density control (NEXT-4) vs oracle/train.py
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [1, 700, 100_003])
+def test_densify_matches_oracle(n):
+    from oracle import train as T
+    rng = np.random.default_rng(n)
+    sc = synth.random_scene(2200 + n % 1000, n, sh_degree=1, sg_count=2, density_range=(0.02, 40),
+                            scale_range=(0.002, 0.05))
+    g = rg.Gaussians.from_scene(sc)
+    st = rg.DensityStats(n)
+    acc = np.zeros(n, np.float32); cnt = np.zeros(n, np.int32)
+    for it in range(3):
+        gm = (rng.normal(size=(n, 3)) * 10.0 ** rng.uniform(-6, -3, size=(n, 1))).astype(np.float32)
+        gm[rng.random(n) < 0.3] = 0.0                 # not seen this iteration
+        st.accumulate(torch.from_numpy(gm).cuda())
+        acc, cnt = T.densify_accumulate(acc, cnt, gm)
+    torch.cuda.synchronize()
+    assert np.array_equal(st.acc.cpu().numpy(), acc) and np.array_equal(st.cnt.cpu().numpy(), cnt)
+    act_np = {k: v for k, v in zip(rg.GROUPS, sc.arrays())}
+    action_ref = T.densify_plan(act_np, acc, cnt, grad_eps=2e-4, extent=1.2, sigma_eps=0.1)
+    z = rng.normal(size=(n, 2, 3)).astype(np.float32)
+    opt = rg.Adam(g)
+    opt.m = {k: torch.full_like(v, 0.5) for k, v in opt.m.items()}
+    raw_before = {k: v.clone() for k, v in opt.raw.items()}
+    g2, action = rg.densify(g, st, 2e-4, 1.2, 0.1, z=torch.from_numpy(z).cuda(), adam=opt)
+    torch.cuda.synchronize()
+    assert np.array_equal(action.cpu().numpy(), action_ref)
+    out_ref, src = T.densify_apply(act_np, action_ref, z.astype(np.float64))
+    assert g2.n == len(src)
+    nkeep = int(np.sum(action_ref <= 1)); nclone = int(np.sum(action_ref == 1))
+    for k in rg.GROUPS:
+        mine = getattr(g2, k).cpu().numpy().astype(np.float64)
+        ref = out_ref[k]
+        if k in ("mean", "scale"):
+            assert np.array_equal(mine[:nkeep + nclone], ref[:nkeep + nclone]), k
+            assert np.allclose(mine, ref, rtol=1e-6, atol=1e-6), k
+        else:
+            assert np.array_equal(mine, ref), k
+    # optimiser state: raw rows follow the same order; children's raw mean equals the
+    # activated child mean bit for bit, raw scale = raw - ln 1.6; new rows' moments 0
+    rb = {k: v.cpu().numpy() for k, v in raw_before.items()}
+    assert np.array_equal(opt.raw["mean"].cpu().numpy(), g2.mean.cpu().numpy())
+    base = nkeep + nclone
+    if g2.n > base:
+        parents = src[base:]
+        assert np.allclose(opt.raw["scale"][base:].cpu().numpy(), rb["scale"][parents] - np.log(1.6),
+                           atol=1e-6)
+    assert np.array_equal(opt.raw["sh"].cpu().numpy(), rb["sh"][src])
+    m = opt.m["quat"].cpu().numpy()
+    assert np.all(m[:nkeep] == 0.5) and np.all(m[nkeep:] == 0.0)
+
+
+def test_densify_then_render(oracle):
+    sc = synth.random_scene(2300, 300, sh_degree=1, sg_count=1, density_range=(0.05, 30),
+                            scale_range=(0.03, 0.1), extent=0.4)
+    g = rg.Gaussians.from_scene(sc)
+    st = rg.DensityStats(g.n)
+    st.accumulate(torch.full((g.n, 3), 1e-3, device="cuda"))
+    g2, action = rg.densify(g, st, 1e-3, 1.0, 0.1, generator=torch.Generator(device="cuda").manual_seed(0))
+    a = action.cpu().numpy()
+    assert (a == 1).any() and (a == 2).any() and (a == 3).any()
+    p = synth.RenderParams(dt=4e-3, t_eps=1e-4)
+    cfg = rg.Config.of(p)
+    o, d = synth.random_rays(2301, 500)
+    out = rg.render_forward(g2, rg.build_bvh(g2, cfg), cfg,
+                            rays=(torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()))
+    sc2 = synth.Scene(*[getattr(g2, k).cpu().numpy() for k in rg.GROUPS], sc.sh_degree, sc.sg_count)
+    ref = oracle.render(sc2, p, o, d, mode=2)
+    assert np.abs(out["rgb"].cpu().numpy() - ref["rgb"]).max() <= PIX_TOL
