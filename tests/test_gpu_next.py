@@ -373,8 +373,10 @@ def test_densify_matches_oracle(n):
 
 
 def test_densify_then_render(oracle):
-    sc = synth.random_scene(2300, 300, sh_degree=1, sg_count=1, density_range=(0.05, 30),
+    sc = synth.random_scene(2300, 300, sh_degree=1, sg_count=1, density_range=(0.5, 30),
                             scale_range=(0.03, 0.1), extent=0.4)
+    sc.scale[::5] *= 0.1          # small: cloned
+    sc.density[::7] = 0.05        # below sigma_eps: pruned
     g = rg.Gaussians.from_scene(sc)
     st = rg.DensityStats(g.n)
     st.accumulate(torch.full((g.n, 3), 1e-3, device="cuda"))
