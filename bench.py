@@ -393,6 +393,18 @@ def run_ours(args):
     mo, md = torch.cat(mix_o)[perm].contiguous(), torch.cat(mix_d)[perm].contiguous()
     del mix_o, mix_d
     mix_ms = timed(lambda: rg.render_forward(g, bvh, cfg, rays=(mo, md), out=fo))
+    # NEXT-4: one adaptive-density-control step (statistic of this step's dL/dmu,
+    # plan, apply to the parameters and the Adam state), grad_eps of P:644 (Blender)
+    dstats = rg.DensityStats(g.n, dev)
+    dstats.accumulate(gb.views["mean"])
+    dz = torch.randn(g.n, 2, 3, device=dev, generator=torch.Generator(device=dev).manual_seed(3))
+    dens_out = {}
+
+    def dens_step():
+        g3, act3 = rg.densify(ga, dstats, 5e-5, 1.3, p.sigma_eps, z=dz, adam=opt)
+        dens_out["n"] = g3.n
+        opt.scene = ga
+    dens_ms = timed(dens_step)
     next_rows = {
         "alg3_iteration_ms": iter_ms,
         "refit_bvh_ms": refit_ms,
@@ -402,6 +414,8 @@ def run_ours(args):
         "l1_dssim_ms": ssim_ms,
         "raygauss4x": {"fwd_ms": fwd4_ms, "rays": 4 * R, "cost_vs_1x": fwd4_ms / fwd_ms,
                        "paper": "about 3x (P:775)"},
+        "densify": {"ms": dens_ms, "n_in": g.n, "n_out": dens_out.get("n"),
+                    "what": "accumulate + plan + apply (params, raw, m, v), grad_eps 5e-5"},
         "uncorrelated_rays": {"fwd_ms": mix_ms, "rays": R,
                               "mrays_s": R / (mix_ms * 1e-3) / 1e6,
                               "what": "random sample of the rays of the 8 training views, shuffled"},
