@@ -40,7 +40,7 @@ class OgConfig(C.Structure):
     _fields_ = [("dt", C.c_float), ("slab_samples", C.c_int32), ("sigma_eps", C.c_float),
                 ("t_eps", C.c_float), ("hit_capacity", C.c_int32), ("radius_mode", C.c_int32),
                 ("k_sigma", C.c_float), ("t_near", C.c_float), ("background", C.c_float * 3),
-                ("pad_", C.c_int32)]
+                ("basis", C.c_int32)]
 
 
 class OgCounters(C.Structure):
@@ -79,6 +79,10 @@ def lib():
         _lib.og_camera_rays_spp.argtypes = [C.c_int32, C.c_int32, C.c_float, C.c_float, C.c_float,
                                             C.c_float, P, C.c_int32, C.c_int32, C.c_int32,
                                             C.c_int32, C.c_int32, P, P]
+        _lib.og_basis_phi.restype = C.c_double
+        _lib.og_basis_phi.argtypes = [C.c_int32, C.c_double]
+        _lib.og_basis_psi.restype = C.c_double
+        _lib.og_basis_psi.argtypes = [C.c_int32, C.c_double, C.c_double]
         _lib.og_clip.restype = C.c_int32
         _lib.og_clip.argtypes = [P, P, P, C.c_float, P, P]
         _lib.og_color.argtypes = [P, C.c_int32, P, P]
@@ -110,6 +114,7 @@ def config(params) -> OgConfig:
     c.dt = params.dt; c.slab_samples = params.slab_samples; c.sigma_eps = params.sigma_eps
     c.t_eps = params.t_eps; c.hit_capacity = params.hit_capacity
     c.radius_mode = params.radius_mode; c.k_sigma = params.k_sigma; c.t_near = params.t_near
+    c.basis = getattr(params, "basis", 0)
     for i in range(3):
         c.background[i] = params.background[i]
     return c
@@ -167,6 +172,17 @@ def camera_rays_spp(cam, spp):
     lib().og_camera_rays_spp(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, _p(c2w),
                              x0, y0, x1, y1, spp, _p(o), _p(d))
     return o, d
+
+
+BASES = ("gaussian", "bump", "wendland", "inv_multiquadric", "inv_quadratic", "matern_c0")
+
+
+def basis_phi(basis, q):
+    return lib().og_basis_phi(basis, float(q))
+
+
+def basis_psi(basis, sigma, q):
+    return lib().og_basis_psi(basis, float(sigma), float(q))
 
 
 def sh_basis(degree, d):

@@ -118,10 +118,24 @@ void og_prim_setup(const og_gaussians* g, const og_config* c, int32_t i,
   og_rotation_f32(q, R);
   for (int a = 0; a < 3; ++a)
     for (int b = 0; b < 3; ++b) M[3 * a + b] = R[3 * b + a] / s[a];   /* ARITH-2 */
-  if (c->radius_mode == 0)                                             /* ARITH-3 */
-    *r2 = (float)(2.0 * (log((double)dens) - log((double)c->sigma_eps)));
-  else
+  if (c->radius_mode == 0) {                                           /* ARITH-3 */
+    /* r^2 = phi^-1(sigma_eps / sigma~)^2, fp64 then rounded once;
+       compact supports are the unit ball (no truncation needed) */
+    const double k = (double)dens / (double)c->sigma_eps;
+    switch (c->basis) {
+      case 1: case 2: *r2 = 1.0f; break;                                /* Bump, Wendland */
+      case 3: *r2 = (float)(k * k - 1.0); break;                        /* (1+r^2)^-1/2 >= 1/k */
+      case 4: *r2 = (float)(k - 1.0); break;                            /* 1/(1+r^2) >= 1/k */
+      case 5: {                                                         /* e^-r >= 1/k */
+        const double l = log((double)dens) - log((double)c->sigma_eps);
+        *r2 = (float)(l * l);
+        break;
+      }
+      default: *r2 = (float)(2.0 * (log((double)dens) - log((double)c->sigma_eps)));
+    }
+  } else {
     *r2 = c->k_sigma * c->k_sigma;
+  }
   for (int a = 0; a < 3; ++a) {                                         /* ARITH-4 */
     const float a0 = s[0] * R[3 * a + 0];
     const float a1 = s[1] * R[3 * a + 1];
@@ -533,7 +547,33 @@ static const double* color_of(ctx_t* cx, int l, int ray, const double d[3]) {
   return cx->col + 3 * (size_t)l;
 }
 
-/* fp64 weight sigma~ * G(x; mu, q, s) at x (Eq. 12-13) */
+/* basis functions of the supplementary as functions of q = r^2 */
+double og_basis_phi(int32_t basis, double q) {
+  const double r = sqrt(q);
+  switch (basis) {
+    case 1: return q < 1.0 ? exp(1.0 - 1.0 / (1.0 - q)) : 0.0;              /* Bump * e */
+    case 2: return r <= 1.0 ? pow(1.0 - r, 4) * (4.0 * r + 1.0) : 0.0;        /* Wendland */
+    case 3: return 1.0 / sqrt(1.0 + q);                                       /* inv. multiquadric */
+    case 4: return 1.0 / (1.0 + q);                                           /* inv. quadratic */
+    case 5: return exp(-r);                                                   /* C0-Matern */
+    default: return exp(-0.5 * q);                                            /* Gaussian */
+  }
+}
+
+/* psi = -2 sigma~ dphi/dq: dw/dy = -psi y for y = M(x - mu), |y|^2 = q */
+double og_basis_psi(int32_t basis, double sigma, double q) {
+  const double r = sqrt(q);
+  switch (basis) {
+    case 1: return q < 1.0 ? 2.0 * sigma * og_basis_phi(1, q) / ((1.0 - q) * (1.0 - q)) : 0.0;
+    case 2: return r <= 1.0 ? 20.0 * sigma * pow(1.0 - r, 3) : 0.0;
+    case 3: return sigma * pow(1.0 + q, -1.5);
+    case 4: return 2.0 * sigma / ((1.0 + q) * (1.0 + q));
+    case 5: return r > 0.0 ? sigma * exp(-r) / r : 0.0;    /* kink at r = 0: subgradient 0 */
+    default: return sigma * exp(-0.5 * q);
+  }
+}
+
+/* fp64 weight sigma~ * phi(|M(x-mu)|) at x (Eq. 12-13; other bases P:456-515) */
 static double weight_at(const ctx_t* cx, int l, const double x[3], double y_out[3]) {
   const double* M = cx->M64 + 9 * (size_t)l;
   const float* mu = cx->g->mean + 3 * (size_t)l;
@@ -541,7 +581,7 @@ static double weight_at(const ctx_t* cx, int l, const double x[3], double y_out[
   double y[3];
   for (int a = 0; a < 3; ++a) y[a] = M[3 * a] * v0 + M[3 * a + 1] * v1 + M[3 * a + 2] * v2;
   if (y_out) { y_out[0] = y[0]; y_out[1] = y[1]; y_out[2] = y[2]; }
-  return (double)cx->g->density[l] * exp(-0.5 * (y[0] * y[0] + y[1] * y[1] + y[2] * y[2]));
+  return (double)cx->g->density[l] * og_basis_phi(cx->cfg->basis, y[0] * y[0] + y[1] * y[1] + y[2] * y[2]);
 }
 
 /* per-slab hit set: Gaussians whose support interval overlaps [tlo, thi] (L9) */
@@ -864,17 +904,19 @@ int32_t og_backward(const og_gaussians* g, const og_config* c, int32_t mode, con
         double y[3];
         const double wchk = weight_at(&cx, l, x, y);
         (void)wchk;
+        const double psi = og_basis_psi(c->basis, (double)g->density[l],
+                                        y[0] * y[0] + y[1] * y[1] + y[2] * y[2]);
         const double v[3] = {x[0] - mu[0], x[1] - mu[1], x[2] - mu[2]};
-        for (int b = 0; b < 3; ++b) {     /* dw/dmu = w M^T y */
+        for (int b = 0; b < 3; ++b) {     /* dw/dmu = psi M^T y (psi = w: Gaussian) */
           const double mty = M[b] * y[0] + M[3 + b] * y[1] + M[6 + b] * y[2];
-          g_mean[3 * (size_t)l + b] += dLdw * w * mty;
+          g_mean[3 * (size_t)l + b] += dLdw * psi * mty;
         }
         g_density[l] += dLdw * w / (double)g->density[l];
         double dLdR[9] = {0};
         for (int a = 0; a < 3; ++a) {
           const double sa = sc[a];
           for (int b = 0; b < 3; ++b) {
-            const double dLdM = dLdw * (-w * y[a] * v[b]);     /* dw/dM_ab = -w y_a v_b */
+            const double dLdM = dLdw * (-psi * y[a] * v[b]);   /* dw/dM_ab = -psi y_a v_b */
             g_scale[3 * (size_t)l + a] += dLdM * (-R[3 * b + a] / (sa * sa));
             dLdR[3 * b + a] += dLdM / sa;                       /* M_ab = R_ba / s_a */
           }

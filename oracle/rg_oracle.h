@@ -48,7 +48,8 @@ typedef struct {
   float k_sigma;
   float t_near;
   float background[3];
-  int32_t pad_;
+  int32_t basis;         /* basis function phi: 0 Gaussian, 1 Bump, 2 Wendland,
+                            3 inverse multiquadric, 4 inverse quadratic, 5 C0-Matern */
 } og_config;
 
 typedef struct {
@@ -92,6 +93,11 @@ void og_camera_rays_spp(int32_t width, int32_t height, float fx, float fy, float
 /* scene-bbox clip (ARITH-8): returns 1 if t0 < t1 */
 int32_t og_clip(const float box[6], const float o[3], const float d[3], float t_near,
                 float* t0, float* t1);
+
+/* basis function phi(r) at q = r^2 (fp64), and psi = -2 sigma~ dphi/dq
+   (the weight's sensitivity to q; psi = w for the Gaussian) */
+double og_basis_phi(int32_t basis, double q);
+double og_basis_psi(int32_t basis, double sigma, double q);
 
 /* ---- BVH (own implementation: O3) ------------------------------------- */
 typedef struct og_bvh og_bvh;

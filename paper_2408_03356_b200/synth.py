@@ -92,6 +92,8 @@ class RenderParams:
     k_sigma: float = 3.0
     t_near: float = 0.0
     background: tuple = (1.0, 1.0, 1.0)
+    basis: int = 0              # basis function: 0 Gaussian, 1 Bump, 2 Wendland,
+                                # 3 inverse multiquadric, 4 inverse quadratic, 5 C0-Matern
 
     def replace(self, **kw) -> "RenderParams":
         d = dict(self.__dict__)
