@@ -73,8 +73,13 @@ typedef struct {
   float k_sigma;         /* support radius in radius_mode 1 (north star "3-sigma") */
   float t_near;          /* t0 = max(bbox entry, t_near) (L13), usually 0 */
   float background[3];   /* pixel = C + T_end * background (L12) */
-  int32_t pad_;
+  int32_t basis;         /* basis function phi (supplementary P:456-515, L33):
+                            RG_BASIS_* below; non-Gaussian bases need radius_mode 0 and
+                            slab_samples >= 5 (else RG_ERR_NOT_IMPLEMENTED) */
 } rg_config;
+
+enum { RG_BASIS_GAUSSIAN = 0, RG_BASIS_BUMP = 1, RG_BASIS_WENDLAND = 2,
+       RG_BASIS_INV_MULTIQUADRIC = 3, RG_BASIS_INV_QUADRATIC = 4, RG_BASIS_MATERN_C0 = 5 };
 
 /* Explicit, possibly uncorrelated rays: device [n,3] origins and
    unit directions. */

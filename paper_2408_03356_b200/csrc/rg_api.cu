@@ -26,6 +26,8 @@ bool config_ok(const rg_config* c) {
   if (c->radius_mode != 0 && c->radius_mode != 1) return false;
   if (c->radius_mode == 1 && !(c->k_sigma > 0.0f)) return false;
   if (!isfinite(c->t_near)) return false;
+  if (c->basis < 0 || c->basis > 5) return false;
+  if (c->basis != 0 && c->radius_mode != 0) return false;
   return true;
 }
 
@@ -258,7 +260,8 @@ rg_status rg_render_forward(const rg_gaussians* g, const rg_bvh* bvh, const rg_c
                             int32_t* debug_counts, int32_t* debug_records, void* stream) {
   if (!gaussians_ok(g) || !config_ok(cfg) || !bvh_ok(bvh, g) || !rays_ok(rays, cam))
     return RG_ERR_INVALID_ARG;
-  const int64_t n = rays ? rays->n : (int64_t)(cam->x1 - cam->x0) * (cam->y1 - cam->y0);
+  if (cfg->basis != 0 && cfg->slab_samples < 5) return RG_ERR_NOT_IMPLEMENTED;
+  const int64_t n = rays ? rays->n : (int64_t)(cam->x1 - cam->x0) * (cam->y1 - cam->y0) * cam->spp;
   if (n > 0 && (!rgb || !T || !replay)) return RG_ERR_INVALID_ARG;
   if (debug_records && (debug_rays < 0 || debug_cap < 1 || !debug_counts))
     return RG_ERR_INVALID_ARG;
@@ -292,7 +295,8 @@ rg_status rg_render_backward(const rg_gaussians* g, const rg_bvh* bvh, const rg_
                              size_t ws_bytes, void* stream) {
   if (!gaussians_ok(g) || !config_ok(cfg) || !bvh_ok(bvh, g) || !rays_ok(rays, cam) || !grads)
     return RG_ERR_INVALID_ARG;
-  const int64_t n = rays ? rays->n : (int64_t)(cam->x1 - cam->x0) * (cam->y1 - cam->y0);
+  if (cfg->basis != 0 && cfg->slab_samples < 5) return RG_ERR_NOT_IMPLEMENTED;
+  const int64_t n = rays ? rays->n : (int64_t)(cam->x1 - cam->x0) * (cam->y1 - cam->y0) * cam->spp;
   if (n > 0 && (!rgb || !replay || !d_rgb)) return RG_ERR_INVALID_ARG;
   if (!ws || (reinterpret_cast<uintptr_t>(ws) & 15) != 0) return RG_ERR_INVALID_ARG;
   if (ws_bytes < rg_backward_workspace_bytes(g->n, g->sh_degree, g->sg_count))

@@ -65,10 +65,24 @@ __device__ void support_exact(const rg_gaussians& g, const rg_config& c, int i, 
   for (int a = 0; a < 3; ++a)
     for (int b = 0; b < 3; ++b) M[3 * a + b] = div_(R[3 * b + a], s[a]);
   if (!active) { r2 = -1.0f; return; }
-  if (c.radius_mode == 0)
-    r2 = (float)(2.0 * (log((double)g.density[i]) - log((double)c.sigma_eps)));
-  else
+  if (c.radius_mode == 0) {
+    // r = phi^-1(sigma_eps / sigma~) in fp64, rounded once; compact bases:
+    // the unit ball
+    const double k = (double)g.density[i] / (double)c.sigma_eps;
+    switch (c.basis) {
+      case 1: case 2: r2 = 1.0f; break;
+      case 3: r2 = (float)(k * k - 1.0); break;
+      case 4: r2 = (float)(k - 1.0); break;
+      case 5: {
+        const double l = log((double)g.density[i]) - log((double)c.sigma_eps);
+        r2 = (float)(l * l);
+        break;
+      }
+      default: r2 = (float)(2.0 * (log((double)g.density[i]) - log((double)c.sigma_eps)));
+    }
+  } else {
     r2 = mul_(c.k_sigma, c.k_sigma);
+  }
 }
 
 __global__ void __launch_bounds__(kThreads) k_preprocess(rg_gaussians g, rg_config c,

@@ -56,7 +56,7 @@ static_assert(kA == 64, "expire/n_in handle two 32-slot chunks");
 // backward traverses only for rays whose fetch log overflowed and must stay within
 // its 48 KB block budget
 constexpr int kStkFwd = RG_STK_FWD;
-constexpr int kStkBwd = 216;
+constexpr int kStkBwd = 192;
 constexpr unsigned kFull = 0xffffffffu;
 
 struct Counters {
@@ -106,7 +106,9 @@ struct WarpMemT {
 struct WarpAcc {
   float4 a[kSlots];    // Sw, Sw1, Sw2, dc_r
   float2 b[kSlots];    // dc_g, dc_b
-  float4 s0[32], s1[32];  // per-sample backward values of the current group / window:
+  float c[kSlots];     // sum w dL/dw (dL/dsigma~ of non-Gaussian bases; = a.x for the Gaussian)
+  float4 s0[32];
+  float s1[32];        // per-sample backward values of the current group / window:
                           // {tk, dls, dc0, dc1}, {dc2, gc, inv, live}
 };
 
@@ -423,7 +425,42 @@ __device__ __forceinline__ float3 pair_color(const SceneView& S, const float* Y,
 #else
 #define RG_SCATTER_ATTR __forceinline__
 #endif
-template <bool VEC, class WM>
+// ---- basis functions (supplementary P:456-515).  Gaussian slots hold
+// log2 w(tau) = c0 + tau (c1 + c2 tau); other bases hold q(tau) = |M x(tau)|^2 =
+// qm + tau (2 b1 + A tau) (e0.w, e1.x, e1.y) and sigma~ (e2.w).
+template <int BASIS>
+__device__ __forceinline__ float basis_w(float tau, const float4& a, const float4& q, float sig,
+                                         float& qq) {
+  const float p = fmaf(tau, fmaf(q.y, tau, q.x), a.w);
+  qq = p;
+  if (BASIS == 0) return ex2_approx(p);
+  const float pp = fmaxf(p, 0.f);
+  if (BASIS == 1) return pp < 1.f ? sig * ex2_approx((1.f - 1.f / (1.f - pp)) * kLog2e) : 0.f;
+  if (BASIS == 2) {
+    const float r = sqrtf(pp), u = 1.f - r;
+    return r <= 1.f ? sig * ((u * u) * (u * u)) * fmaf(4.f, r, 1.f) : 0.f;
+  }
+  if (BASIS == 3) return sig * rsqrtf(1.f + pp);
+  if (BASIS == 4) return sig / (1.f + pp);
+  return sig * ex2_approx(-sqrtf(pp) * kLog2e);                    // C0-Matern
+}
+// psi = -2 sigma~ dphi/dq (dw/dy = -psi y); the Gaussian's psi is w
+template <int BASIS>
+__device__ __forceinline__ float basis_psi(float w, float qq, float sig) {
+  if (BASIS == 0) return w;
+  const float pp = fmaxf(qq, 0.f);
+  if (BASIS == 1) { const float u = 1.f - pp; return pp < 1.f ? 2.f * w / (u * u) : 0.f; }
+  if (BASIS == 2) {
+    const float r = sqrtf(pp), u = 1.f - r;
+    return r <= 1.f ? 20.f * sig * (u * u * u) : 0.f;
+  }
+  if (BASIS == 3) { const float ph = w / sig; return w * ph * ph; }     // sigma~ (1+q)^-3/2
+  if (BASIS == 4) return 2.f * w * (w / sig);                           // 2 sigma~ (1+q)^-2
+  const float r = sqrtf(pp);
+  return r > 0.f ? w / r : 0.f;                                         // kink at r = 0
+}
+
+template <bool VEC, int BASIS, class WM>
 __device__ RG_SETUP_ATTR void setup_pair(const SceneView& S, WM& M, int sl, const Ray& R,
                                         uint32_t pos) {
   const float4* gp = S.geom + 4 * (size_t)pos;
@@ -439,9 +476,15 @@ __device__ RG_SETUP_ATTR void setup_pair(const SceneView& S, WM& M, int sl, cons
   const float qm = u0 * u0 + u1 * u1 + u2 * u2;
   const float b1 = u0 * pg.dl0 + u1 * pg.dl1 + u2 * pg.dl2;
   const float3 col = pair_color<VEC>(S, M.Y, (int)pos, R.d);
-  M.e0[sl] = make_float4(pg.te, pg.tx, pg.tm, lg2_approx(g0.w) - 0.5f * kLog2e * qm);
-  M.e1[sl] = make_float4(-kLog2e * b1, -0.5f * kLog2e * pg.A, col.x, col.y);
-  M.e2[sl] = make_float4(col.z, __int_as_float((int)pos), g3.z, 0.f);
+  if (BASIS == 0) {
+    M.e0[sl] = make_float4(pg.te, pg.tx, pg.tm, lg2_approx(g0.w) - 0.5f * kLog2e * qm);
+    M.e1[sl] = make_float4(-kLog2e * b1, -0.5f * kLog2e * pg.A, col.x, col.y);
+    M.e2[sl] = make_float4(col.z, __int_as_float((int)pos), g3.z, 0.f);
+  } else {
+    M.e0[sl] = make_float4(pg.te, pg.tx, pg.tm, qm);
+    M.e1[sl] = make_float4(2.f * b1, pg.A, col.x, col.y);
+    M.e2[sl] = make_float4(col.z, __int_as_float((int)pos), g3.z, g0.w);
+  }
 }
 
 // 1 - exp(-x) without cancellation for small x
@@ -458,7 +501,7 @@ struct Lanes {
 };
 
 // sigma and sigma*c at this lane's sample from slots [e0, e1)
-template <int GW, class WM>
+template <int GW, int BASIS, class WM>
 __device__ __forceinline__ void eval_range(const WM& M, int e0, int e1, const Lanes<GW>& L,
                                            float tk, bool val, float& s, float& r, float& g,
                                            float& b, uint32_t& evals) {
@@ -467,9 +510,11 @@ __device__ __forceinline__ void eval_range(const WM& M, int e0, int e1, const La
     const float4 a = M.e0[e];
     if (val && a.x <= tk && tk <= a.y) {
       const float4 q = M.e1[e];
-      const float cb = M.e2[e].x;
+      const float4 e2 = M.e2[e];
+      const float cb = e2.x;
       const float tau = tk - a.z;
-      const float w = ex2_approx(fmaf(tau, fmaf(q.y, tau, q.x), a.w));
+      float qq;
+      const float w = basis_w<BASIS>(tau, a, q, e2.w, qq);
       s += w;
       r = fmaf(w, q.z, r);
       g = fmaf(w, q.w, g);
@@ -486,7 +531,7 @@ struct SampleGrad {   // per-sample backward quantities (lanes of sample j)
 // accumulate the per-pair moments of slots [e0, e1) over this group's samples:
 // lane = slot, loop over the GW samples whose backward values the composite
 // step left in A.s0/A.s1 (broadcast reads), moments kept in registers.
-template <int GW, class WM>
+template <int GW, int BASIS, class WM>
 __device__ __forceinline__ void grad_range(const WM& M, WarpAcc& A, int e0, int e1) {
   __syncwarp();
   for (int base = e0; base < e1; base += 32) {
@@ -494,24 +539,27 @@ __device__ __forceinline__ void grad_range(const WM& M, WarpAcc& A, int e0, int 
     if (e < e1) {
       const float4 a = M.e0[e];
       const float4 q = M.e1[e];
-      const float cb = M.e2[e].x;
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
+      const float4 e2 = M.e2[e];
+      const float cb = e2.x;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f;
 #pragma unroll
       for (int j = 0; j < GW; ++j) {
         const float4 s0 = A.s0[j];
         const float tk = s0.x;
         if (a.x <= tk && tk <= a.y) {
-          const float b2 = A.s1[j].x;
+          const float b2 = A.s1[j];
           const float tau = tk - a.z;
-          const float w = ex2_approx(fmaf(tau, fmaf(q.y, tau, q.x), a.w));
+          float qq;
+          const float w = basis_w<BASIS>(tau, a, q, e2.w, qq);
           const float dldw = fmaf(s0.z, q.z, fmaf(s0.w, q.w, fmaf(b2, cb, s0.y)));
-          const float wd = w * dldw;
+          const float wd = basis_psi<BASIS>(w, qq, e2.w) * dldw;
           a0 += wd;
           a1 = fmaf(wd, tau, a1);
           a2 = fmaf(wd * tau, tau, a2);
           a3 = fmaf(w, s0.z, a3);
           a4 = fmaf(w, s0.w, a4);
           a5 = fmaf(w, b2, a5);
+          if (BASIS != 0) a6 = fmaf(w, dldw, a6);
         }
       }
       float4 v = A.a[e];
@@ -520,6 +568,7 @@ __device__ __forceinline__ void grad_range(const WM& M, WarpAcc& A, int e0, int 
       w.x += a4; w.y += a5;
       A.a[e] = v;
       A.b[e] = w;
+      if (BASIS != 0) A.c[e] += a6;
     }
   }
   __syncwarp();
@@ -531,7 +580,7 @@ __device__ __forceinline__ void grad_range(const WM& M, WarpAcc& A, int e0, int 
 //  With x = x' + tau d, u = M x', d_l = M d and Sw = sum w dL/dw, Sw1 = sum w dL/dw tau,
 //  Sw2 = sum w dL/dw tau^2:  dL/dmu = M^T (Sw u + Sw1 d_l),
 //  dL/dM = -(Sw u x'^T + Sw1 (u d^T + d_l x'^T) + Sw2 d_l d^T),  dL/dsigma~ = Sw / sigma~.
-template <class WM>
+template <int BASIS, class WM>
 __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, const WarpAcc& A,
                                            int base, unsigned mask, const Ray& R,
                                            float* gbuf, int gstride) {
@@ -543,7 +592,8 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, c
     if (mask & (1u << lane)) {
       const float4 v = A.a[base + lane];
       const float2 w = A.b[base + lane];
-      nz = v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f || w.x != 0.f || w.y != 0.f;
+      nz = v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f || w.x != 0.f || w.y != 0.f ||
+           (BASIS != 0 && A.c[base + lane] != 0.f);
     }
     mask = __ballot_sync(kFull, nz);
   }
@@ -583,7 +633,7 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, c
         dM[3 * r + b] = -(Sw * u[r] * xp[b] + Sw1 * (u[r] * dv[b] + dl[r] * xp[b]) +
                           Sw2 * dl[r] * dv[b]);
     float4* row = reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride);
-    atomicAdd(row + 0, make_float4(gm[0], gm[1], gm[2], Sw / g0.w));
+    atomicAdd(row + 0, make_float4(gm[0], gm[1], gm[2], (BASIS == 0 ? Sw : A.c[e]) / g0.w));
     atomicAdd(row + 1, make_float4(dM[0], dM[1], dM[2], dM[3]));
     atomicAdd(row + 2, make_float4(dM[4], dM[5], dM[6], dM[7]));
     atomicAdd(row + 3, make_float4(dM[8], 0.f, 0.f, 0.f));
@@ -685,7 +735,7 @@ __device__ __forceinline__ void dbg_put(const RenderArgs& P, int ray, int& dbg_n
 
 // INSTR: counters (rg_stats) and the debug dump; the uninstrumented variant
 // compiles them out (8 fewer live registers through the march)
-template <bool BWD, int GW, bool INSTR>
+template <bool BWD, int GW, bool INSTR, int BASIS>
 __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FWD) k_render(const RenderArgs P) {
   // static shared memory (fwd 35.6 KB, bwd 48.0 KB <= the 48 KB static limit): constant
   // shared-window offsets; the dynamic (extern) form made the compiler re-derive the
@@ -789,7 +839,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
               const unsigned gm = h ? gone1 : gone0;
               if (!gm) continue;
               if (nret + __popc(gm) > 32) {
-                scatter_batch(P.S, M, A, kRet, nret >= 32 ? kFull : ((1u << nret) - 1u), R,
+                scatter_batch<BASIS>(P.S, M, A, kRet, nret >= 32 ? kFull : ((1u << nret) - 1u), R,
                               P.gbuf, P.gstride);
                 nret = 0;
                 __syncwarp();
@@ -799,6 +849,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
                 const int dst = kRet + nret + __popc(gm & ((1u << lane) - 1u));
                 M.e0[dst] = M.e0[e]; M.e1[dst] = M.e1[e]; M.e2[dst] = M.e2[e];
                 A.a[dst] = A.a[e]; A.b[dst] = A.b[e];
+                if (BASIS != 0) A.c[dst] = A.c[e];
               }
               nret += __popc(gm);
               __syncwarp();
@@ -811,16 +862,17 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             const bool keep = e < count && !(((h ? gone1 : gone0) >> lane) & 1u);
             float4 v0, v1, v2, a0;
             float2 a1;
+            float a2c = 0.f;
             if (keep) {
               v0 = M.e0[e]; v1 = M.e1[e]; v2 = M.e2[e];
-              if (BWD) { a0 = A.a[e]; a1 = A.b[e]; }
+              if (BWD) { a0 = A.a[e]; a1 = A.b[e]; if (BASIS != 0) a2c = A.c[e]; }
             }
             const unsigned km = __ballot_sync(kFull, keep);
             const int dst = nc + __popc(km & ((1u << lane) - 1u));
             __syncwarp();
             if (keep) {
               M.e0[dst] = v0; M.e1[dst] = v1; M.e2[dst] = v2;
-              if (BWD) { A.a[dst] = a0; A.b[dst] = a1; }
+              if (BWD) { A.a[dst] = a0; A.b[dst] = a1; if (BASIS != 0) A.c[dst] = a2c; }
             }
             nc += __popc(km);
             __syncwarp();
@@ -849,7 +901,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
           }
         } else {
           got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
-          if ((int)lane < got) setup_pair<!BWD>(P.S, M, count + (int)lane, R, pos);
+          if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, count + (int)lane, R, pos);
           if (!BWD && log_ok) {
             unsigned long long off = 0;
             if (lane == 0 && got > 0) off = atomicAdd(P.arena_ctr, (unsigned long long)got);
@@ -872,6 +924,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
         if (BWD && (int)lane < got) {
           A.a[count + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
           A.b[count + lane] = make_float2(0.f, 0.f);
+          A.c[count + lane] = 0.f;
         }
         if (lane == 0) cnt.pairs += got;
         count += got;
@@ -907,9 +960,11 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             const float4 a = M.e0[e];
             if (val && a.x <= tk && tk <= a.y) {
               const float4 q = M.e1[e];
-              const float cbv = M.e2[e].x;
+              const float4 e2 = M.e2[e];
+              const float cbv = e2.x;
               const float tau_ = tk - a.z;
-              const float w = ex2_approx(fmaf(tau_, fmaf(q.y, tau_, q.x), a.w));
+              float qq;
+              const float w = basis_w<BASIS>(tau_, a, q, e2.w, qq);
               sg += w;
               sr = fmaf(w, q.z, sr);
               sgg = fmaf(w, q.w, sgg);
@@ -998,7 +1053,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             // dL/dw_e = (dls - gc/sigma) + <dc, c_e>/sigma: per-sample coefficients
             // (zero for dead samples, so the member loop needs no liveness test)
             A.s0[lane] = make_float4(tk, H.dls - H.gc * H.inv, H.dc0 * H.inv, H.dc1 * H.inv);
-            A.s1[lane] = make_float4(H.dc2 * H.inv, 0.f, 0.f, 0.f);
+            A.s1[lane] = H.dc2 * H.inv;
             __syncwarp();
             // lane = (member, part): P2 members per pass, each member's window samples
             // split into 32/P2 parts of P2 samples; parts reduced by xor shuffles
@@ -1006,12 +1061,13 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             for (int base = 0; base < n3; base += P2) {
               const int e = base + ((int)lane & (P2 - 1));
               const int part0 = (int)lane & ~(P2 - 1);   // first sample of this lane's part
-              float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
+              float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f;
               float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
               if (e < n3) {
                 a = M.e0[e];
                 const float4 q = M.e1[e];
-                const float cbv = M.e2[e].x;
+                const float4 e2 = M.e2[e];
+                const float cbv = e2.x;
                 const float kf = (float)k0 + 0.5f;
                 int kl = (int)floorf((a.x - t0) / c.dt - kf) - 1;
                 int kh = (int)ceilf((a.y - t0) / c.dt - kf) + 1;
@@ -1022,17 +1078,19 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
                   const float4 s0 = A.s0[k];
                   const float tkk = s0.x;
                   if (a.x <= tkk && tkk <= a.y) {
-                    const float b2 = A.s1[k].x;
+                    const float b2 = A.s1[k];
                     const float tau_ = tkk - a.z;
-                    const float w = ex2_approx(fmaf(tau_, fmaf(q.y, tau_, q.x), a.w));
+                    float qq;
+                    const float w = basis_w<BASIS>(tau_, a, q, e2.w, qq);
                     const float dldw = fmaf(s0.z, q.z, fmaf(s0.w, q.w, fmaf(b2, cbv, s0.y)));
-                    const float wd = w * dldw;
+                    const float wd = basis_psi<BASIS>(w, qq, e2.w) * dldw;
                     a0 += wd;
                     a1 = fmaf(wd, tau_, a1);
                     a2 = fmaf(wd * tau_, tau_, a2);
                     a3 = fmaf(w, s0.z, a3);
                     a4 = fmaf(w, s0.w, a4);
                     a5 = fmaf(w, b2, a5);
+                    if (BASIS != 0) a6 = fmaf(w, dldw, a6);
                   }
                 }
               }
@@ -1043,6 +1101,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
                 a3 += __shfl_xor_sync(kFull, a3, off);
                 a4 += __shfl_xor_sync(kFull, a4, off);
                 a5 += __shfl_xor_sync(kFull, a5, off);
+                if (BASIS != 0) a6 += __shfl_xor_sync(kFull, a6, off);
               }
               if (e < n3 && part0 == 0) {
                 float4 v = A.a[e];
@@ -1051,6 +1110,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
                 w2.x += a4; w2.y += a5;
                 A.a[e] = v;
                 A.b[e] = w2;
+                if (BASIS != 0) A.c[e] += a6;
               }
             }
             __syncwarp();
@@ -1089,7 +1149,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
         const bool val = (g0 + L.j < B) && (tk < t1);
         float sg = 0.f, sr = 0.f, sgg = 0.f, sb = 0.f;
         uint32_t ev = 0;
-        eval_range<GW>(M, 0, n_use, L, tk, val, sg, sr, sgg, sb, ev);
+        eval_range<GW, BASIS>(M, 0, n_use, L, tk, val, sg, sr, sgg, sb, ev);
         if (more) {   // slab set larger than the active list: stream the rest
           unsigned long long cur2 = cursor;
           int remaining = K - n_use;
@@ -1099,9 +1159,9 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             unsigned long long key;
             uint32_t pos;
             const int got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
-            if ((int)lane < got) setup_pair<!BWD>(P.S, M, kTrans + (int)lane, R, pos);
+            if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, kTrans + (int)lane, R, pos);
             __syncwarp();
-            eval_range<GW>(M, kA, kA + got, L, tk, val, sg, sr, sgg, sb, ev);
+            eval_range<GW, BASIS>(M, kA, kA + got, L, tk, val, sg, sr, sgg, sb, ev);
             if (dbg && g0 == 0) dbg_put(P, ray, dbg_n, s, got, M, kA);
             if (g0 == 0 && lane == 0) cnt.pairs += got;
             remaining -= got;
@@ -1162,7 +1222,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
           }
           if (L.esub == 0) {
             A.s0[L.j] = make_float4(tk, H.dls - H.gc * H.inv, H.dc0 * H.inv, H.dc1 * H.inv);
-            A.s1[L.j] = make_float4(H.dc2 * H.inv, 0.f, 0.f, 0.f);
+            A.s1[L.j] = H.dc2 * H.inv;
           }
         }
         const float tot_x = __shfl_sync(kFull, incl, GW - 1, GW);
@@ -1177,7 +1237,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
         const unsigned smask = __ballot_sync(kFull, live && L.esub == 0);
         if (lane == 0) cnt.samples += __popc(smask);
         if (BWD) {
-          grad_range<GW>(M, A, 0, n_use);
+          grad_range<GW, BASIS>(M, A, 0, n_use);
           if (more) {
             unsigned long long cur2 = cursor;
             int remaining = K - n_use;
@@ -1187,13 +1247,14 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
               uint32_t pos;
               const int got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
               if ((int)lane < got) {
-                setup_pair<!BWD>(P.S, M, kTrans + (int)lane, R, pos);
+                setup_pair<!BWD, BASIS>(P.S, M, kTrans + (int)lane, R, pos);
                 A.a[kA + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
                 A.b[kA + lane] = make_float2(0.f, 0.f);
+                A.c[kA + lane] = 0.f;
               }
               __syncwarp();
-              grad_range<GW>(M, A, kA, kA + got);
-              scatter_batch(P.S, M, A, kA, got >= 32 ? kFull : ((1u << got) - 1u), R, P.gbuf,
+              grad_range<GW, BASIS>(M, A, kA, kA + got);
+              scatter_batch<BASIS>(P.S, M, A, kA, got >= 32 ? kFull : ((1u << got) - 1u), R, P.gbuf,
                             P.gstride);
               remaining -= got;
               if (got > 0) cur2 = shfl64(key, got - 1);
@@ -1215,9 +1276,9 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
     if (BWD) {
       const unsigned m0 = count >= 32 ? kFull : ((1u << count) - 1u);
       const unsigned m1 = count >= 64 ? kFull : (count > 32 ? ((1u << (count - 32)) - 1u) : 0u);
-      scatter_batch(P.S, M, A, 0, m0, R, P.gbuf, P.gstride);
-      scatter_batch(P.S, M, A, 32, m1, R, P.gbuf, P.gstride);
-      scatter_batch(P.S, M, A, kRet, nret >= 32 ? kFull : ((1u << nret) - 1u), R, P.gbuf,
+      scatter_batch<BASIS>(P.S, M, A, 0, m0, R, P.gbuf, P.gstride);
+      scatter_batch<BASIS>(P.S, M, A, 32, m1, R, P.gbuf, P.gstride);
+      scatter_batch<BASIS>(P.S, M, A, kRet, nret >= 32 ? kFull : ((1u << nret) - 1u), R, P.gbuf,
                     P.gstride);
     } else if (lg != nullptr && lane == 0) {
       lg[0] = log_ok ? lp : -1;
@@ -1373,35 +1434,45 @@ void ray_grid(RenderArgs& A, const rg_rays* rays, const rg_camera* cam, dim3& gr
 }
 
 // dynamic shared memory above the 48 KB default needs a per-kernel opt-in
-template <bool BWD, int GW, bool INSTR>
+template <bool BWD, int GW, bool INSTR, int BASIS>
 void launch_one(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
 #ifdef RG_STATIC_SMEM
   (void)smem;
-  k_render<BWD, GW, INSTR><<<grid, kBlock, 0, st>>>(A);
+  k_render<BWD, GW, INSTR, BASIS><<<grid, kBlock, 0, st>>>(A);
 #else
   static bool opted = false;
   if (!opted) {
-    cudaFuncSetAttribute(k_render<BWD, GW, INSTR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_render<BWD, GW, INSTR, BASIS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     opted = true;
   }
-  k_render<BWD, GW, INSTR><<<grid, kBlock, smem, st>>>(A);
+  k_render<BWD, GW, INSTR, BASIS><<<grid, kBlock, smem, st>>>(A);
 #endif
 }
 
-template <bool BWD, int GW>
+template <bool BWD, int GW, int BASIS>
 void launch_gw(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
-  if (A.stats != nullptr || A.dbg_rec != nullptr) launch_one<BWD, GW, true>(A, grid, smem, st);
-  else launch_one<BWD, GW, false>(A, grid, smem, st);
+  if (A.stats != nullptr || A.dbg_rec != nullptr) launch_one<BWD, GW, true, BASIS>(A, grid, smem, st);
+  else launch_one<BWD, GW, false, BASIS>(A, grid, smem, st);
 }
 
 template <bool BWD>
 void launch_render(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
   const int B = A.c.slab_samples;
-  if (B >= 5) launch_gw<BWD, 8>(A, grid, smem, st);
-  else if (B >= 3) launch_gw<BWD, 4>(A, grid, smem, st);
-  else if (B == 2) launch_gw<BWD, 2>(A, grid, smem, st);
-  else launch_gw<BWD, 1>(A, grid, smem, st);
+  // non-Gaussian bases (NEXT-3) are instantiated for GW = 8 only (B >= 5; the API
+  // rejects them otherwise)
+  if (B >= 5) {
+    switch (A.c.basis) {
+      case 1: launch_gw<BWD, 8, 1>(A, grid, smem, st); break;
+      case 2: launch_gw<BWD, 8, 2>(A, grid, smem, st); break;
+      case 3: launch_gw<BWD, 8, 3>(A, grid, smem, st); break;
+      case 4: launch_gw<BWD, 8, 4>(A, grid, smem, st); break;
+      case 5: launch_gw<BWD, 8, 5>(A, grid, smem, st); break;
+      default: launch_gw<BWD, 8, 0>(A, grid, smem, st);
+    }
+  } else if (B >= 3) launch_gw<BWD, 4, 0>(A, grid, smem, st);
+  else if (B == 2) launch_gw<BWD, 2, 0>(A, grid, smem, st);
+  else launch_gw<BWD, 1, 0>(A, grid, smem, st);
 }
 
 constexpr size_t kSmemFwd = sizeof(WarpMemT<kStkFwd>) * kWarps;

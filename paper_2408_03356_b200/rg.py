@@ -42,7 +42,7 @@ class _Config(C.Structure):
     _fields_ = [("dt", C.c_float), ("slab_samples", C.c_int32), ("sigma_eps", C.c_float),
                 ("t_eps", C.c_float), ("hit_capacity", C.c_int32), ("radius_mode", C.c_int32),
                 ("k_sigma", C.c_float), ("t_near", C.c_float), ("background", C.c_float * 3),
-                ("pad_", C.c_int32)]
+                ("basis", C.c_int32)]
 
 
 class _AdamConfig(C.Structure):
@@ -174,11 +174,13 @@ class Config:
     k_sigma: float = 3.0
     t_near: float = 0.0
     background: tuple = (1.0, 1.0, 1.0)
+    basis: int = 0            # RG_BASIS_*: 0 Gaussian, 1 Bump, 2 Wendland, 3 inverse
+                              # multiquadric, 4 inverse quadratic, 5 C0-Matern
 
     @classmethod
     def of(cls, p) -> "Config":
         return cls(p.dt, p.slab_samples, p.sigma_eps, p.t_eps, p.hit_capacity, p.radius_mode,
-                   p.k_sigma, p.t_near, tuple(p.background))
+                   p.k_sigma, p.t_near, tuple(p.background), getattr(p, "basis", 0))
 
     def struct(self) -> _Config:
         c = _Config()
@@ -187,6 +189,7 @@ class Config:
                                                               self.k_sigma, self.t_near)
         for i in range(3):
             c.background[i] = self.background[i]
+        c.basis = self.basis
         return c
 
 

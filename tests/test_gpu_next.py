@@ -391,3 +391,54 @@ def test_densify_then_render(oracle):
     sc2 = synth.Scene(*[getattr(g2, k).cpu().numpy() for k in rg.GROUPS], sc.sh_degree, sc.sg_count)
     ref = oracle.render(sc2, p, o, d, mode=2)
     assert np.abs(out["rgb"].cpu().numpy() - ref["rgb"]).max() <= PIX_TOL
+
+
+# ---------------------------------------------------------------------------
+# alternative basis functions (NEXT-3)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("basis", [1, 2, 3, 4, 5])
+def test_basis_forward_matches_oracle(oracle, basis):
+    from test_gpu_parity import _fwd_case
+    sc = synth.random_scene(2400 + basis, 250, sh_degree=2, sg_count=2, density_range=(0.3, 3.0),
+                            scale_range=(0.03, 0.1), extent=0.45)
+    p = synth.RenderParams(dt=3e-3, t_eps=1e-4, basis=basis)
+    o, d = synth.random_rays(2401, 1500)
+    rg_, ref, ok = _fwd_case(oracle, sc, p, o, d, debug_rays=300)
+    if ok.all():
+        for k in ("slabs", "evals", "samples"):
+            assert rg_["stats"][k] == ref["counters"][k], k
+
+
+@pytest.mark.parametrize("basis", [1, 2, 3, 4, 5])
+def test_basis_backward_matches_oracle(oracle, basis):
+    sc = synth.random_scene(2500 + basis, 70, sh_degree=1, sg_count=2, density_range=(0.3, 3.0),
+                            scale_range=(0.04, 0.12), extent=0.4)
+    p = synth.RenderParams(dt=4e-3, t_eps=1e-4, basis=basis, background=(1.0, 0.5, 0.0))
+    cfg = rg.Config.of(p)
+    o, d = oracle.camera_rays(synth.orbit_camera(2.2, 20 * basis, 20, 20, 20, 24.0))
+    g = rg.Gaussians.from_scene(sc)
+    b = rg.build_bvh(g, cfg)
+    to, td = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
+    fwd = rg.render_forward(g, b, cfg, rays=(to, td), log=rg.new_log(len(o)))
+    up = np.random.default_rng(basis).normal(size=(len(o), 3)).astype(np.float32)
+    grads = rg.render_backward(g, b, cfg, fwd, torch.from_numpy(up).cuda(), rays=(to, td))
+    torch.cuda.synchronize()
+    ref_f = oracle.render(sc, p, o, d, mode=2)
+    assert np.array_equal(fwd["replay"].cpu().numpy(), ref_f["s_term"])
+    ref = oracle.backward(sc, p, o, d, up.astype(np.float64), mode=2)
+    grad_check(grads, ref)
+
+
+def test_basis_validation():
+    sc = synth.random_scene(2600, 20)
+    g = rg.Gaussians.from_scene(sc)
+    b = rg.build_bvh(g, rg.Config())
+    o, d = synth.random_rays(2601, 8)
+    rays = (torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda())
+    with pytest.raises(rg.RGError, match="not implemented"):
+        rg.render_forward(g, b, rg.Config(basis=4, slab_samples=4), rays=rays)
+    with pytest.raises(rg.RGError, match="invalid"):
+        rg.render_forward(g, b, rg.Config(basis=4, radius_mode=1), rays=rays)
+    with pytest.raises(rg.RGError, match="invalid"):
+        rg.render_forward(g, b, rg.Config(basis=6), rays=rays)
