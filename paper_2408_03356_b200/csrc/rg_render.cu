@@ -510,11 +510,11 @@ __device__ __forceinline__ void eval_range(const WM& M, int e0, int e1, const La
     const float4 a = M.e0[e];
     if (val && a.x <= tk && tk <= a.y) {
       const float4 q = M.e1[e];
-      const float4 e2 = M.e2[e];
-      const float cb = e2.x;
+      const float cb = M.e2[e].x;
+      const float sge = BASIS != 0 ? M.e2[e].w : 0.f;   // sigma~ (non-Gaussian slots)
       const float tau = tk - a.z;
       float qq;
-      const float w = basis_w<BASIS>(tau, a, q, e2.w, qq);
+      const float w = basis_w<BASIS>(tau, a, q, sge, qq);
       s += w;
       r = fmaf(w, q.z, r);
       g = fmaf(w, q.w, g);
@@ -539,8 +539,8 @@ __device__ __forceinline__ void grad_range(const WM& M, WarpAcc& A, int e0, int 
     if (e < e1) {
       const float4 a = M.e0[e];
       const float4 q = M.e1[e];
-      const float4 e2 = M.e2[e];
-      const float cb = e2.x;
+      const float cb = M.e2[e].x;
+      const float sge = BASIS != 0 ? M.e2[e].w : 0.f;   // sigma~ (non-Gaussian slots)
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f;
 #pragma unroll
       for (int j = 0; j < GW; ++j) {
@@ -550,9 +550,9 @@ __device__ __forceinline__ void grad_range(const WM& M, WarpAcc& A, int e0, int 
           const float b2 = A.s1[j];
           const float tau = tk - a.z;
           float qq;
-          const float w = basis_w<BASIS>(tau, a, q, e2.w, qq);
+          const float w = basis_w<BASIS>(tau, a, q, sge, qq);
           const float dldw = fmaf(s0.z, q.z, fmaf(s0.w, q.w, fmaf(b2, cb, s0.y)));
-          const float wd = basis_psi<BASIS>(w, qq, e2.w) * dldw;
+          const float wd = basis_psi<BASIS>(w, qq, sge) * dldw;
           a0 += wd;
           a1 = fmaf(wd, tau, a1);
           a2 = fmaf(wd * tau, tau, a2);
@@ -960,11 +960,11 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             const float4 a = M.e0[e];
             if (val && a.x <= tk && tk <= a.y) {
               const float4 q = M.e1[e];
-              const float4 e2 = M.e2[e];
-              const float cbv = e2.x;
+              const float cbv = M.e2[e].x;
+              const float sge = BASIS != 0 ? M.e2[e].w : 0.f;
               const float tau_ = tk - a.z;
               float qq;
-              const float w = basis_w<BASIS>(tau_, a, q, e2.w, qq);
+              const float w = basis_w<BASIS>(tau_, a, q, sge, qq);
               sg += w;
               sr = fmaf(w, q.z, sr);
               sgg = fmaf(w, q.w, sgg);
@@ -1066,8 +1066,8 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
               if (e < n3) {
                 a = M.e0[e];
                 const float4 q = M.e1[e];
-                const float4 e2 = M.e2[e];
-                const float cbv = e2.x;
+                const float cbv = M.e2[e].x;
+                const float sge = BASIS != 0 ? M.e2[e].w : 0.f;
                 const float kf = (float)k0 + 0.5f;
                 int kl = (int)floorf((a.x - t0) / c.dt - kf) - 1;
                 int kh = (int)ceilf((a.y - t0) / c.dt - kf) + 1;
@@ -1081,9 +1081,9 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
                     const float b2 = A.s1[k];
                     const float tau_ = tkk - a.z;
                     float qq;
-                    const float w = basis_w<BASIS>(tau_, a, q, e2.w, qq);
+                    const float w = basis_w<BASIS>(tau_, a, q, sge, qq);
                     const float dldw = fmaf(s0.z, q.z, fmaf(s0.w, q.w, fmaf(b2, cbv, s0.y)));
-                    const float wd = basis_psi<BASIS>(w, qq, e2.w) * dldw;
+                    const float wd = basis_psi<BASIS>(w, qq, sge) * dldw;
                     a0 += wd;
                     a1 = fmaf(wd, tau_, a1);
                     a2 = fmaf(wd * tau_, tau_, a2);
