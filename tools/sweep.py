@@ -46,6 +46,13 @@ def main():
         ms = fwd_ms(g, cfg, cam)
         rows["sigma_eps"].append({"sigma_eps": se, "fwd_ms": ms, "fps": 1e3 / ms,
                                   "paper_fps_rtx4090": fps})
+    rows["basis"] = []
+    for b, name in enumerate(("gaussian", "bump", "wendland", "inv_multiquadric", "inv_quadratic",
+                              "matern_c0")):
+        cfg = rg.Config.of(p)
+        cfg.basis = b
+        ms = fwd_ms(g, cfg, cam)
+        rows["basis"].append({"basis": name, "fwd_ms": ms, "fps": 1e3 / ms})
     out = {"workload": "C1 800x800 view, 300k Gaussians SH3+7SG (synthetic)", **rows}
     txt = json.dumps(out, indent=1)
     print(txt)
