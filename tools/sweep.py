@@ -46,9 +46,12 @@ def main():
         ms = fwd_ms(g, cfg, cam)
         rows["sigma_eps"].append({"sigma_eps": se, "fwd_ms": ms, "fps": 1e3 / ms,
                                   "paper_fps_rtx4090": fps})
-    rows["basis"] = []
-    for b, name in enumerate(("gaussian", "bump", "wendland", "inv_multiquadric", "inv_quadratic",
-                              "matern_c0")):
+    # bases: the inverse multiquadric / quadratic supports grow like sigma~/sigma_eps
+    # (P:529-539): with C1's densities (20..2000) every primitive spans the scene, so
+    # they are not measured on this workload
+    rows["basis"] = [{"basis": "inv_multiquadric", "skipped": "support radius sqrt((s/se)^2-1) >> scene"},
+                     {"basis": "inv_quadratic", "skipped": "support radius sqrt(s/se-1) >> scene"}]
+    for b, name in ((0, "gaussian"), (1, "bump"), (2, "wendland"), (5, "matern_c0")):
         cfg = rg.Config.of(p)
         cfg.basis = b
         ms = fwd_ms(g, cfg, cam)
