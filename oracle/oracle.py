@@ -61,7 +61,7 @@ def lib():
         _lib.og_build.restype = P
         _lib.og_build.argtypes = [P, P]
         _lib.og_free.argtypes = [P]
-        _lib.og_bvh_views.argtypes = [P] + [P] * 10
+        _lib.og_bvh_views.argtypes = [P] + [P] * 11
         _lib.og_render.restype = C.c_int32
         _lib.og_render.argtypes = [P, P, P, C.c_int32, P, C.c_int32, P, P, P, P, P, P, P,
                                    C.c_int32, P, P]
@@ -71,8 +71,8 @@ def lib():
         _lib.og_isect.restype = C.c_int32
         _lib.og_isect.argtypes = [P, C.c_float, P, P, P, P, P]
         _lib.og_rotation_f32.argtypes = [P, P]
-        _lib.og_morton.argtypes = [P, P, P, P, P]
-        _lib.og_sort.argtypes = [C.c_int32, P, P, P]
+        _lib.og_morton.argtypes = [P, P, P, P, P, P]
+        _lib.og_sort.argtypes = [C.c_int32, P, P, P, P]
         _lib.og_camera_rays.argtypes = [C.c_int32, C.c_int32, C.c_float, C.c_float, C.c_float,
                                         C.c_float, P, C.c_int32, C.c_int32, C.c_int32,
                                         C.c_int32, P, P]
@@ -206,7 +206,7 @@ class BVH:
         self._cfg = config(params)
         self.n = scene.n
         self.h = lib().og_build(self._sr.ptr, C.byref(self._cfg))
-        ptrs = [C.c_void_p() for _ in range(10)]
+        ptrs = [C.c_void_p() for _ in range(11)]
         lib().og_bvh_views(self.h, *[C.byref(p) for p in ptrs])
         n = self.n
 
@@ -225,6 +225,7 @@ class BVH:
         self.root = view(ptrs[7], 6, np.float32)
         self.mean_lo = view(ptrs[8], 3, np.float32)
         self.mean_hi = view(ptrs[9], 3, np.float32)
+        self.fine = view(ptrs[10], n, np.uint32)
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -178,8 +178,8 @@ int32_t og_isect(const float M[9], float r2, const float mu[3], const float o[3]
 /* ------------------------------------------------------------------------ */
 /* ARITH-6  30-bit Morton codes of the means (north star; L18)               */
 /* ------------------------------------------------------------------------ */
-void og_morton(const og_gaussians* g, const og_config* c, uint32_t* codes, float lo[3],
-               float hi[3]) {
+void og_morton(const og_gaussians* g, const og_config* c, uint32_t* codes, uint32_t* fine,
+               float lo[3], float hi[3]) {
   const int n = g->n;
   int* valid = (int*)malloc(sizeof(int) * (n > 0 ? n : 1));
   for (int a = 0; a < 3; ++a) { lo[a] = INFINITY; hi[a] = -INFINITY; }
@@ -196,8 +196,8 @@ void og_morton(const og_gaussians* g, const og_config* c, uint32_t* codes, float
     }
   }
   for (int i = 0; i < n; ++i) {
-    if (!valid[i]) { codes[i] = 0xFFFFFFFFu; continue; }
-    uint32_t qv[3];
+    if (!valid[i]) { codes[i] = 0xFFFFFFFFu; fine[i] = 0u; continue; }
+    uint32_t qv[3], fv[3];
     for (int a = 0; a < 3; ++a) {
       const float ext = hi[a] - lo[a];
       float u = 0.0f;
@@ -207,7 +207,18 @@ void og_morton(const og_gaussians* g, const og_config* c, uint32_t* codes, float
       if (qi < 0) qi = 0;
       if (qi > 1023) qi = 1023;
       qv[a] = (uint32_t)qi;
+      int fi = (int)floorf(u * 131072.0f);          /* 2^17: 7 more bits (exact scaling) */
+      if (fi < 0) fi = 0;
+      if (fi > 131071) fi = 131071;
+      fv[a] = (uint32_t)fi & 127u;
     }
+    uint32_t fc = 0;
+    for (int b = 0; b < 7; ++b) {
+      fc |= ((fv[0] >> b) & 1u) << (3 * b + 2);
+      fc |= ((fv[1] >> b) & 1u) << (3 * b + 1);
+      fc |= ((fv[2] >> b) & 1u) << (3 * b + 0);
+    }
+    fine[i] = fc;
     uint32_t code = 0;
     for (int b = 0; b < 10; ++b) {   /* x takes the top bit of each triplet */
       code |= ((qv[0] >> b) & 1u) << (3 * b + 2);
@@ -219,23 +230,29 @@ void og_morton(const og_gaussians* g, const og_config* c, uint32_t* codes, float
   free(valid);
 }
 
-/* stable merge sort of indices by code (O3: "std::stable_sort on codes") */
-static void msort(uint32_t* idx, uint32_t* tmp, const uint32_t* codes, int lo, int hi) {
+/* stable merge sort of indices by (code, fine) (O3: "std::stable_sort on codes") */
+static uint64_t sort_key(const uint32_t* codes, const uint32_t* fine, uint32_t i) {
+  return ((uint64_t)codes[i] << 32) | fine[i];
+}
+static void msort(uint32_t* idx, uint32_t* tmp, const uint32_t* codes, const uint32_t* fine, int lo,
+                  int hi) {
   if (hi - lo < 2) return;
   const int mid = lo + (hi - lo) / 2;
-  msort(idx, tmp, codes, lo, mid);
-  msort(idx, tmp, codes, mid, hi);
+  msort(idx, tmp, codes, fine, lo, mid);
+  msort(idx, tmp, codes, fine, mid, hi);
   int i = lo, j = mid, k = lo;
-  while (i < mid && j < hi) tmp[k++] = (codes[idx[j]] < codes[idx[i]]) ? idx[j++] : idx[i++];
+  while (i < mid && j < hi)
+    tmp[k++] = (sort_key(codes, fine, idx[j]) < sort_key(codes, fine, idx[i])) ? idx[j++] : idx[i++];
   while (i < mid) tmp[k++] = idx[i++];
   while (j < hi) tmp[k++] = idx[j++];
   memcpy(idx + lo, tmp + lo, sizeof(uint32_t) * (hi - lo));
 }
 
-void og_sort(int32_t n, const uint32_t* codes, uint32_t* order, uint32_t* sorted) {
+void og_sort(int32_t n, const uint32_t* codes, const uint32_t* fine, uint32_t* order,
+             uint32_t* sorted) {
   uint32_t* tmp = (uint32_t*)malloc(sizeof(uint32_t) * (n > 0 ? n : 1));
   for (int i = 0; i < n; ++i) order[i] = (uint32_t)i;
-  msort(order, tmp, codes, 0, n);
+  msort(order, tmp, codes, fine, 0, n);
   for (int i = 0; i < n; ++i) sorted[i] = codes[order[i]];
   free(tmp);
 }
@@ -373,7 +390,7 @@ int32_t og_clip(const float box[6], const float o[3], const float d[3], float t_
 /* ------------------------------------------------------------------------ */
 struct og_bvh {
   int32_t n;
-  uint32_t *codes, *sorted, *order;
+  uint32_t *codes, *sorted, *order, *fine;
   int32_t *left, *right;
   float *leaf_boxes, *node_boxes;
   float root[6], mean_lo[3], mean_hi[3];
@@ -385,14 +402,15 @@ og_bvh* og_build(const og_gaussians* g, const og_config* c) {
   const size_t n1 = n > 0 ? (size_t)n : 1;
   b->n = n;
   b->codes = (uint32_t*)malloc(4 * n1);
+  b->fine = (uint32_t*)malloc(4 * n1);
   b->sorted = (uint32_t*)malloc(4 * n1);
   b->order = (uint32_t*)malloc(4 * n1);
   b->left = (int32_t*)malloc(4 * n1);
   b->right = (int32_t*)malloc(4 * n1);
   b->leaf_boxes = (float*)malloc(24 * n1);
   b->node_boxes = (float*)malloc(24 * n1);
-  og_morton(g, c, b->codes, b->mean_lo, b->mean_hi);
-  og_sort(n, b->codes, b->order, b->sorted);
+  og_morton(g, c, b->codes, b->fine, b->mean_lo, b->mean_hi);
+  og_sort(n, b->codes, b->fine, b->order, b->sorted);
   og_karras(n, b->sorted, b->left, b->right);
   for (int p = 0; p < n; ++p) {
     float M[9], r2;
@@ -405,14 +423,15 @@ og_bvh* og_build(const og_gaussians* g, const og_config* c) {
 
 void og_free(og_bvh* b) {
   if (!b) return;
-  free(b->codes); free(b->sorted); free(b->order); free(b->left); free(b->right);
+  free(b->codes); free(b->fine); free(b->sorted); free(b->order); free(b->left); free(b->right);
   free(b->leaf_boxes); free(b->node_boxes); free(b);
 }
 
 void og_bvh_views(const og_bvh* b, const uint32_t** codes_unsorted, const uint32_t** sorted_codes,
                   const uint32_t** order, const int32_t** left, const int32_t** right,
                   const float** leaf_boxes_sorted, const float** node_boxes, const float** root,
-                  const float** mean_lo, const float** mean_hi) {
+                  const float** mean_lo, const float** mean_hi, const uint32_t** fine) {
+  if (fine) *fine = b->fine;
   if (codes_unsorted) *codes_unsorted = b->codes;
   if (sorted_codes) *sorted_codes = b->sorted;
   if (order) *order = b->order;

@@ -69,11 +69,14 @@ void og_prim_setup(const og_gaussians* g, const og_config* c, int32_t i,
 /* segment/ellipsoid support interval; returns 1 on hit and writes te, tx */
 int32_t og_isect(const float M[9], float r2, const float mu[3], const float o[3],
                  const float d[3], float* te, float* tx);
-/* Morton codes of the means (ARITH-6); codes of invalid Gaussians = 0xFFFFFFFF */
-void og_morton(const og_gaussians* g, const og_config* c, uint32_t* codes,
+/* Morton codes of the means (ARITH-6); codes of invalid Gaussians = 0xFFFFFFFF.
+   fine: the next 7 bits per axis (floor(u 2^17) & 127) interleaved into 21 bits, the
+   sort's tie-break inside an equal-code run (L34; 0 for invalid) */
+void og_morton(const og_gaussians* g, const og_config* c, uint32_t* codes, uint32_t* fine,
                float lo[3], float hi[3]);
-/* stable sort of codes -> order[pos] = original index; sorted codes out */
-void og_sort(int32_t n, const uint32_t* codes, uint32_t* order, uint32_t* sorted);
+/* stable sort by (code, fine) -> order[pos] = original index; sorted codes out */
+void og_sort(int32_t n, const uint32_t* codes, const uint32_t* fine, uint32_t* order,
+             uint32_t* sorted);
 /* Karras hierarchy (recursive top-down definition); children: >=0 internal,
    <0 leaf ~pos.  left/right have n-1 entries. */
 void og_karras(int32_t n, const uint32_t* sorted_codes, int32_t* left, int32_t* right);
@@ -107,7 +110,7 @@ void og_free(og_bvh* b);
 void og_bvh_views(const og_bvh* b, const uint32_t** codes_unsorted, const uint32_t** sorted_codes,
                   const uint32_t** order, const int32_t** left, const int32_t** right,
                   const float** leaf_boxes_sorted, const float** node_boxes, const float** root,
-                  const float** mean_lo, const float** mean_hi);
+                  const float** mean_lo, const float** mean_hi, const uint32_t** fine);
 
 /* ---- forward / backward (fp64 values) --------------------------------- */
 /* mode 0: plain per-sample definition: every active Gaussian tested at every

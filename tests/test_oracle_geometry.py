@@ -222,6 +222,11 @@ def test_morton_hand_values(oracle):
         qv = np.clip(np.floor(u * np.float32(1024)), 0, 1023).astype(int)
         code = (_morton_magic(qv[0]) << 2) | (_morton_magic(qv[1]) << 1) | _morton_magic(qv[2])
         assert code == b.codes[i]
+        # the tie-break code (L34): the next 7 bits of each axis, same interleave
+        q17 = np.clip(np.floor(u * np.float32(131072)), 0, 131071).astype(int)
+        assert np.array_equal(q17 >> 7, qv)
+        fv = q17 & 127
+        assert b.fine[i] == (_morton_magic(fv[0]) << 2) | (_morton_magic(fv[1]) << 1) | _morton_magic(fv[2])
 
 
 def test_sort_and_karras_structure(oracle):
@@ -232,7 +237,8 @@ def test_sort_and_karras_structure(oracle):
         if n == 3000:   # duplicate codes exercise the index tie-break
             sc.mean[1000:1200] = sc.mean[0]
         b = oracle.BVH(sc, synth.RenderParams())
-        assert np.array_equal(b.order, np.argsort(b.codes, kind="stable"))
+        # stable sort by (code, fine code, index) (L34), via numpy's lexsort
+        assert np.array_equal(b.order, np.lexsort((np.arange(n), b.fine, b.codes)))
         assert np.array_equal(b.sorted_codes, b.codes[b.order])
         keys = [(int(c) << 32) | i for i, c in enumerate(b.sorted_codes)]
         seen_leaf = np.zeros(n, int); seen_int = np.zeros(max(n - 1, 1), int)
