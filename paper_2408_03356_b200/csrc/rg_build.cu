@@ -145,9 +145,9 @@ __global__ void __launch_bounds__(kThreads) k_morton(rg_gaussians g, const int* 
                                                      uint32_t* keys, uint32_t* vals) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.n) return;
-  uint32_t code = 0xFFFFFFFFu;
+  uint32_t code = 0xFFFFFFFFu, fine = 0u;
   if (flags[i] & 1) {
-    uint32_t q[3];
+    uint32_t q[3], f[3];
     for (int a = 0; a < 3; ++a) {                               // ARITH-6
       const float lo = ord_dec(bounds[a]), hi = ord_dec(bounds[3 + a]);
       const float ext = sub_(hi, lo);
@@ -157,12 +157,26 @@ __global__ void __launch_bounds__(kThreads) k_morton(rg_gaussians g, const int* 
       int qi = (int)floorf(v);
       qi = qi < 0 ? 0 : (qi > 1023 ? 1023 : qi);
       q[a] = (uint32_t)qi;
+      int fi = (int)floorf(mul_(u, 131072.0f));                 // L34: 7 more bits per axis
+      fi = fi < 0 ? 0 : (fi > 131071 ? 131071 : fi);
+      f[a] = (uint32_t)fi & 127u;
     }
     code = (spread10(q[0]) << 2) | (spread10(q[1]) << 1) | spread10(q[2]);
+    fine = (spread10(f[0]) << 2) | (spread10(f[1]) << 1) | spread10(f[2]);
   }
   codes[i] = code;
-  keys[i] = code;
+  keys[i] = fine;            // the first (tie-break) sort runs on the fine code
   vals[i] = (uint32_t)i;
+}
+
+// keys of the second (primary) sort: the 30-bit codes in the fine-sorted order
+__global__ void __launch_bounds__(kThreads) k_gather_codes(const uint32_t* codes, const uint32_t* vin,
+                                                           uint32_t* kout, uint32_t* vout, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const uint32_t v = vin[j];
+  kout[j] = codes[v];
+  vout[j] = v;
 }
 
 // --- radix sort -----------------------------------------------------------
@@ -575,7 +589,7 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
   k_init<<<1, 32, 0, st>>>(bounds, root_box);
   count_launches(1);
   if (n == 0) return cudaGetLastError();
-  count_launches(n > 1 ? 18 : 17);
+  count_launches(n > 1 ? 28 : 27);
   const int blocks = (n + kThreads - 1) / kThreads;
   float* box_orig = reinterpret_cast<float*>(ws + L.box_orig);
   int* flags = reinterpret_cast<int*>(ws + L.flags);
@@ -587,15 +601,24 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
   k_morton<<<blocks, kThreads, 0, st>>>(g, flags, bounds,
                                         reinterpret_cast<uint32_t*>(ws + L.codes), ka, va);
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);
-  for (int pass = 0; pass < 4; ++pass) {
-    const int shift = 8 * pass;
-    uint32_t *ki = (pass & 1) ? kb : ka, *vi = (pass & 1) ? vb : va;
-    uint32_t *ko = (pass & 1) ? ka : kb, *vo = (pass & 1) ? va : vb;
+  auto radix_pass = [&](const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo,
+                        int shift) {
     k_radix_hist<<<L.tiles, kThreads, 0, st>>>(ki, n, shift, hist, L.tiles);
     k_radix_scan<<<1, 1024, 0, st>>>(hist, 256 * L.tiles);
     k_radix_scatter<<<L.tiles, kThreads, 0, st>>>(ki, vi, ko, vo, n, shift, hist, L.tiles);
+  };
+  // stable LSD sort by (code, fine code, index) (L34): first the 21-bit fine code
+  // (3 passes, ending in kb/vb), then the 30-bit code (4 passes, ending in ka/va)
+  radix_pass(ka, va, kb, vb, 0);
+  radix_pass(kb, vb, ka, va, 8);
+  radix_pass(ka, va, kb, vb, 16);
+  k_gather_codes<<<blocks, kThreads, 0, st>>>(reinterpret_cast<const uint32_t*>(ws + L.codes), vb,
+                                              ka, va, n);
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 8 * pass;
+    if (pass & 1) radix_pass(kb, vb, ka, va, shift);
+    else radix_pass(ka, va, kb, vb, shift);
   }
-  // after 4 passes the sorted keys / order are back in ka / va
   float4* geom = reinterpret_cast<float4*>(ws + L.geom);
   float* app = reinterpret_cast<float*>(ws + L.app);
   float* leaf_box = reinterpret_cast<float*>(ws + L.leaf_box);
