@@ -540,6 +540,115 @@ __global__ void __launch_bounds__(128) k_wide_refit(const float4* nodes, const f
   }
 }
 
+// Warp-per-item variant of the collapse: lane k holds candidate entry k (id, box,
+// area) in registers; each round opens, in parallel, the largest-area internal
+// entries that still fit (left child in place, right child appended), so a
+// wide node takes a few rounds of parallel loads instead of up to 30 serial
+// ones.  Same queue protocol as above (one item per warp, bulk reservations).
+__global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, WideNode* wide, int2* q,
+                                                       int* wide_src, int* counts) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  volatile int* vc = counts;
+  volatile long long* vq = reinterpret_cast<volatile long long*>(q);
+  while (true) {
+    long long raw = -1;
+    int have = 0;
+    if (lane == 0) {
+      const int it = atomicAdd(counts + 1, 1);
+      while (true) {
+        const int done = vc[2];
+        __threadfence();
+        const int res = vc[4];
+        if (it < res) {
+          raw = vq[it];
+          if ((int)(raw & 0xFFFFFFFF) != -1) { have = 1; break; }
+        } else if (done == res) {
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+    have = __shfl_sync(full, have, 0);
+    if (!have) return;
+    raw = __shfl_sync(full, raw, 0);
+    const int jb = (int)(raw & 0xFFFFFFFF), jw = (int)(raw >> 32);
+    // entries 0, 1: the binary node's children
+    int id = -1;
+    float b[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    if (lane < 2) {
+      const float* w = reinterpret_cast<const float*>(nodes + 4 * (size_t)jb);
+      const int4 c = *reinterpret_cast<const int4*>(nodes + 4 * (size_t)jb + 3);
+      id = lane == 0 ? c.x : c.y;
+      for (int k = 0; k < 6; ++k) b[k] = w[6 * lane + k];
+    }
+    int m = 2;
+    while (m < kWide) {
+      const bool internal = lane < m && id >= 0;
+      const unsigned cm = __ballot_sync(full, internal);
+      if (!cm) break;
+      const float area = internal ? box_area(b) : -2.f;
+      int rank = 0;                                   // by area, descending (ties: lane)
+      for (unsigned mm = cm; mm; mm &= mm - 1) {
+        const int o = __ffs(mm) - 1;
+        const float ao = __shfl_sync(full, area, o);
+        rank += (ao > area) || (ao == area && o < lane);
+      }
+      const int r = min(__popc(cm), kWide - m);
+      const bool open = internal && rank < r;
+      int rid = -1;
+      float rb[6];
+      if (open) {                                     // left child in place, right one out
+        const float* w = reinterpret_cast<const float*>(nodes + 4 * (size_t)id);
+        const int4 c = *reinterpret_cast<const int4*>(nodes + 4 * (size_t)id + 3);
+        id = c.x;
+        rid = c.y;
+        for (int k = 0; k < 6; ++k) { b[k] = w[k]; rb[k] = w[6 + k]; }
+      }
+      const unsigned om = __ballot_sync(full, open);
+      for (int j = 0; j < r; ++j) {                   // right child of rank j -> lane m + j
+        const int src = __ffs(__ballot_sync(full, open && rank == j)) - 1;
+        const int vid = __shfl_sync(full, rid, src);
+        float vb[6];
+        for (int k = 0; k < 6; ++k) vb[k] = __shfl_sync(full, open ? rb[k] : 0.f, src);
+        if (lane == m + j) {
+          id = vid;
+          for (int k = 0; k < 6; ++k) b[k] = vb[k];
+        }
+      }
+      (void)om;
+      m += r;
+    }
+    // write the wide node; internal children become queue items
+    const bool live = lane < m;
+    const bool internal = live && id >= 0;
+    const unsigned im = __ballot_sync(full, internal);
+    const int nint = __popc(im);
+    int wid0 = 0, qs0 = 0;
+    if (lane == 0 && nint) {
+      wid0 = atomicAdd(counts + 0, nint);
+      qs0 = atomicAdd(counts + 4, nint);              // reserve the queue slots
+    }
+    wid0 = __shfl_sync(full, wid0, 0);
+    qs0 = __shfl_sync(full, qs0, 0);
+    int child = live ? id : kWideEmpty;
+    if (internal) {
+      const int rk = __popc(im & ((1u << lane) - 1u));
+      const int wid = wid0 + rk;
+      wide_src[wid] = id;
+      vq[qs0 + rk] = ((long long)wid << 32) | (unsigned)id;   // publish with one store
+      child = wid;
+    }
+    WideNode& W = wide[jw];
+    W.lox[lane] = b[0]; W.loy[lane] = b[1]; W.loz[lane] = b[2];
+    W.hix[lane] = b[3]; W.hiy[lane] = b[4]; W.hiz[lane] = b[5];
+    W.child[lane] = child;
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicAdd(counts + 2, 1);          // this item is done
+  }
+}
+
 // error flag: unfinished items or wide-node capacity exceeded
 __global__ void k_collapse_check(int* counts, int capacity) {
   counts[3] = (counts[2] != counts[4] || counts[0] > capacity) ? 1 : 0;
@@ -652,7 +761,11 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // all blocks co-resident (waiting threads spin): 2 blocks of 128 per SM
+#ifdef RG_COLLAPSE_THREAD
     k_collapse_persistent<<<2 * sms, 128, 0, st>>>(nodes, wide, qa, wsrc, wc);
+#else
+    k_collapse_warp<<<4 * sms, 128, 0, st>>>(nodes, wide, qa, wsrc, wc);
+#endif
     k_collapse_check<<<1, 1, 0, st>>>(wc, (int)wide_capacity(n));
     count_launches(2);
   }
