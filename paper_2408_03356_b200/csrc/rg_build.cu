@@ -416,8 +416,13 @@ __global__ void k_collapse_init(int n, const float* leaf_box, WideNode* wide, in
     }
   }
   if (n == 1) {
-    const float empty[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
-    wide_set(wide[0], l, l == 0 ? leaf_box : empty, l == 0 ? ~0 : kWideEmpty);
+    wide[0].lox[l] = l == 0 ? leaf_box[0] : INFINITY;
+    wide[0].loy[l] = l == 0 ? leaf_box[1] : INFINITY;
+    wide[0].loz[l] = l == 0 ? leaf_box[2] : INFINITY;
+    wide[0].hix[l] = l == 0 ? leaf_box[3] : -INFINITY;
+    wide[0].hiy[l] = l == 0 ? leaf_box[4] : -INFINITY;
+    wide[0].hiz[l] = l == 0 ? leaf_box[5] : -INFINITY;
+    wide[0].child[l] = l == 0 ? ~0 : kWideEmpty;
   }
 }
 
@@ -493,10 +498,13 @@ __global__ void __launch_bounds__(128) k_collapse_persistent(const float4* nodes
           vq[qs] = ((long long)wid << 32) | (unsigned)child;     // publish with one store
           child = wid;
         }
-        wide_set(W, k, bx[k], child);
+        W.lox[k] = bx[k][0]; W.loy[k] = bx[k][1]; W.loz[k] = bx[k][2];
+        W.hix[k] = bx[k][3]; W.hiy[k] = bx[k][4]; W.hiz[k] = bx[k][5];
+        W.child[k] = child;
       } else {
-        const float empty[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        wide_set(W, k, empty, kWideEmpty);
+        W.lox[k] = W.loy[k] = W.loz[k] = INFINITY;
+        W.hix[k] = W.hiy[k] = W.hiz[k] = -INFINITY;
+        W.child[k] = kWideEmpty;
       }
     }
     __threadfence();
@@ -515,7 +523,7 @@ __global__ void __launch_bounds__(128) k_wide_refit(const float4* nodes, const f
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nw;
        w += (gridDim.x * blockDim.x) >> 5) {
     WideNode& W = wide[w];
-    const int child = W.e[lane].child;
+    const int child = W.child[lane];
     if (child == kWideEmpty) continue;
     float b[6];
     if (child < 0) {
@@ -527,7 +535,8 @@ __global__ void __launch_bounds__(128) k_wide_refit(const float4* nodes, const f
         b[3 + k] = fmaxf(x[3 + k], x[9 + k]);
       }
     }
-    wide_set(W, lane, b, child);
+    W.lox[lane] = b[0]; W.loy[lane] = b[1]; W.loz[lane] = b[2];
+    W.hix[lane] = b[3]; W.hiy[lane] = b[4]; W.hiz[lane] = b[5];
   }
 }
 
@@ -635,7 +644,10 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
       vq[qs0 + rk] = ((long long)wid << 32) | (unsigned)id;   // publish with one store
       child = wid;
     }
-    wide_set(wide[jw], lane, b, child);
+    WideNode& W = wide[jw];
+    W.lox[lane] = b[0]; W.loy[lane] = b[1]; W.loz[lane] = b[2];
+    W.hix[lane] = b[3]; W.hiy[lane] = b[4]; W.hiz[lane] = b[5];
+    W.child[lane] = child;
     __threadfence();
     __syncwarp();
     if (lane == 0) atomicAdd(counts + 2, 1);          // this item is done

@@ -7,7 +7,6 @@
 // (oracle/rg_oracle.c; no code is shared).
 #pragma once
 
-#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -58,34 +57,10 @@ __host__ __device__ inline int grad_stride(int deg, int lobes) {
 // kWideEmpty: unused slot (its box is empty).
 constexpr int kWide = 32;
 constexpr int kWideEmpty = 0x7FFFFFFF;
-// 32-wide node: per child one 16-B entry (one LDG.128 per lane in the traversal):
-// the child box in fp16 rounded OUTWARD (lo toward -inf, hi toward +inf: the box
-// only grows, traversal stays conservative and results exact) and the child id.
-struct WideEntry {
-  unsigned int lxy, lzhx, hyz;   // half2 (lo.x, lo.y), (lo.z, hi.x), (hi.y, hi.z)
-  int child;
-};
 struct WideNode {
-  WideEntry e[kWide];
+  float lox[kWide], loy[kWide], loz[kWide], hix[kWide], hiy[kWide], hiz[kWide];
+  int child[kWide];
 };
-__device__ __forceinline__ unsigned h2u(__half a, __half b) {
-  return (unsigned)__half_as_ushort(a) | ((unsigned)__half_as_ushort(b) << 16);
-}
-__device__ __forceinline__ void wide_set(WideNode& W, int k, const float* b, int child) {
-  const unsigned p0 = h2u(__float2half_rd(b[0]), __float2half_rd(b[1]));
-  const unsigned p1 = h2u(__float2half_rd(b[2]), __float2half_ru(b[3]));
-  const unsigned p2 = h2u(__float2half_ru(b[4]), __float2half_ru(b[5]));
-  *reinterpret_cast<int4*>(&W.e[k]) = make_int4((int)p0, (int)p1, (int)p2, child);
-}
-__device__ __forceinline__ float h_lo(unsigned u) { return __half2float(__ushort_as_half((unsigned short)(u & 0xFFFFu))); }
-__device__ __forceinline__ float h_hi(unsigned u) { return __half2float(__ushort_as_half((unsigned short)(u >> 16))); }
-__device__ __forceinline__ int wide_get(const WideNode& W, int k, float b[6]) {
-  const int4 v = __ldg(reinterpret_cast<const int4*>(&W.e[k]));
-  b[0] = h_lo((unsigned)v.x); b[1] = h_hi((unsigned)v.x);
-  b[2] = h_lo((unsigned)v.y); b[3] = h_hi((unsigned)v.y);
-  b[4] = h_lo((unsigned)v.z); b[5] = h_hi((unsigned)v.z);
-  return v.w;
-}
 __host__ __device__ constexpr size_t wide_capacity(int n) { return (size_t)(n / 2 + 2); }
 
 struct SceneView {

@@ -290,12 +290,16 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
     const bool two = nodeB >= 0;
     const WideNode& WA = S.wide[nodeA];
     const WideNode& WB = S.wide[two ? nodeB : nodeA];
-    float ba[6], bb[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    const int childA = wide_get(WA, lane, ba);
+    const int childA = __ldg(&WA.child[lane]);
+    const float alx = __ldg(&WA.lox[lane]), aly = __ldg(&WA.loy[lane]), alz = __ldg(&WA.loz[lane]);
+    const float ahx = __ldg(&WA.hix[lane]), ahy = __ldg(&WA.hiy[lane]), ahz = __ldg(&WA.hiz[lane]);
     int childB = kWideEmpty;
-    if (two) childB = wide_get(WB, lane, bb);
-    const float alx = ba[0], aly = ba[1], alz = ba[2], ahx = ba[3], ahy = ba[4], ahz = ba[5];
-    const float blx = bb[0], bly = bb[1], blz = bb[2], bhx = bb[3], bhy = bb[4], bhz = bb[5];
+    float blx = 0.f, bly = 0.f, blz = 0.f, bhx = 0.f, bhy = 0.f, bhz = 0.f;
+    if (two) {
+      childB = __ldg(&WB.child[lane]);
+      blx = __ldg(&WB.lox[lane]); bly = __ldg(&WB.loy[lane]); blz = __ldg(&WB.loz[lane]);
+      bhx = __ldg(&WB.hix[lane]); bhy = __ldg(&WB.hiy[lane]); bhz = __ldg(&WB.hiz[lane]);
+    }
     float tnA, tfA, tnB, tfB;
     box_t(alx, aly, alz, ahx, ahy, ahz, R.inv, R.oinv, tnA, tfA);
     box_t(blx, bly, blz, bhx, bhy, bhz, R.inv, R.oinv, tnB, tfB);

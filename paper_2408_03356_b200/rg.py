@@ -267,16 +267,12 @@ class BVH:
         )
 
     def wide_nodes(self):
-        """decoded 32-wide nodes: boxes [count, 6, 32] (fp32 values of the stored fp16,
-        lo x,y,z, hi x,y,z) and child ids [count, 32]; entries are 16 B (3 half2 +
-        int32), see rg_internal.cuh WideEntry"""
+        """[count, 7, 32] view of the 32-wide nodes (6 box planes + child ids)."""
         info = self.debug_views()["wide_info"].cpu()
         cnt = int(info[0])
         base = self.h.wide - self.ws.data_ptr()
-        raw = self.ws.view(torch.uint8)[base:base + cnt * 512].cpu()
-        words = raw.view(torch.int32).reshape(cnt, 32, 4)
-        halves = raw.view(torch.float16).reshape(cnt, 32, 8)[:, :, :6].float()
-        return halves.permute(0, 2, 1).contiguous(), words[:, :, 3].contiguous()
+        raw = self.ws.view(torch.uint8)[base:base + cnt * 896]
+        return raw.view(torch.float32).reshape(cnt, 7, 32), raw.view(torch.int32).reshape(cnt, 7, 32)
 
 
 def bvh_workspace(scene: Gaussians):

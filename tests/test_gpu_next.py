@@ -37,22 +37,21 @@ def _leaf_boxes_by_index(ref):
 
 
 def _check_refit_tree(b, boxes_morton, root):
-    from test_gpu_parity import outward16
     wf, wi = b.wide_nodes()
-    wf, wi = wf.numpy(), wi.numpy()
+    wf, wi = wf.cpu().numpy(), wi.cpu().numpy()
     n = len(boxes_morton)
     seen = np.zeros(n, int)
 
     def walk(w):
         lo = np.full(3, np.inf, np.float32); hi = np.full(3, -np.inf, np.float32)
         for k in range(32):
-            ch = wi[w, k]
+            ch = wi[w, 6, k]
             if ch == 0x7FFFFFFF:
                 continue
             sub = boxes_morton[~ch] if ch < 0 else walk(ch)
             if ch < 0:
                 seen[~ch] += 1
-            assert np.array_equal(wf[w, :6, k], outward16(sub))
+            assert np.array_equal(wf[w, :6, k], sub)
             lo = np.minimum(lo, sub[:3]); hi = np.maximum(hi, sub[3:])
         return np.concatenate([lo, hi])
     import sys

@@ -101,34 +101,19 @@ def test_build_bitexact(oracle, kind, n):
     check_wide_tree(b, ref, n)
 
 
-def outward16(box):
-    """a box [6] (lo, hi) rounded outward to fp16 (lo toward -inf, hi toward +inf):
-    what the 32-wide nodes store (rg_internal.cuh WideEntry)"""
-    out = np.empty(6, np.float32)
-    for i, x in enumerate(np.asarray(box, np.float32)):
-        h = np.float16(x)
-        if i < 3 and np.float32(h) > x:
-            h = np.nextafter(h, np.float16(-np.inf))
-        if i >= 3 and np.float32(h) < x:
-            h = np.nextafter(h, np.float16(np.inf))
-        out[i] = np.float32(h)
-    return out
-
-
 def check_wide_tree(b, ref, n):
-    """32-wide collapse: every leaf exactly once, every wide child box equals the
-    exact union of the leaf boxes below it rounded outward to fp16, no unfinished
-    collapse round."""
+    """32-wide collapse: every leaf exactly once, every wide child box equals
+    the exact union of the leaf boxes below it, no unfinished collapse round."""
     info = b.debug_views()["wide_info"].cpu().numpy()
     assert info[3] == 0
     wf, wi = b.wide_nodes()
-    wf, wi = wf.numpy(), wi.numpy()
+    wf, wi = wf.cpu().numpy(), wi.cpu().numpy()
     seen = np.zeros(n, int)
 
     def walk(w):
         lo = np.full(3, np.inf, np.float32); hi = np.full(3, -np.inf, np.float32)
         for k in range(32):
-            ch = wi[w, k]
+            ch = wi[w, 6, k]
             if ch == 0x7FFFFFFF:
                 continue
             cb = wf[w, :6, k]
@@ -137,7 +122,7 @@ def check_wide_tree(b, ref, n):
                 sub = ref.leaf_boxes[~ch]
             else:
                 sub = walk(ch)
-            assert np.array_equal(cb, outward16(sub))
+            assert np.array_equal(cb, sub)
             lo = np.minimum(lo, sub[:3]); hi = np.maximum(hi, sub[3:])
         return np.concatenate([lo, hi])
     if n >= 1 and n <= 300_000:
