@@ -645,13 +645,10 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, c
   // flight per instruction (the per-pair loop below waits on one pair at a time)
   if (S.lobes > 0) {
     const int per = 2 * S.lobes;
-    const float inv_per = 1.0f / (float)per;
     const int nitems = (32 - __clz(mask)) * per;
     const int c0 = 3 * qsh;                           // first SG chunk of the row
     for (int it = (int)lane; it - (int)lane < nitems; it += 32) {
-      int b = (int)((float)it * inv_per);             // it / per (small ints), corrected
-      if (b * per > it) --b;
-      if ((b + 1) * per <= it) ++b;
+      const int b = it / per;
       const int c = it - b * per;
       if (it < nitems && ((mask >> b) & 1u)) {
         const int e = base + b;
@@ -675,25 +672,19 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, c
       }
     }
   }
-  // SH: one coalesced burst per pair, lane = (pair group g, channel, 4 coefficients):
-  // dL/dc~_m = dc[ch] Y_m(d), Y(d) from shared memory (zero past the degree); the
-  // 3 qsh chunks of a pair use a group of GL lanes, 32 / GL pairs per iteration
-  const int nch = 3 * qsh;
-  const int GL = nch <= 4 ? 4 : (nch <= 8 ? 8 : 16);
-  const int g = (int)lane / GL, cix = (int)lane - g * GL;
-  const int ch = cix < nch ? cix / qsh : -1;
+  // SH: one coalesced burst per pair, lane = (channel, 4 coefficients):
+  // dL/dc~_m = dc[ch] Y_m(d), Y(d) from shared memory (zero past the degree)
+  const int ch = (int)lane < 3 * qsh ? (int)lane / qsh : -1;
   float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (ch >= 0) y = *reinterpret_cast<const float4*>(&M.Y[4 * (cix - ch * qsh)]);
+  if (ch >= 0) y = *reinterpret_cast<const float4*>(&M.Y[4 * ((int)lane - ch * qsh)]);
   while (mask) {
-    unsigned mm = mask;
-    for (int k = 0; k < g; ++k) mm &= mm - 1;       // this group's pair: the g-th set bit
-    const int b = mm ? __ffs(mm) - 1 : -1;
-    for (int k = 0; k < 32 / GL; ++k) mask &= mask - 1;
-    if (b >= 0 && ch >= 0) {
-      const int e = base + b;
-      const int pos = __float_as_int(M.e2[e].y);
+    const int b = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const int e = base + b;
+    const int pos = __float_as_int(M.e2[e].y);
+    if (ch >= 0) {
       const float dsel = ch == 0 ? A.a[e].w : (ch == 1 ? A.b[e].x : A.b[e].y);
-      atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + cix,
+      atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + lane,
                 make_float4(dsel * y.x, dsel * y.y, dsel * y.z, dsel * y.w));
     }
   }
