@@ -645,10 +645,13 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, c
   // flight per instruction (the per-pair loop below waits on one pair at a time)
   if (S.lobes > 0) {
     const int per = 2 * S.lobes;
+    const float inv_per = 1.0f / (float)per;
     const int nitems = (32 - __clz(mask)) * per;
     const int c0 = 3 * qsh;                           // first SG chunk of the row
     for (int it = (int)lane; it - (int)lane < nitems; it += 32) {
-      const int b = it / per;
+      int b = (int)((float)it * inv_per);             // it / per (small ints), corrected
+      if (b * per > it) --b;
+      if ((b + 1) * per <= it) ++b;
       const int c = it - b * per;
       if (it < nitems && ((mask >> b) & 1u)) {
         const int e = base + b;
