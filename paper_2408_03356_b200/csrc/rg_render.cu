@@ -267,8 +267,12 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       const float ot = RES ? __shfl_xor_sync(kFull, ktx, j) : 0.f;
       if ((((int)lane & j) == 0) ? (ok < key) : (ok > key)) { key = ok; pos = op; ktx = ot; }
     }
-    pend((int)lane >= kmax, key, pos, ktx);            // truncated beyond kmax (uniform call)
-    if ((int)lane >= kmax) { key = ~0ull; pos = 0u; }
+    if ((int)lane >= kmax) {
+      pend(true, key, pos, ktx);                       // truncated beyond kmax
+      key = ~0ull; pos = 0u;
+    } else {
+      pend(false, 0ull, 0u, 0.f);
+    }
     nk = __popc(__ballot_sync(kFull, key != ~0ull));
     if (nk == kmax) {
       kth = shfl64(key, kmax - 1);
