@@ -96,18 +96,14 @@ struct RenderArgs {
 
 // per-slot entry (AoS, three float4 so a lane reads a slot with LDS.128):
 //   e0 = {t_entry, t_exit, t_mid, c0}   e1 = {c1, c2, r, g}   e2 = {b, pos, idx, -}
-template <int STK, int PEND>
+template <int STK>
 struct WarpMemT {
   static constexpr int kStack = STK;
-  static constexpr int kPend = PEND;
-  unsigned long long pk[PEND > 0 ? PEND : 1];   // resumable fetch: pending candidate keys,
-  uint32_t pp[PEND > 0 ? PEND : 1];             // positions and exit times
-  float ptx[PEND > 0 ? PEND : 1];
   float4 e0[kSlots], e1[kSlots], e2[kSlots];
   uint32_t stk[STK];   // stacked wide node ids
   uint16_t stn[STK];  // their boxes' entry distances as 16-bit order keys (fp16 rounded
                        // down): pop-time selection and pruning
-  uint32_t lq[104];    // fetch: queued leaves awaiting the exact test (< 32 + 2 x 32 + 2)
+  uint32_t lq[96];     // fetch: queued leaves awaiting the exact test (< 32 + 2 x 32)
   alignas(16) float Y[16];   // Y(d) of the ray (zero past the degree), read as float4 by the scatter
 };
 struct WarpAcc {
@@ -160,78 +156,59 @@ __device__ __forceinline__ float stn_dec(unsigned k) {
   return __half2float(__ushort_as_half((unsigned short)b));
 }
 
-#ifdef RG_NO_RESUME
-constexpr bool kResume = false;
-#else
-constexpr bool kResume = true;
-#endif
-// Resumable-query state of the refill fetch (forward): the stack and the
-// pending candidates persist in shared memory between two refills of a ray.
-struct ResumeState {
-  int sp = 0;        // stack entries left by the last resumable fetch
-  int npend = 0;     // pending candidates (keys beyond the last result)
-  bool valid = false;
-};
-
 // Warp-cooperative k-nearest query on the 32-wide BVH: the kmax (<= 32)
 // smallest keys (t_entry bits, index) > cursor among Gaussians whose exact
 // support interval satisfies t_exit >= seg_lo and t_entry <= seg_hi.
 // Result: lane l < return value holds the l-th smallest key and its position.
-// RES (the forward's refill): instead of restarting at the root, continue the
-// previous query of this ray: unexpanded stack entries (children and leaves
-// beyond the k-th key are kept on the stack, leaves queued when popped) and the
-// pending candidates (tested but rejected, evicted or truncated, with their exit
-// times) all hold keys > the previous k-th key = this cursor.  Any overflow of the
-// pending list or the stack margin invalidates the state (the next query then
-// restarts at the root, which is always correct).
-template <bool RES, class WM>
+template <class WM>
 __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, float seg_hi,
                      unsigned long long cursor, int kmax, unsigned long long& key, uint32_t& pos,
-                     Counters& cnt, ResumeState& rs) {
+                     Counters& cnt) {
   const unsigned lane = lane_id();
   const unsigned lt_mask = (1u << lane) - 1u;
   if (lane == 0) cnt.fetches++;
   // candidate sort scratch aliases the transient slots, dead during every fetch
   unsigned long long* const kscr = reinterpret_cast<unsigned long long*>(&M.e0[kTrans]);
   uint32_t* const pscr = reinterpret_cast<uint32_t*>(&M.e1[kTrans]);
-  float* const tscr = reinterpret_cast<float*>(&M.e2[kTrans]);
   key = ~0ull;
   pos = 0;
-  float ktx = 0.f;           // RES: exit time of this lane's k-buffer entry
   int nk = 0;
   float te_lim = INFINITY;
   unsigned long long kth = ~0ull;
   const float slack = 1e-5f * (fabsf(seg_lo) + fabsf(seg_hi)) + 1e-6f;
   const float lo_s = seg_lo - slack, hi_s = seg_hi + slack;
-  bool keep = RES;           // the state stays resumable
-  int sp, qn = 0;
-  if (RES && rs.valid) {
-    sp = rs.sp;
-  } else {
-    sp = 1;
-    if (lane == 0) { M.stk[0] = 0; M.stn[0] = stn_enc(-INFINITY); }
-    if (RES) rs.npend = 0;
-  }
+  int sp = 1, qn = 0;
+  if (lane == 0) { M.stk[0] = 0; M.stn[0] = stn_enc(-INFINITY); }
   __syncwarp();
-  // RES: append (k, p, tx) of the flagged lanes to the pending list
-  auto pend = [&](bool give, unsigned long long k, uint32_t p, float tx) {
-    if (!RES) return;
-    const unsigned gm = __ballot_sync(kFull, give && k != ~0ull);
-    if (!gm) return;
-    const int n = __popc(gm);
-    if (rs.npend + n > WM::kPend) { keep = false; return; }
-    if (give && k != ~0ull) {
-      const int r = rs.npend + __popc(gm & lt_mask);
-      M.pk[r] = k; M.pp[r] = p; M.ptx[r] = tx;
-    }
-    rs.npend += n;
+  // Exact leaf tests are batched: box-passing leaves are queued in shared
+  // memory and tested 32 at a time (all lanes busy), then the candidates are
+  // bitonic-sorted and bitonic-merged into the k-buffer.
+  auto flush = [&](int n) {
     __syncwarp();
-  };
-  // merge candidates (one per flagged lane) into the k-buffer: rank sort, then the 32
-  // smallest of (k-buffer, candidates) form a bitonic sequence
-  auto merge = [&](bool cand, unsigned long long ck, uint32_t cp, float ctx) {
+    const uint32_t cp = (int)lane < n ? M.lq[lane] : 0u;
+    bool cand = false;
+    unsigned long long ck = ~0ull;
+    if ((int)lane < n) {
+      const float4* gp = S.geom + 4 * (size_t)cp;
+      const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2), g3 = __ldg(gp + 3);
+      PairGeom pg;
+      if (isect_exact(g0, g1, g2, g3, R.o, R.d, pg) && pg.tx >= seg_lo && pg.te <= seg_hi) {
+        ck = ((unsigned long long)fkey(pg.te) << 32) | (uint32_t)__float_as_int(g3.z);
+        cand = ck > cursor && ck < kth;
+        if (!cand) ck = ~0ull;
+      }
+    }
+    // drop the consumed queue entries
+    const int rem = qn - n;   // < 64 left over (two nodes' leaves per iteration)
+    const uint32_t mv = (int)lane < rem ? M.lq[n + lane] : 0u;
+    const uint32_t mv2 = (int)lane + 32 < rem ? M.lq[n + 32 + lane] : 0u;
+    __syncwarp();
+    if ((int)lane < rem) M.lq[lane] = mv;
+    if ((int)lane + 32 < rem) M.lq[32 + lane] = mv2;
+    qn = rem;
     const unsigned cmask = __ballot_sync(kFull, cand);
     if (!cmask) return;
+    // sort the candidates by rank (O(#candidates)): place, then read back in order
     {
       int crank = 0;
       unsigned mm = cmask;
@@ -241,133 +218,45 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
         const unsigned long long kb = shfl64(ck, b);
         crank += (cand && kb < ck) ? 1 : 0;
       }
-      __syncwarp();
-      if (cand) { kscr[crank] = ck; pscr[crank] = cp; if (RES) tscr[crank] = ctx; }
+      if (cand) { kscr[crank] = ck; pscr[crank] = cp; }
       __syncwarp();
       const int ncand = __popc(cmask);
       ck = (int)lane < ncand ? kscr[lane] : ~0ull;
     }
     uint32_t cpos = pscr[lane];
-    float ct = RES ? tscr[lane] : 0.f;
     __syncwarp();
+    // the 32 smallest of (k-buffer, candidates) form a bitonic sequence: merge
     {
       const unsigned long long rk = shfl64(ck, 31 - (int)lane);
       const uint32_t rp = __shfl_sync(kFull, cpos, 31 - (int)lane);
-      const float rt = RES ? __shfl_sync(kFull, ct, 31 - (int)lane) : 0.f;
-      unsigned long long ek = rk;                      // the larger one is evicted
-      uint32_t ep = rp;
-      float et = rt;
-      if (rk < key) { ek = key; ep = pos; et = ktx; key = rk; pos = rp; ktx = rt; }
-      pend(true, ek, ep, et);
+      if (rk < key) { key = rk; pos = rp; }
     }
 #pragma unroll
     for (int j = 16; j > 0; j >>= 1) {
       const unsigned long long ok = shfl64x(key, j);
       const uint32_t op = __shfl_xor_sync(kFull, pos, j);
-      const float ot = RES ? __shfl_xor_sync(kFull, ktx, j) : 0.f;
-      if ((((int)lane & j) == 0) ? (ok < key) : (ok > key)) { key = ok; pos = op; ktx = ot; }
+      if ((((int)lane & j) == 0) ? (ok < key) : (ok > key)) { key = ok; pos = op; }
     }
-    if ((int)lane >= kmax) {
-      pend(true, key, pos, ktx);                       // truncated beyond kmax
-      key = ~0ull; pos = 0u;
-    } else {
-      pend(false, 0ull, 0u, 0.f);
-    }
+    if ((int)lane >= kmax) { key = ~0ull; pos = 0u; }
     nk = __popc(__ballot_sync(kFull, key != ~0ull));
     if (nk == kmax) {
       kth = shfl64(key, kmax - 1);
       te_lim = fkey_inv((uint32_t)(kth >> 32));
     }
   };
-  // exact leaf tests, batched: queued leaves tested 32 at a time
-  auto flush = [&](int n) {
-    __syncwarp();
-    const uint32_t cp = (int)lane < n ? M.lq[lane] : 0u;
-    bool cand = false, later = false;
-    unsigned long long ck = ~0ull;
-    float ctx = 0.f;
-    if ((int)lane < n) {
-      const float4* gp = S.geom + 4 * (size_t)cp;
-      const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2), g3 = __ldg(gp + 3);
-      PairGeom pg;
-      if (isect_exact(g0, g1, g2, g3, R.o, R.d, pg) && pg.tx >= seg_lo && pg.te <= seg_hi) {
-        ck = ((unsigned long long)fkey(pg.te) << 32) | (uint32_t)__float_as_int(g3.z);
-        ctx = pg.tx;
-        cand = ck > cursor && ck < kth;
-        later = RES && ck > cursor && !cand;          // a key for a later query
-      }
-    }
-    // drop the consumed queue entries
-    const int rem = qn - n;   // < 72 left over
-    const uint32_t mv = (int)lane < rem ? M.lq[n + lane] : 0u;
-    const uint32_t mv2 = (int)lane + 32 < rem ? M.lq[n + 32 + lane] : 0u;
-    const uint32_t mv3 = (int)lane + 64 < rem ? M.lq[n + 64 + lane] : 0u;
-    __syncwarp();
-    if ((int)lane < rem) M.lq[lane] = mv;
-    if ((int)lane + 32 < rem) M.lq[32 + lane] = mv2;
-    if ((int)lane + 64 < rem) M.lq[64 + lane] = mv3;
-    qn = rem;
-    __syncwarp();
-    pend(later, ck, cp, ctx);
-    merge(cand, cand ? ck : ~0ull, cp, ctx);
-  };
-  // RES: the pending candidates of the previous query seed the k-buffer
-  if (RES && rs.valid && rs.npend > 0) {
-    const int np0 = rs.npend;
-    unsigned long long k0 = ~0ull, k1 = ~0ull;
-    uint32_t p0 = 0, p1 = 0;
-    float t0_ = 0.f, t1_ = 0.f;
-    if ((int)lane < np0) { k0 = M.pk[lane]; p0 = M.pp[lane]; t0_ = M.ptx[lane]; }
-    if ((int)lane + 32 < np0) { k1 = M.pk[32 + lane]; p1 = M.pp[32 + lane]; t1_ = M.ptx[32 + lane]; }
-    __syncwarp();
-    rs.npend = 0;
-    const bool c0 = (int)lane < np0 && k0 > cursor && t0_ >= seg_lo;
-    const bool c1 = (int)lane + 32 < np0 && k1 > cursor && t1_ >= seg_lo;
-    merge(c0, c0 ? k0 : ~0ull, p0, t0_);
-    const bool c1b = c1 && k1 < kth;                   // kth may have tightened
-    pend(c1 && !c1b, k1, p1, t1_);
-    merge(c1b, c1b ? k1 : ~0ull, p1, t1_);
-  }
-  // Best-first-ish DFS: each iteration pops the two entries with the smallest entry
+  // Best-first-ish DFS: each iteration pops the two nodes with the smallest entry
   // distances among the top 32 stack entries and visits both (their 14 child-box
   // loads per lane are in flight together); when even the nearest lies beyond the
-  // k-th key, all 32 are dropped (RES: the query stops if no entry of the whole
-  // stack can still hold a key <= the k-th; the stack is kept).
+  // k-th key, all 32 are dropped.  Pushes are unordered (the pop selects).
   while (sp > 0) {
-    int nodeA, nodeB = 0;
-    bool hasB = false;
+    int nodeA, nodeB = -1;
     {
       const int nwin = min(sp, 32);
       unsigned k16 = 0xFFFFu, nid = 0;
       if ((int)lane < nwin) { k16 = M.stn[sp - 1 - (int)lane]; nid = M.stk[sp - 1 - (int)lane]; }
-      unsigned kmin = __reduce_min_sync(kFull, k16);
+      const unsigned kmin = __reduce_min_sync(kFull, k16);
       if (stn_dec(kmin) > te_lim + slack) {
-        if (!RES) {
-          sp -= nwin;
-          continue;
-        }
-        // RES: look below the window for an entry within the limit
-        int best = -1;
-        unsigned bk = 0xFFFFu;
-        for (int top = sp - 32; top > 0; top -= 32) {
-          const int lo = max(top - 32, 0);
-          const int ii = top - 1 - (int)lane;
-          const unsigned kk = ii >= lo ? (unsigned)M.stn[ii] : 0xFFFFu;
-          const unsigned km = __reduce_min_sync(kFull, kk);
-          if (km < bk) {
-            bk = km;
-            best = top - 1 - (__ffs(__ballot_sync(kFull, kk == km)) - 1);
-          }
-        }
-        if (best < 0 || stn_dec(bk) > te_lim + slack) break;
-        // swap it to the top and pop it next
-        __syncwarp();
-        if (lane == 0) {
-          const uint32_t ta = M.stk[best]; const uint16_t tb = M.stn[best];
-          M.stk[best] = M.stk[sp - 1]; M.stn[best] = M.stn[sp - 1];
-          M.stk[sp - 1] = ta; M.stn[sp - 1] = tb;
-        }
-        __syncwarp();
+        sp -= nwin;
         continue;
       }
       const int srcA = __ffs(__ballot_sync(kFull, k16 == kmin)) - 1;
@@ -379,7 +268,6 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       if (kmin2 != 0xFFFFu && stn_dec(kmin2) <= te_lim + slack) {
         srcB = __ffs(__ballot_sync(kFull, k16b == kmin2)) - 1;
         nodeB = (int)__shfl_sync(kFull, nid, srcB);
-        hasB = true;
       }
 #endif
       // remove the popped entries: the surviving top entries (lanes 0, 1) fill the
@@ -398,25 +286,8 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       }
       __syncwarp();
     }
-    if (RES) {   // popped leaves (kept on the stack by an earlier query): queue them
-      const bool la = nodeA < 0, lb = hasB && nodeB < 0;
-      if (la || lb) {
-        if (lane == 0) {
-          if (la) M.lq[qn] = (uint32_t)(~nodeA);
-          if (lb) M.lq[qn + (la ? 1 : 0)] = (uint32_t)(~nodeB);
-        }
-        qn += (la ? 1 : 0) + (lb ? 1 : 0);
-        __syncwarp();
-        if (la) {
-          if (hasB && !lb) { nodeA = nodeB; hasB = false; }
-          else { while (qn >= 32) flush(32); continue; }   // nothing to visit
-        } else {
-          hasB = false;
-        }
-      }
-    }
-    if (lane == 0) cnt.nodes += hasB ? 2 : 1;
-    const bool two = hasB;
+    if (lane == 0) cnt.nodes += nodeB >= 0 ? 2 : 1;
+    const bool two = nodeB >= 0;
     const WideNode& WA = S.wide[nodeA];
     const WideNode& WB = S.wide[two ? nodeB : nodeA];
     const int childA = __ldg(&WA.child[lane]);
@@ -432,10 +303,10 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
     float tnA, tfA, tnB, tfB;
     box_t(alx, aly, alz, ahx, ahy, ahz, R.inv, R.oinv, tnA, tfA);
     box_t(blx, bly, blz, bhx, bhy, bhz, R.inv, R.oinv, tnB, tfB);
-    const bool boxA = childA != kWideEmpty && tnA <= tfA && tfA >= lo_s && tnA <= hi_s;
-    const bool boxB = childB != kWideEmpty && tnB <= tfB && tfB >= lo_s && tnB <= hi_s;
-    const bool hitA = boxA && tnA <= te_lim + slack;
-    const bool hitB = boxB && tnB <= te_lim + slack;
+    const bool hitA = childA != kWideEmpty && tnA <= tfA && tfA >= lo_s && tnA <= hi_s &&
+                      tnA <= te_lim + slack;
+    const bool hitB = childB != kWideEmpty && tnB <= tfB && tfB >= lo_s && tnB <= hi_s &&
+                      tnB <= te_lim + slack;
     // queue box-passing leaves (A's, then B's)
     {
       const unsigned lmA = __ballot_sync(kFull, hitA && childA < 0);
@@ -447,23 +318,18 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
         qn += __popc(lmA) + __popc(lmB);
       }
     }
-    // stacked children, any order (the pop selects): internal ones within the limit,
-    // and (RES) every box-passing child beyond it, leaves included
-    const bool pushA = childA >= 0 ? (RES ? boxA : hitA) : (RES && boxA && !hitA);
-    const bool pushB = childB >= 0 ? (RES ? boxB : hitB) : (RES && boxB && !hitB);
-    const unsigned imA = __ballot_sync(kFull, pushA);
-    const unsigned imB = __ballot_sync(kFull, pushB);
+    // internal children, any order (the pop selects)
+    const unsigned imA = __ballot_sync(kFull, hitA && childA >= 0);
+    const unsigned imB = __ballot_sync(kFull, hitB && childB >= 0);
     if (imA | imB) {
       const int npA = __popc(imA), np = npA + __popc(imB);
       __syncwarp();
-      // RES keeps a margin so that entries needed by this query always fit
-      const bool beyond_ok = !RES || sp + np <= WM::kStack - 64;
-      if (sp + np <= WM::kStack && beyond_ok) {
-        if (pushA) {
+      if (sp + np <= WM::kStack) {
+        if (hitA && childA >= 0) {
           const int r = sp + __popc(imA & lt_mask);
           M.stk[r] = (uint32_t)childA; M.stn[r] = stn_enc(tnA);
         }
-        if (pushB) {
+        if (hitB && childB >= 0) {
           const int r = sp + npA + __popc(imB & lt_mask);
           M.stk[r] = (uint32_t)childB; M.stn[r] = stn_enc(tnB);
         }
@@ -471,26 +337,6 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
 #ifdef RG_STACK_PROBE
         if (lane == 0 && (uint32_t)sp > cnt.stackov) cnt.stackov = sp;   // max depth, not overflows
 #endif
-      } else if (RES) {
-        // no room for the beyond entries: push only those within the limit, and the
-        // state is not resumable any more
-        keep = false;
-        const unsigned jA = __ballot_sync(kFull, hitA && childA >= 0);
-        const unsigned jB = __ballot_sync(kFull, hitB && childB >= 0);
-        const int nA = __popc(jA), n2 = nA + __popc(jB);
-        if (sp + n2 <= WM::kStack) {
-          if (hitA && childA >= 0) {
-            const int r = sp + __popc(jA & lt_mask);
-            M.stk[r] = (uint32_t)childA; M.stn[r] = stn_enc(tnA);
-          }
-          if (hitB && childB >= 0) {
-            const int r = sp + nA + __popc(jB & lt_mask);
-            M.stk[r] = (uint32_t)childB; M.stn[r] = stn_enc(tnB);
-          }
-          sp += n2;
-        } else if (lane == 0) {
-          cnt.stackov++;
-        }
       } else if (lane == 0) {
         cnt.stackov++;
       }
@@ -499,10 +345,6 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
     while (qn >= 32) flush(32);
   }
   while (qn > 0) flush(min(qn, 32));
-  if (RES) {
-    rs.sp = sp;
-    rs.valid = keep;
-  }
   return nk;
 }
 
@@ -905,7 +747,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
   // shared-window offsets; the dynamic (extern) form made the compiler re-derive the
   // window base (S2UR SR_CgaCtaId + ULEA) at loop heads of the hot loops
 #ifdef RG_STATIC_SMEM
-  using WM = WarpMemT<BWD ? kStkBwd : kStkFwd, BWD ? 0 : 64>;
+  using WM = WarpMemT<BWD ? kStkBwd : kStkFwd>;
   __shared__ WM sm_mem[kWarps];
   __shared__ WarpAcc sm_acc[BWD ? kWarps : 1];
   const unsigned lane = lane_id();
@@ -916,7 +758,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const unsigned lane = lane_id();
   const int wid = threadIdx.x >> 5;
-  using WM = WarpMemT<BWD ? kStkBwd : kStkFwd, BWD ? 0 : 64>;
+  using WM = WarpMemT<BWD ? kStkBwd : kStkFwd>;
   WM& M = reinterpret_cast<WM*>(smem_raw)[wid];
   WarpAcc& A = reinterpret_cast<WarpAcc*>(smem_raw + sizeof(WM) * kWarps)[BWD ? wid : 0];
 #endif
@@ -977,7 +819,6 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
     L.esub = (int)(lane / GW);
     int count = 0, nret = 0;
     unsigned long long cursor = 0;
-    ResumeState rs;     // resumable refill queries (forward)
     bool exhausted = false;
     int32_t* lg = P.log ? P.log + (size_t)ray * kLogWords : nullptr;
     int lp = 1;
@@ -1069,7 +910,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             M.e2[count + lane] = src[2];
           }
         } else {
-          got = fetch<!BWD && kResume>(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt, rs);
+          got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
           if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, count + (int)lane, R, pos);
           if (!BWD && log_ok) {
             unsigned long long off = 0;
@@ -1334,8 +1175,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
       } else if (!BWD && n_in == K && n_in == kA && !exhausted) {
         unsigned long long pk;
         uint32_t pp;
-        rs.valid = false;   // the probe clobbers the resumable query state
-        if (fetch<false>(P.S, M, R, tlo, thi, cursor, 1, pk, pp, cnt, rs) > 0 && lane == 0) cnt.overflows++;
+        if (fetch(P.S, M, R, tlo, thi, cursor, 1, pk, pp, cnt) > 0 && lane == 0) cnt.overflows++;
       }
       if (dbg) dbg_put(P, ray, dbg_n, s, n_use, M, 0);
       for (int g0 = 0; g0 < B; g0 += GW) {
@@ -1352,8 +1192,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             const int want = min(32, remaining);
             unsigned long long key;
             uint32_t pos;
-            rs.valid = false;
-            const int got = fetch<false>(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt, rs);
+            const int got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
             if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, kTrans + (int)lane, R, pos);
             __syncwarp();
             eval_range<GW, BASIS>(M, kA, kA + got, L, tk, val, sg, sr, sgg, sb, ev);
@@ -1367,7 +1206,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
           if (g0 == 0 && remaining == 0 && full_last) {
             unsigned long long pk;
             uint32_t pp;
-            if (fetch<false>(P.S, M, R, tlo, thi, cur2, 1, pk, pp, cnt, rs) > 0 && lane == 0) cnt.overflows++;
+            if (fetch(P.S, M, R, tlo, thi, cur2, 1, pk, pp, cnt) > 0 && lane == 0) cnt.overflows++;
           }
         }
         cnt.evals += ev;
@@ -1440,8 +1279,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
               const int want = min(32, remaining);
               unsigned long long key;
               uint32_t pos;
-              rs.valid = false;
-            const int got = fetch<false>(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt, rs);
+              const int got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
               if ((int)lane < got) {
                 setup_pair<!BWD, BASIS>(P.S, M, kTrans + (int)lane, R, pos);
                 A.a[kA + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1671,8 +1509,8 @@ void launch_render(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st)
   else launch_gw<BWD, 1, 0>(A, grid, smem, st);
 }
 
-constexpr size_t kSmemFwd = sizeof(WarpMemT<kStkFwd, 64>) * kWarps;
-constexpr size_t kSmemBwd = (sizeof(WarpMemT<kStkBwd, 0>) + sizeof(WarpAcc)) * kWarps;
+constexpr size_t kSmemFwd = sizeof(WarpMemT<kStkFwd>) * kWarps;
+constexpr size_t kSmemBwd = (sizeof(WarpMemT<kStkBwd>) + sizeof(WarpAcc)) * kWarps;
 // 4 resident backward blocks must fit the 196 KB shared-memory carve-out (1 KB
 // reserved per block): a larger carve-out halves L1 and costs ~6% (measured)
 static_assert(kSmemBwd <= 48 * 1024 + 128, "backward block exceeds the 196 KB carve-out budget");
