@@ -196,10 +196,10 @@ rg_status rg_render_forward(const rg_gaussians* g, const rg_bvh* bvh, const rg_c
                             int32_t* debug_counts, int32_t* debug_records, void* stream);
 
 /* Bytes of a fetch log for n_rays rays with room for pairs_per_ray set-up
-   pairs per ray on average (pairs_per_ray <= 0: a default of 48) and, per ray,
-   the per-sample sums of its first 4 four-slab windows (the backward reloads
-   them instead of re-evaluating; later windows are recomputed, results
-   identical either way). */
+   pairs per ray on average (pairs_per_ray <= 0: a default of 48) and, for the
+   4-slab windows, 2 * pairs_per_ray stored per-sample sums per ray on average
+   (the backward reloads them instead of re-evaluating; windows that do not fit
+   are recomputed, results identical either way). */
 size_t rg_fetch_log_bytes(int32_t n_rays, int32_t pairs_per_ray);
 
 /* ---- backward (a11-a12) ------------------------------------------------- */

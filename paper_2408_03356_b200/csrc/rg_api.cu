@@ -278,9 +278,8 @@ rg_status rg_render_forward(const rg_gaussians* g, const rg_bvh* bvh, const rg_c
 size_t rg_fetch_log_bytes(int32_t n_rays, int32_t pairs_per_ray) {
   if (n_rays < 0) return 0;
   const size_t ppr = pairs_per_ray > 0 ? (size_t)pairs_per_ray : 48;
-  // per pair a 48-B slot, per ray kWinFix stored windows of 32 float4 (rg_internal.cuh)
-  const size_t n = (size_t)(n_rays > 0 ? n_rays : 1);
-  return fetch_log_header_bytes(n_rays) + 48 * ppr * n + (size_t)kWinFix * 512 * n;
+  // per pair: a 48-B slot plus 2 stored window samples of 16 B (rg_internal.cuh split)
+  return fetch_log_header_bytes(n_rays) + 80 * ppr * (size_t)(n_rays > 0 ? n_rays : 1);
 }
 
 size_t rg_backward_workspace_bytes(int32_t n, int32_t sh_degree, int32_t sg_count) {

@@ -238,13 +238,14 @@ __device__ __forceinline__ void sh_basis(int deg, float x, float y, float z, flo
 // ---------------------------------------------------------------------------
 // host-side launchers (defined in the .cu files)
 // ---------------------------------------------------------------------------
-// fetch log (training): [0, 256) pair-arena counter (u64 @0); then per-ray
-// records of kLogWords int32 ([0] = fetch words used | stored windows << 16, or
-// -1; then (count, arena entry offset) per fetch); then the arena of 48-B pair
-// slots (3 float4 each); then, at the tail, kWinFix fixed window slots per ray
-// (32 float4 (sigma, sigma c) each: the first 4-slab windows of the ray).
+// fetch log (training): [0, 256) pair-arena counter (u64 @0) and sample-arena
+// counter (u64 @8); then per-ray records of kLogWords int32 ([0] = fetch words
+// used | stored windows << 16, or -1; then (count, arena entry offset) per fetch
+// from the front and one window-slot index per stored 4-slab window from the
+// back); then the arena of 48-B pair slots (3 float4 each); then the sample
+// arena (one float4 (sigma, sigma c) per lane of a stored window).  Split of the
+// space after the records: rest / 80 pair slots, the remainder float4 samples.
 constexpr int kLogWords = 64;
-constexpr int kWinFix = 4;    // stored 4-slab windows per ray (fixed slots at the log's tail)
 __host__ __device__ inline size_t fetch_log_header_bytes(int n_rays) {
   return 256 + ((4 * (size_t)kLogWords * (size_t)(n_rays > 0 ? n_rays : 1) + 255) & ~(size_t)255);
 }

@@ -79,8 +79,9 @@ struct RenderArgs {
   float4* arena;           // pair slots (3 float4 each)
   unsigned long long* arena_ctr;
   long long arena_cap;     // slots
-  float4* samp;            // per-window sample sums (sigma, sigma c_r, c_g, c_b): ray r's window
-                           // w < kWinFix at ((r * kWinFix + w) * 32 + lane), or null
+  float4* samp;            // per-window sample sums (sigma, sigma c_r, c_g, c_b), 32 per window
+  unsigned long long* samp_ctr;
+  long long samp_cap;      // float4 units
   rg_stats* stats;
   int dbg_rays, dbg_cap;
   int32_t* dbg_counts;
@@ -825,7 +826,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
     const bool replay_log = BWD && lg != nullptr && lg[0] >= 0;
     // stored windows (forward: count so far; backward: how many the forward stored)
     int nwin = BWD ? (replay_log ? (lg[0] >> 16) : 0) : 0;
-    bool wlog = !BWD && log_ok && P.samp != nullptr;
+    bool wlog = !BWD && log_ok;
     int wcur = 0;
     int s = 0;
     while (true) {
@@ -915,7 +916,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             unsigned long long off = 0;
             if (lane == 0 && got > 0) off = atomicAdd(P.arena_ctr, (unsigned long long)got);
             off = shfl64(off, 0);
-            if (lp + 2 > kLogWords || (long long)(off + got) > P.arena_cap) {
+            if (lp + 2 > kLogWords - nwin || (long long)(off + got) > P.arena_cap) {
               log_ok = false;
             } else {
               if (lane == 0) { lg[lp] = got; lg[lp + 1] = (int)off; }
@@ -969,7 +970,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
           bool stored = false;
           if (BWD && !INSTR) {
             if (wcur < nwin) {
-              const float4 v = P.samp[((size_t)ray * kWinFix + wcur) * 32 + lane];
+              const float4 v = P.samp[(size_t)lg[kLogWords - 1 - wcur] * 32 + lane];
               sg = v.x; sr = v.y; sgg = v.z; sb = v.w;
               stored = true;
             }
@@ -993,11 +994,16 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             }
           }
           if (!BWD && wlog && log_ok) {   // store this window's sums for the backward
-            if (nwin < kWinFix) {          // the ray's own fixed slots: no allocation
-              P.samp[((size_t)ray * kWinFix + nwin) * 32 + lane] = make_float4(sg, sr, sgg, sb);
-              ++nwin;
-            } else {
+            unsigned long long off = 0;
+            if (lane == 0) off = atomicAdd(P.samp_ctr, 32ull);
+            off = shfl64(off, 0);
+            // keep >= 8 record words for later fetch records (they have priority)
+            if (kLogWords - nwin - lp < 9 || (long long)(off + 32) > P.samp_cap) {
               wlog = false;
+            } else {
+              if (lane == 0) lg[kLogWords - 1 - nwin] = (int)(off >> 5);
+              P.samp[off + lane] = make_float4(sg, sr, sgg, sb);
+              ++nwin;
             }
           }
           const bool live0 = val && sg > 0.f;
@@ -1518,14 +1524,10 @@ void set_log(RenderArgs& A, const void* log, size_t log_bytes, int n_rays) {
   A.log = reinterpret_cast<int32_t*>(base + 256);
   A.arena = reinterpret_cast<float4*>(base + hdr);
   const size_t rest = log_bytes - hdr;
-  const size_t samp_bytes = (size_t)n_rays * kWinFix * 32 * 16;   // fixed per-ray window slots
-  if (rest >= samp_bytes + 48 * (size_t)n_rays) {
-    A.samp = reinterpret_cast<float4*>(base + log_bytes - samp_bytes);   // 16-B aligned tail
-    A.arena_cap = (long long)((rest - samp_bytes) / 48);
-  } else {
-    A.samp = nullptr;
-    A.arena_cap = (long long)(rest / 48);
-  }
+  A.arena_cap = (long long)(rest / 80);
+  A.samp_ctr = reinterpret_cast<unsigned long long*>(base + 8);
+  A.samp = reinterpret_cast<float4*>(base + hdr + 48 * (size_t)A.arena_cap);
+  A.samp_cap = (long long)((rest - 48 * (size_t)A.arena_cap) / 16);
 }
 
 }  // namespace
@@ -1550,7 +1552,7 @@ cudaError_t launch_forward(const rg_gaussians& g, const rg_bvh& b, const rg_conf
   if (A.n_rays == 0) return cudaSuccess;
   A.rgb = rgb; A.T = T; A.replay = replay; A.stats = stats;
   set_log(A, log, log_bytes, A.n_rays);
-  if (log) cudaMemsetAsync(A.arena_ctr, 0, 8, st);
+  if (log) cudaMemsetAsync(A.arena_ctr, 0, 16, st);
   A.dbg_rays = dbg_rec ? dbg_rays : 0;
   A.dbg_cap = dbg_cap; A.dbg_counts = dbg_counts; A.dbg_rec = dbg_rec;
   launch_render<false>(A, grid, kSmemFwd, st);
