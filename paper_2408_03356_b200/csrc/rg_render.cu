@@ -809,9 +809,10 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
       float Y[16];
       sh_basis(P.S.deg, R.d.x, R.d.y, R.d.z, Y);
       const int nc = (P.S.deg + 1) * (P.S.deg + 1);
+      float ym = 0.f;                 // lane m < nc stores Y_m (register selects, one store)
 #pragma unroll
-      for (int m = 0; m < 16; ++m)
-        if ((int)lane == m) M.Y[m] = m < nc ? Y[m] : 0.f;
+      for (int m = 0; m < 16; ++m) ym = (int)lane == m ? Y[m] : ym;
+      if (lane < 16) M.Y[lane] = (int)lane < nc ? ym : 0.f;
       __syncwarp();
     }
     Lanes<GW> L;
