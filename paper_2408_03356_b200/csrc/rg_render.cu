@@ -79,6 +79,7 @@ struct RenderArgs {
   float4* arena;           // pair slots (3 float4 each)
   unsigned long long* arena_ctr;
   long long arena_cap;     // slots
+  int pair_fix;            // pair slots owned by each ray (arena [0, n_rays * pair_fix))
   float4* samp;            // per-window sample sums (sigma, sigma c_r, c_g, c_b), 32 per window
   unsigned long long* samp_ctr;
   long long samp_cap;      // float4 units
@@ -829,6 +830,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
     int nwin = BWD ? (replay_log ? (lg[0] >> 16) : 0) : 0;
     bool wlog = !BWD && log_ok;
     int wcur = 0;
+    int fix_used = 0;   // forward: pair slots used in the ray's own block
     int s = 0;
     while (true) {
       const int k0 = s * B;
@@ -914,10 +916,19 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
           got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
           if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, count + (int)lane, R, pos);
           if (!BWD && log_ok) {
+            // the ray's own pair_fix slots first (no allocation), then the shared
+            // overflow region (one atomic per fetch)
             unsigned long long off = 0;
-            if (lane == 0 && got > 0) off = atomicAdd(P.arena_ctr, (unsigned long long)got);
-            off = shfl64(off, 0);
-            if (lp + 2 > kLogWords - nwin || (long long)(off + got) > P.arena_cap) {
+            bool fits = true;
+            if (fix_used + got <= P.pair_fix) {
+              off = (unsigned long long)ray * P.pair_fix + fix_used;
+              fix_used += got;
+            } else {
+              if (lane == 0 && got > 0) off = atomicAdd(P.arena_ctr, (unsigned long long)got);
+              off = shfl64(off, 0) + (unsigned long long)P.n_rays * P.pair_fix;
+              fits = (long long)(off + got) <= P.arena_cap;
+            }
+            if (lp + 2 > kLogWords - nwin || !fits) {
               log_ok = false;
             } else {
               if (lane == 0) { lg[lp] = got; lg[lp + 1] = (int)off; }
@@ -1526,6 +1537,9 @@ void set_log(RenderArgs& A, const void* log, size_t log_bytes, int n_rays) {
   A.arena = reinterpret_cast<float4*>(base + hdr);
   const size_t rest = log_bytes - hdr;
   A.arena_cap = (long long)(rest / 80);
+  // per-ray blocks of 40 slots when the arena has >= 48 per ray (the default budget):
+  // most rays never touch the shared counter
+  A.pair_fix = A.arena_cap >= 48ll * n_rays ? 40 : 0;
   A.samp_ctr = reinterpret_cast<unsigned long long*>(base + 8);
   A.samp = reinterpret_cast<float4*>(base + hdr + 48 * (size_t)A.arena_cap);
   A.samp_cap = (long long)((rest - 48 * (size_t)A.arena_cap) / 16);
