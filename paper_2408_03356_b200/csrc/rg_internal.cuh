@@ -242,7 +242,7 @@ __device__ __forceinline__ void sh_basis(int deg, float x, float y, float z, flo
 // counter (u64 @8); then per-ray records of kLogWords int32 ([0] = fetch words
 // used | stored windows << 16, or -1; then (count, arena entry offset) per fetch
 // from the front and one window-slot index per stored 4-slab window from the
-// back); then the arena of 48-B pair slots (3 float4 each: per-ray blocks of 40
+// back); then the arena of 48-B pair slots (3 float4 each: per-ray blocks of 32
 // slots, then a shared overflow region bump-allocated through the counter); then the sample
 // arena (one float4 (sigma, sigma c) per lane of a stored window).  Split of the
 // space after the records: rest / 80 pair slots, the remainder float4 samples.

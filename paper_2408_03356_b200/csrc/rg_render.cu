@@ -1537,9 +1537,9 @@ void set_log(RenderArgs& A, const void* log, size_t log_bytes, int n_rays) {
   A.arena = reinterpret_cast<float4*>(base + hdr);
   const size_t rest = log_bytes - hdr;
   A.arena_cap = (long long)(rest / 80);
-  // per-ray blocks of 40 slots when the arena has >= 48 per ray (the default budget):
-  // most rays never touch the shared counter
-  A.pair_fix = A.arena_cap >= 48ll * n_rays ? 40 : 0;
+  // per-ray blocks of 32 slots (a ray's first fetch always fits) when the arena has
+  // >= 48 per ray (the default budget); later fetches use the shared region
+  A.pair_fix = A.arena_cap >= 48ll * n_rays ? 32 : 0;
   A.samp_ctr = reinterpret_cast<unsigned long long*>(base + 8);
   A.samp = reinterpret_cast<float4*>(base + hdr + 48 * (size_t)A.arena_cap);
   A.samp_cap = (long long)((rest - 48 * (size_t)A.arena_cap) / 16);
