@@ -426,92 +426,6 @@ __global__ void k_collapse_init(int n, const float* leaf_box, WideNode* wide, in
   }
 }
 
-// One persistent launch over a device work queue of (binary id, wide id)
-// items.  counts: [0] wide nodes allocated, [1] head (claims), [2] items done,
-// [3] error flag, [4] items reserved.  The queue is pre-filled with -1; an
-// item is written with one 8-byte store after its slot is reserved.  A thread
-// whose claimed slot is not reserved exits once done == reserved is observed
-// (done read before reserved): every reserved item is then finished, so no
-// further item can appear.
-__global__ void __launch_bounds__(128) k_collapse_persistent(const float4* nodes, WideNode* wide,
-                                                             int2* q, int* wide_src, int* counts) {
-  volatile int* vc = counts;
-  volatile long long* vq = reinterpret_cast<volatile long long*>(q);
-  while (true) {
-    const int it = atomicAdd(counts + 1, 1);
-    bool have = false;
-    long long raw = -1;
-    while (true) {
-      const int done = vc[2];
-      __threadfence();
-      const int res = vc[4];
-      if (it < res) {
-        raw = vq[it];
-        if ((int)(raw & 0xFFFFFFFF) != -1) { have = true; break; }
-      } else if (done == res) {
-        break;
-      }
-      __nanosleep(64);
-    }
-    if (!have) return;
-    const int2 job = make_int2((int)(raw & 0xFFFFFFFF), (int)(raw >> 32));
-    int ids[kWide];
-    float bx[kWide][6];
-    int m = 0;
-    {
-      const float* w = reinterpret_cast<const float*>(nodes + 4 * (size_t)job.x);
-      const int4 c = *reinterpret_cast<const int4*>(nodes + 4 * (size_t)job.x + 3);
-      ids[0] = c.x; ids[1] = c.y;
-      for (int k = 0; k < 6; ++k) { bx[0][k] = w[k]; bx[1][k] = w[6 + k]; }
-      m = 2;
-    }
-    while (m < kWide) {
-      int best = -1;
-      float ba = -2.f;
-      for (int k = 0; k < m; ++k)
-        if (ids[k] >= 0) {
-          const float a = box_area(bx[k]);
-          if (a > ba) { ba = a; best = k; }
-        }
-      if (best < 0) break;
-      const int b = ids[best];
-      const float* w = reinterpret_cast<const float*>(nodes + 4 * (size_t)b);
-      const int4 c = *reinterpret_cast<const int4*>(nodes + 4 * (size_t)b + 3);
-      ids[best] = c.x;
-      for (int k = 0; k < 6; ++k) bx[best][k] = w[k];
-      ids[m] = c.y;
-      for (int k = 0; k < 6; ++k) bx[m][k] = w[6 + k];
-      ++m;
-    }
-    int nint = 0;
-    for (int k = 0; k < m; ++k) nint += ids[k] >= 0;
-    const int wid0 = nint ? atomicAdd(counts + 0, nint) : 0;
-    int slot = 0;
-    WideNode& W = wide[job.y];
-    for (int k = 0; k < kWide; ++k) {
-      if (k < m) {
-        int child = ids[k];
-        if (child >= 0) {
-          const int wid = wid0 + slot++;
-          wide_src[wid] = child;                                 // for rg_refit_bvh
-          const int qs = atomicAdd(counts + 4, 1);               // reserve a queue slot
-          vq[qs] = ((long long)wid << 32) | (unsigned)child;     // publish with one store
-          child = wid;
-        }
-        W.lox[k] = bx[k][0]; W.loy[k] = bx[k][1]; W.loz[k] = bx[k][2];
-        W.hix[k] = bx[k][3]; W.hiy[k] = bx[k][4]; W.hiz[k] = bx[k][5];
-        W.child[k] = child;
-      } else {
-        W.lox[k] = W.loy[k] = W.loz[k] = INFINITY;
-        W.hix[k] = W.hiy[k] = W.hiz[k] = -INFINITY;
-        W.child[k] = kWideEmpty;
-      }
-    }
-    __threadfence();
-    atomicAdd(counts + 2, 1);                // this item is done
-  }
-}
-
 // refit of the wide nodes after k_refit (rg_refit_bvh): one warp per wide
 // node, lane = child slot; an internal child's box is the union of its binary
 // node's two child boxes, a leaf's its padded AABB; the topology is kept.
@@ -543,11 +457,18 @@ __global__ void __launch_bounds__(128) k_wide_refit(const float4* nodes, const f
 #ifndef RG_COLLAPSE_OPEN
 #define RG_COLLAPSE_OPEN 1
 #endif
-// Warp-per-item variant of the collapse: lane k holds candidate entry k (id, box,
+// Collapse of the binary tree into 32-wide nodes, one persistent launch over a
+// device work queue of (binary id, wide id) items.  The queue is pre-filled with
+// -1; an item is written with one 8-byte store after its slot is reserved.  A
+// warp whose claimed slot is not reserved exits once done == reserved is observed
+// (done read before reserved): every reserved item is then finished, so no
+// further item can appear.  counts: [0] wide nodes allocated, [1] head (claims),
+// [2] items done, [3] error flag, [4] items reserved.
+// Per item (one warp): lane k holds candidate entry k (id, box,
 // area) in registers; each round opens, in parallel, the largest-area internal
 // entries (RG_COLLAPSE_OPEN per round; 1 = the greedy cut of the thread variant),
 // left child in place, right child appended; no local-memory candidate arrays.
-// Same queue protocol as above (one item per warp, bulk reservations).
+// Bulk reservations of wide ids and queue slots per item.
 __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, WideNode* wide, int2* q,
                                                        int* wide_src, int* counts) {
   const unsigned full = 0xffffffffu;
@@ -766,11 +687,7 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // all blocks co-resident (waiting threads spin): 2 blocks of 128 per SM
-#ifdef RG_COLLAPSE_THREAD
-    k_collapse_persistent<<<2 * sms, 128, 0, st>>>(nodes, wide, qa, wsrc, wc);
-#else
     k_collapse_warp<<<4 * sms, 128, 0, st>>>(nodes, wide, qa, wsrc, wc);
-#endif
     k_collapse_check<<<1, 1, 0, st>>>(wc, (int)wide_capacity(n));
     count_launches(2);
   }

@@ -747,22 +747,12 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
   // static shared memory (fwd 35.6 KB, bwd 48.0 KB <= the 48 KB static limit): constant
   // shared-window offsets; the dynamic (extern) form made the compiler re-derive the
   // window base (S2UR SR_CgaCtaId + ULEA) at loop heads of the hot loops
-#ifdef RG_STATIC_SMEM
-  using WM = WarpMemT<BWD ? kStkBwd : kStkFwd>;
-  __shared__ WM sm_mem[kWarps];
-  __shared__ WarpAcc sm_acc[BWD ? kWarps : 1];
-  const unsigned lane = lane_id();
-  const int wid = threadIdx.x >> 5;
-  WM& M = sm_mem[wid];
-  WarpAcc& A = sm_acc[BWD ? wid : 0];
-#else
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const unsigned lane = lane_id();
   const int wid = threadIdx.x >> 5;
   using WM = WarpMemT<BWD ? kStkBwd : kStkFwd>;
   WM& M = reinterpret_cast<WM*>(smem_raw)[wid];
   WarpAcc& A = reinterpret_cast<WarpAcc*>(smem_raw + sizeof(WM) * kWarps)[BWD ? wid : 0];
-#endif
   int ray;
   Ray R;
   if (P.cam_mode) {
@@ -1482,10 +1472,6 @@ void ray_grid(RenderArgs& A, const rg_rays* rays, const rg_camera* cam, dim3& gr
 // dynamic shared memory above the 48 KB default needs a per-kernel opt-in
 template <bool BWD, int GW, bool INSTR, int BASIS>
 void launch_one(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
-#ifdef RG_STATIC_SMEM
-  (void)smem;
-  k_render<BWD, GW, INSTR, BASIS><<<grid, kBlock, 0, st>>>(A);
-#else
   static bool opted = false;
   if (!opted) {
     cudaFuncSetAttribute(k_render<BWD, GW, INSTR, BASIS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1493,7 +1479,6 @@ void launch_one(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
     opted = true;
   }
   k_render<BWD, GW, INSTR, BASIS><<<grid, kBlock, smem, st>>>(A);
-#endif
 }
 
 template <bool BWD, int GW, int BASIS>
