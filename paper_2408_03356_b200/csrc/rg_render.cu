@@ -69,7 +69,6 @@ struct RenderArgs {
   int cam_mode;
   rg_camera cam;
   int rw, rh, tiles_x;
-  int n_units;             // block work units (tiles / pixels / ray quads)
   const float* ro;
   const float* rd;
   int n_rays;
@@ -743,16 +742,21 @@ __device__ __forceinline__ void dbg_put(const RenderArgs& P, int ray, int& dbg_n
 
 // INSTR: counters (rg_stats) and the debug dump; the uninstrumented variant
 // compiles them out (8 fewer live registers through the march)
-// One unit of work of a block: a 2x2 pixel tile (camera mode), one pixel's 4
-// subsamples (RayGauss4x) or 4 consecutive explicit rays; warp = one ray.
-template <bool BWD, int GW, bool INSTR, int BASIS, class WM>
-__device__ __forceinline__ void render_unit(const RenderArgs& P, WM& M, WarpAcc& A, int unit) {
+template <bool BWD, int GW, bool INSTR, int BASIS>
+__global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FWD) k_render(const RenderArgs P) {
+  // static shared memory (fwd 35.6 KB, bwd 48.0 KB <= the 48 KB static limit): constant
+  // shared-window offsets; the dynamic (extern) form made the compiler re-derive the
+  // window base (S2UR SR_CgaCtaId + ULEA) at loop heads of the hot loops
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const unsigned lane = lane_id();
   const int wid = threadIdx.x >> 5;
+  using WM = WarpMemT<BWD ? kStkBwd : kStkFwd>;
+  WM& M = reinterpret_cast<WM*>(smem_raw)[wid];
+  WarpAcc& A = reinterpret_cast<WarpAcc*>(smem_raw + sizeof(WM) * kWarps)[BWD ? wid : 0];
   int ray;
   Ray R;
   if (P.cam_mode) {
-    const int tile = unit;
+    const int tile = blockIdx.x;
     if (P.cam.spp == 1) {         // block = 2x2 pixel tile, warp = pixel
       const int px = 2 * (tile % P.tiles_x) + (wid & 1);
       const int py = 2 * (tile / P.tiles_x) + (wid >> 1);
@@ -766,7 +770,7 @@ __device__ __forceinline__ void render_unit(const RenderArgs& P, WM& M, WarpAcc&
                  R.o, R.d);
     }
   } else {
-    ray = unit * kWarps + wid;
+    ray = blockIdx.x * kWarps + wid;
     if (ray >= P.n_rays) return;
     R.o = make_float3(P.ro[3 * ray], P.ro[3 * ray + 1], P.ro[3 * ray + 2]);
     R.d = make_float3(P.rd[3 * ray], P.rd[3 * ray + 1], P.rd[3 * ray + 2]);
@@ -1327,20 +1331,6 @@ __device__ __forceinline__ void render_unit(const RenderArgs& P, WM& M, WarpAcc&
   if (INSTR && P.stats) flush_stats(P.stats, cnt, hit);
 }
 
-// Persistent grid (SMs x resident blocks): each block loops over units with a grid
-// stride, so warps never idle behind a block's slowest ray and no block is
-// launched per tile; units interleave, which balances the ray costs.
-template <bool BWD, int GW, bool INSTR, int BASIS>
-__global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FWD) k_render(const RenderArgs P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int wid = threadIdx.x >> 5;
-  using WM = WarpMemT<BWD ? kStkBwd : kStkFwd>;
-  WM& M = reinterpret_cast<WM*>(smem_raw)[wid];
-  WarpAcc& A = reinterpret_cast<WarpAcc*>(smem_raw + sizeof(WM) * kWarps)[BWD ? wid : 0];
-  for (int unit = blockIdx.x; unit < P.n_units; unit += gridDim.x)
-    render_unit<BWD, GW, INSTR, BASIS>(P, M, A, unit);
-}
-
 // (mu, M) -> (mu, q, s) and Morton -> caller order
 __global__ void __launch_bounds__(256) k_finalize(const float* gbuf, int gstride,
                                                   const uint32_t* order, rg_gaussians g,
@@ -1477,18 +1467,6 @@ void ray_grid(RenderArgs& A, const rg_rays* rays, const rg_camera* cam, dim3& gr
     A.n_rays = rays->n;
     grid = dim3((unsigned)((rays->n + kWarps - 1) / kWarps));
   }
-  A.n_units = (int)grid.x;
-#ifndef RG_NO_PERSIST
-  // persistent grid: the resident blocks of all SMs (RG_MIN_BLOCKS per SM)
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  const unsigned cap = (unsigned)(sms * RG_MIN_BLOCKS);
-  if (grid.x > cap) grid.x = cap;
-#endif
 }
 
 // dynamic shared memory above the 48 KB default needs a per-kernel opt-in
