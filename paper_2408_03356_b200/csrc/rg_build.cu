@@ -395,8 +395,8 @@ __global__ void __launch_bounds__(kThreads) k_refit(const float* leaf_box, float
 // --- collapse of the binary tree into 32-wide nodes (traversal structure) --------
 // Greedy top-down: a wide node's children are a cut of the binary subtree,
 // grown by repeatedly opening the internal entry with the largest box surface
-// area until 32 entries (or only leaves) remain.  Level-synchronous rounds with
-// device-side work queues (binary id, wide id).
+// area until 32 entries (or only leaves) remain.  One persistent launch over a
+// device work queue of (binary id, wide id) items (k_collapse_warp).
 __device__ __forceinline__ float box_area(const float* b) {
   const float dx = b[3] - b[0], dy = b[4] - b[1], dz = b[5] - b[2];
   return (dx < 0.f || dy < 0.f || dz < 0.f) ? -1.f : dx * dy + dy * dz + dz * dx;
@@ -674,7 +674,7 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
     cudaMemsetAsync(cnt, 0, sizeof(int) * (size_t)(n - 1), st);
   }
   k_refit<<<blocks, kThreads, 0, st>>>(leaf_box, nodes, parent_int, parent_leaf, cnt, root_box, n);
-  // 32-wide collapse (level-synchronous; queue slots 1/2 alternate)
+  // 32-wide collapse: one persistent launch over the device work queue
   WideNode* wide = reinterpret_cast<WideNode*>(ws + L.wide);
   int2* qa = reinterpret_cast<int2*>(ws + L.wq_a);
   int* wc = reinterpret_cast<int*>(ws + L.wcounts);
