@@ -36,6 +36,12 @@ namespace {
 #ifndef RG_MIN_BLOCKS
 #define RG_MIN_BLOCKS 4                // resident blocks per SM the register budget targets (bwd)
 #endif
+#ifndef RG_EVAL_UNROLL
+#define RG_EVAL_UNROLL 2         // forward window evaluation loop
+#endif
+#ifndef RG_MEMBER_UNROLL
+#define RG_MEMBER_UNROLL 2       // backward member loop
+#endif
 #ifndef RG_MIN_BLOCKS_FWD
 #define RG_MIN_BLOCKS_FWD RG_MIN_BLOCKS   // forward (no WarpAcc: smem allows more blocks)
 #endif
@@ -978,7 +984,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             }
             ++wcur;
           }
-#pragma unroll 2
+#pragma unroll RG_EVAL_UNROLL
           for (int e = 0; e < (stored ? 0 : n3); ++e) {
             const float4 a = M.e0[e];
             if (val && a.x <= tk && tk <= a.y) {
@@ -1109,7 +1115,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
                 int kh = (int)ceilf((a.y - t0) / c.dt - kf) + 1;
                 kl = max(kl, part0);
                 kh = min(kh, min(last, part0 + P2 - 1));
-#pragma unroll 2
+#pragma unroll RG_MEMBER_UNROLL
                 for (int k = kl; k <= kh; ++k) {
                   const float4 s0 = A.s0[k];
                   const float tkk = s0.x;
