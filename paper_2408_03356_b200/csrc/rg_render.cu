@@ -33,6 +33,12 @@ namespace rg {
 
 namespace {
 
+#ifndef RG_EVAL_UNROLL
+#define RG_EVAL_UNROLL 2         // forward window evaluation loop
+#endif
+#ifndef RG_MEMBER_UNROLL
+#define RG_MEMBER_UNROLL 2       // backward member loop
+#endif
 #ifndef RG_MIN_BLOCKS
 #define RG_MIN_BLOCKS 4                // resident blocks per SM the register budget targets (bwd)
 #endif
