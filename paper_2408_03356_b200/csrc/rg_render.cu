@@ -51,6 +51,8 @@ namespace {
 #ifndef RG_MIN_BLOCKS_FWD
 #define RG_MIN_BLOCKS_FWD RG_MIN_BLOCKS   // forward (no WarpAcc: smem allows more blocks)
 #endif
+constexpr int kEvalUnroll = RG_EVAL_UNROLL;
+constexpr int kMemberUnroll = RG_MEMBER_UNROLL;
 constexpr int kWarps = 4;              // rays (warps) per block
 static_assert(kWarps == 4, "camera mode: a block is a 2x2 pixel tile, or one pixel's 4 subsamples");
 constexpr int kBlock = 32 * kWarps;
@@ -990,7 +992,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             }
             ++wcur;
           }
-#pragma unroll RG_EVAL_UNROLL
+#pragma unroll kEvalUnroll
           for (int e = 0; e < (stored ? 0 : n3); ++e) {
             const float4 a = M.e0[e];
             if (val && a.x <= tk && tk <= a.y) {
@@ -1121,7 +1123,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
                 int kh = (int)ceilf((a.y - t0) / c.dt - kf) + 1;
                 kl = max(kl, part0);
                 kh = min(kh, min(last, part0 + P2 - 1));
-#pragma unroll RG_MEMBER_UNROLL
+#pragma unroll kMemberUnroll
                 for (int k = kl; k <= kh; ++k) {
                   const float4 s0 = A.s0[k];
                   const float tkk = s0.x;
