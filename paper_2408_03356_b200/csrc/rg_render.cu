@@ -34,7 +34,7 @@ namespace rg {
 namespace {
 
 #ifndef RG_EVAL_UNROLL
-#define RG_EVAL_UNROLL 2         // forward window evaluation loop
+#define RG_EVAL_UNROLL 4         // forward window evaluation loop (sweep: 1 +2%, 2 +0.8%)
 #endif
 #ifndef RG_MEMBER_UNROLL
 #define RG_MEMBER_UNROLL 2       // backward member loop
@@ -43,7 +43,7 @@ namespace {
 #define RG_MIN_BLOCKS 4                // resident blocks per SM the register budget targets (bwd)
 #endif
 #ifndef RG_EVAL_UNROLL
-#define RG_EVAL_UNROLL 2         // forward window evaluation loop
+#define RG_EVAL_UNROLL 4         // forward window evaluation loop (sweep: 1 +2%, 2 +0.8%)
 #endif
 #ifndef RG_MEMBER_UNROLL
 #define RG_MEMBER_UNROLL 2       // backward member loop
