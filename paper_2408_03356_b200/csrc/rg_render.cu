@@ -42,12 +42,6 @@ namespace {
 #ifndef RG_MIN_BLOCKS
 #define RG_MIN_BLOCKS 4                // resident blocks per SM the register budget targets (bwd)
 #endif
-#ifndef RG_EVAL_UNROLL
-#define RG_EVAL_UNROLL 4         // forward window evaluation loop (sweep: 1 +2%, 2 +0.8%)
-#endif
-#ifndef RG_MEMBER_UNROLL
-#define RG_MEMBER_UNROLL 2       // backward member loop
-#endif
 #ifndef RG_MIN_BLOCKS_FWD
 #define RG_MIN_BLOCKS_FWD RG_MIN_BLOCKS   // forward (no WarpAcc: smem allows more blocks)
 #endif
