@@ -56,11 +56,12 @@ constexpr int kRet = kA + 32;          // retired (expired, not yet scattered) s
 constexpr int kSlots = kA + 64;
 static_assert(kA == 64, "expire/n_in handle two 32-slot chunks");
 #ifndef RG_STK_FWD
-#define RG_STK_FWD 320
+#define RG_STK_FWD 256
 #endif
-// traversal stack entries (wide nodes; max depth seen: C1 ~60, C3 170; an overflow
-// drops subtrees and is counted in rg_stats.stack_overflows, asserted 0 by the
-// tests): the forward affords 320 (512 costs ~1% through the smaller L1); the
+// traversal stack entries (wide nodes; max depth seen (tools/probe_stack.sh): C1 60,
+// C3 135; an overflow drops subtrees and is counted in rg_stats.stack_overflows,
+// asserted 0 by the tests): the forward takes 256 (320: +0.8% forward, 512: +1%
+// more, through the smaller L1 carve-out); the
 // backward traverses only for rays whose fetch log overflowed and must stay within
 // its 48 KB block budget
 constexpr int kStkFwd = RG_STK_FWD;
@@ -217,6 +218,8 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
     qn = rem;
     const unsigned cmask = __ballot_sync(kFull, cand);
     if (!cmask) return;
+    uint32_t cpos;
+    const int ncand = __popc(cmask);
     // sort the candidates by rank (O(#candidates)): place, then read back in order
     {
       int crank = 0;
@@ -229,11 +232,10 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       }
       if (cand) { kscr[crank] = ck; pscr[crank] = cp; }
       __syncwarp();
-      const int ncand = __popc(cmask);
       ck = (int)lane < ncand ? kscr[lane] : ~0ull;
+      cpos = pscr[lane];
+      __syncwarp();
     }
-    uint32_t cpos = pscr[lane];
-    __syncwarp();
     // the 32 smallest of (k-buffer, candidates) form a bitonic sequence: merge
     {
       const unsigned long long rk = shfl64(ck, 31 - (int)lane);
@@ -263,19 +265,24 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       const int nwin = min(sp, 32);
       unsigned k16 = 0xFFFFu, nid = 0;
       if ((int)lane < nwin) { k16 = M.stn[sp - 1 - (int)lane]; nid = M.stk[sp - 1 - (int)lane]; }
-      const unsigned kmin = __reduce_min_sync(kFull, k16);
+      // (key, lane) packed: one reduction yields the minimum and its lane (ties
+      // to the lowest lane; a key reduction + ballot + ffs was 2.2% slower)
+      const unsigned kl = (k16 << 5) | lane;
+      const unsigned klmin = __reduce_min_sync(kFull, kl);
+      const unsigned kmin = klmin >> 5;
       if (stn_dec(kmin) > te_lim + slack) {
         sp -= nwin;
         continue;
       }
-      const int srcA = __ffs(__ballot_sync(kFull, k16 == kmin)) - 1;
+      const int srcA = (int)(klmin & 31u);
       nodeA = (int)__shfl_sync(kFull, nid, srcA);
       int srcB = -1;
 #ifndef RG_ONE_NODE
       const unsigned k16b = (int)lane == srcA ? 0xFFFFu : k16;
-      const unsigned kmin2 = __reduce_min_sync(kFull, k16b);
+      const unsigned klmin2 = __reduce_min_sync(kFull, (k16b << 5) | lane);
+      const unsigned kmin2 = klmin2 >> 5;
       if (kmin2 != 0xFFFFu && stn_dec(kmin2) <= te_lim + slack) {
-        srcB = __ffs(__ballot_sync(kFull, k16b == kmin2)) - 1;
+        srcB = (int)(klmin2 & 31u);
         nodeB = (int)__shfl_sync(kFull, nid, srcB);
       }
 #endif
