@@ -431,9 +431,9 @@ __global__ void k_collapse_init(int n, const float* leaf_box, WideNode* wide, in
 // node's two child boxes, a leaf's its padded AABB; the topology is kept.
 __global__ void __launch_bounds__(128) k_wide_refit(const float4* nodes, const float* leaf_box,
                                                     const int* wide_src, const int* counts,
-                                                    WideNode* wide) {
+                                                    WideNode* wide, int capacity) {
   const int lane = threadIdx.x & 31;
-  const int nw = counts[0];
+  const int nw = min(counts[0], capacity);
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nw;
        w += (gridDim.x * blockDim.x) >> 5) {
     WideNode& W = wide[w];
@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(128) k_wide_refit(const float4* nodes, const f
 // left child in place, right child appended; no local-memory candidate arrays.
 // Bulk reservations of wide ids and queue slots per item.
 __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, WideNode* wide, int2* q,
-                                                       int* wide_src, int* counts) {
+                                                       int* wide_src, int* counts, int capacity) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   volatile int* vc = counts;
@@ -497,6 +497,10 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
     if (!have) return;
     raw = __shfl_sync(full, raw, 0);
     const int jb = (int)(raw & 0xFFFFFFFF), jw = (int)(raw >> 32);
+    if (jw < 0) {                                     // no-op item (capacity guard)
+      if (lane == 0) atomicAdd(counts + 2, 1);
+      continue;
+    }
     // entries 0, 1: the binary node's children
     int id = -1;
     float b[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -561,9 +565,17 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
     if (internal) {
       const int rk = __popc(im & ((1u << lane) - 1u));
       const int wid = wid0 + rk;
-      wide_src[wid] = id;
-      vq[qs0 + rk] = ((long long)wid << 32) | (unsigned)id;   // publish with one store
-      child = wid;
+      if (wid < capacity) {
+        wide_src[wid] = id;
+        vq[qs0 + rk] = ((long long)wid << 32) | (unsigned)id;   // publish with one store
+        child = wid;
+      } else {
+        // beyond the proven wide_capacity bound (cannot happen): flag, drop the subtree
+        // and publish a no-op item (wide id -1) so that the queue still drains
+        counts[3] = 1;
+        vq[qs0 + rk] = (long long)(~0ull << 32) | (unsigned)id;
+        child = kWideEmpty;
+      }
     }
     WideNode& W = wide[jw];
     W.lox[lane] = b[0]; W.loy[lane] = b[1]; W.loz[lane] = b[2];
@@ -575,9 +587,10 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
   }
 }
 
-// error flag: unfinished items or wide-node capacity exceeded
+// error flag: unfinished items or wide-node capacity exceeded (the guard in
+// k_collapse_warp may already have set it)
 __global__ void k_collapse_check(int* counts, int capacity) {
-  counts[3] = (counts[2] != counts[4] || counts[0] > capacity) ? 1 : 0;
+  counts[3] = (counts[3] != 0 || counts[2] != counts[4] || counts[0] > capacity) ? 1 : 0;
 }
 
 inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -686,8 +699,8 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // all blocks co-resident (waiting threads spin): 2 blocks of 128 per SM
-    k_collapse_warp<<<4 * sms, 128, 0, st>>>(nodes, wide, qa, wsrc, wc);
+    // all blocks co-resident (waiting warps spin): 4 blocks of 128 threads per SM
+    k_collapse_warp<<<4 * sms, 128, 0, st>>>(nodes, wide, qa, wsrc, wc, (int)wide_capacity(n));
     k_collapse_check<<<1, 1, 0, st>>>(wc, (int)wide_capacity(n));
     count_launches(2);
   }
@@ -734,7 +747,7 @@ cudaError_t launch_refit(const rg_gaussians& g, const rg_config& c, char* ws, co
                                       wc);
   } else {
     const int wblocks = min((int)((wide_capacity(n) + 3) / 4), 148 * 8);
-    k_wide_refit<<<wblocks, 128, 0, st>>>(nodes, leaf_box, wsrc, wc, wide);
+    k_wide_refit<<<wblocks, 128, 0, st>>>(nodes, leaf_box, wsrc, wc, wide, (int)wide_capacity(n));
   }
   count_launches(1);
   return cudaGetLastError();

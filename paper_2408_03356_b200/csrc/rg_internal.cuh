@@ -61,7 +61,15 @@ struct WideNode {
   float lox[kWide], loy[kWide], loz[kWide], hix[kWide], hiy[kWide], hiz[kWide];
   int child[kWide];
 };
-__host__ __device__ constexpr size_t wide_capacity(int n) { return (size_t)(n / 2 + 2); }
+// Upper bound on the wide-node count of the greedy collapse: a wide node with
+// fewer than 32 entries holds only leaves (>= 2 of them), so there are at most
+// n/2 such nodes; every other node has 32 entries, and entries = (W - 1) + n,
+// which bounds the full ones by (n - 1 - W_partial)/31.  Hence
+// W <= n/2 + (n/2)/31 + 1 (a balanced grid scene reaches 33825 of 33827 at
+// n = 65536).
+__host__ __device__ constexpr size_t wide_capacity(int n) {
+  return (size_t)(n / 2 + n / 62 + 4);
+}
 
 struct SceneView {
   const float4* geom;

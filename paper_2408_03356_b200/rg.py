@@ -242,6 +242,12 @@ class BVH:
         self.h = handle
         self.scene = scene   # keep parameters alive
 
+    def check(self):
+        """Raise if the build's 32-wide collapse flagged an error (synchronises)."""
+        if self.h.n > 1 and int(self.debug_views()["wide_info"][3].item()) != 0:
+            raise RGError("rg_build_bvh: 32-wide collapse error (rg_bvh.wide_info[3])")
+        return self
+
     def debug_views(self):
         """Device arrays of the build for parity tests."""
         n = self.h.n
@@ -280,9 +286,11 @@ def bvh_workspace(scene: Gaussians):
     return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=scene.mean.device)
 
 
-def build_bvh(scene: Gaussians, cfg: Config, ws=None) -> BVH:
+def build_bvh(scene: Gaussians, cfg: Config, ws=None, check=False) -> BVH:
     """Full LBVH rebuild (UpdateBVH).  `ws` (from bvh_workspace) may be
-    reused across calls; the returned BVH is valid until ws is rebuilt."""
+    reused across calls; the returned BVH is valid until ws is rebuilt.
+    check=True synchronises and raises if the 32-wide collapse reported an
+    error (rg_bvh.wide_info[3])."""
     _require_cuda()
     L = lib()
     nbytes = int(L.rg_bvh_workspace_bytes(scene.n, scene.sh_degree, scene.sg_count))
@@ -294,7 +302,10 @@ def build_bvh(scene: Gaussians, cfg: Config, ws=None) -> BVH:
     gs, cs = scene.struct(), cfg.struct()
     _check(L.rg_build_bvh(C.byref(gs), C.byref(cs), _ptr(ws), nbytes, C.byref(h), _stream()),
            "rg_build_bvh")
-    return BVH(ws, h, scene)
+    b = BVH(ws, h, scene)
+    if check:
+        b.check()
+    return b
 
 
 def refit_bvh(bvh: BVH, scene: Gaussians, cfg: Config) -> BVH:
@@ -331,17 +342,43 @@ def camera_rays(cam, device="cuda"):
     return o, d
 
 
-def _ray_args(rays, camera):
+def _device_f32(t, shape, what, device):
+    """Validated contiguous fp32 device tensor for a raw pointer argument: the
+    returned tensor must be kept alive until the launch has been enqueued."""
+    if not isinstance(t, torch.Tensor):
+        raise RGError(f"{what}: expected a torch tensor")
+    if t.device != torch.device(device):
+        raise RGError(f"{what}: on {t.device}, expected {device}")
+    if tuple(t.shape) != tuple(shape):
+        raise RGError(f"{what}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    return t.contiguous().float()
+
+
+def _ray_args(rays, camera, device):
     if (rays is None) == (camera is None):
         raise RGError("pass exactly one of rays=(origin, dir) or camera=")
     if rays is not None:
         o, d = rays
+        n = int(o.shape[0]) if isinstance(o, torch.Tensor) and o.dim() == 2 else -1
+        o = _device_f32(o, (n, 3), "ray origins", device)
+        d = _device_f32(d, (n, 3), "ray directions", device)
         r = _Rays()
-        r.n = int(o.shape[0])
-        r.origin, r.dir = _ptr(o.contiguous()), _ptr(d.contiguous())
+        r.n = n
+        r.origin, r.dir = _ptr(o), _ptr(d)
         return C.byref(r), None, r.n, (r, o, d)
     cs = camera_struct(camera)
     return None, C.byref(cs), camera.n_rays, (cs,)
+
+
+def check_stats(stats, what="render"):
+    """Data errors the C-ABI only counts (rg.h: rg_stats) become exceptions here
+    (non-finite gradients must be reported): synchronises on the
+    stats tensor.  Traversal-stack overflow drops subtrees, so it is an error too."""
+    s = stats_dict(stats)
+    if s["nonfinite_grads"]:
+        raise RGError(f"{what}: {s['nonfinite_grads']} non-finite gradient values")
+    if s["stack_overflows"]:
+        raise RGError(f"{what}: {s['stack_overflows']} BVH traversal stack overflows")
 
 
 def new_log(n_rays, device="cuda", pairs_per_ray=0):
@@ -351,12 +388,14 @@ def new_log(n_rays, device="cuda", pairs_per_ray=0):
 
 
 def render_forward(scene: Gaussians, bvh: BVH, cfg: Config, *, rays=None, camera=None,
-                   stats=None, debug=None, out=None, log=None):
+                   stats=None, debug=None, out=None, log=None, check=True):
     """Returns dict(rgb [R,3], T [R], replay [R]) (+ debug counts/records).
-    `log` (from new_log) records the BVH query results for render_backward."""
+    `log` (from new_log) records the BVH query results for render_backward.
+    With `stats` and check=True the counters are read back (a synchronisation)
+    and a traversal-stack overflow raises RGError."""
     _require_cuda()
-    rp, cp, n, keep = _ray_args(rays, camera)
     dev = scene.mean.device
+    rp, cp, n, keep = _ray_args(rays, camera, dev)
     if out is None:
         out = dict(rgb=torch.empty(n, 3, dtype=torch.float32, device=dev),
                    T=torch.empty(n, dtype=torch.float32, device=dev),
@@ -376,6 +415,8 @@ def render_forward(scene: Gaussians, bvh: BVH, cfg: Config, *, rays=None, camera
            "rg_render_forward")
     out["log"] = log
     del keep
+    if stats is not None and check:
+        check_stats(stats, "rg_render_forward")
     return out
 
 
@@ -385,19 +426,28 @@ def backward_workspace(scene: Gaussians):
 
 
 def render_backward(scene: Gaussians, bvh: BVH, cfg: Config, fwd: dict, d_rgb, *, rays=None,
-                    camera=None, grads=None, stats=None, ws=None):
-    """Accumulates dL/dparams for L = sum <d_rgb, rgb> into `grads` (dict of tensors)."""
+                    camera=None, grads=None, stats=None, ws=None, check=True):
+    """Accumulates dL/dparams for L = sum <d_rgb, rgb> into `grads` (dict of tensors).
+    With `stats` and check=True the counters are read back (a synchronisation)
+    and non-finite gradients or a traversal-stack overflow raise RGError."""
     _require_cuda()
-    rp, cp, n, keep = _ray_args(rays, camera)
+    dev = scene.mean.device
+    rp, cp, n, keep = _ray_args(rays, camera, dev)
     if grads is None:
         grads = scene.zeros_like_grads()
     if ws is None:
         ws = backward_workspace(scene)
     g = _Grads()
     for k in GROUPS:
-        setattr(g, k, _ptr(grads[k]))
+        t = grads[k]
+        ref = getattr(scene, k)
+        if (t.dtype != torch.float32 or not t.is_contiguous() or t.device != dev
+                or t.shape != ref.shape):
+            raise RGError(f"grads[{k!r}]: need a contiguous fp32 tensor of shape "
+                          f"{tuple(ref.shape)} on {dev}")
+        setattr(g, k, _ptr(t))
     gs, cs = scene.struct(), cfg.struct()
-    d_rgb = d_rgb.contiguous()
+    d_rgb = _device_f32(d_rgb, (n, 3), "d_rgb", dev)
     log = fwd.get("log")
     lw = int(log.numel()) if log is not None else 0
     _check(lib().rg_render_backward(C.byref(gs), C.byref(bvh.h), C.byref(cs), rp, cp,
@@ -405,6 +455,8 @@ def render_backward(scene: Gaussians, bvh: BVH, cfg: Config, fwd: dict, d_rgb, *
                                     _ptr(log), lw, _ptr(d_rgb), C.byref(g), _ptr(stats), _ptr(ws),
                                     ws.numel() * 4, _stream()), "rg_render_backward")
     del keep
+    if stats is not None and check:
+        check_stats(stats, "rg_render_backward")
     return grads
 
 

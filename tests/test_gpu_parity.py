@@ -4,7 +4,8 @@ same seeded inputs.  Bars (BASELINE.json north star):
     rays, per-slab hit sets (debug dump), counters that count decisions;
   * pixels: max |rgb_gpu - rgb_oracle| <= 1e-4 (termination-flip exemption:
     oracle T within 1e-3 relative of T_eps at the flipped slab end);
-  * gradients: per group ||g - g_ref||_inf / ||g_ref||_inf <= 1e-3.
+  * gradients: per group ||g - g_ref||_inf / ||g_ref||_inf <= 1e-3, and
+    elementwise rel <= 1e-3 wherever |g_ref| >= 1e-2 ||g_ref||_inf.
 """
 import numpy as np
 import pytest
@@ -102,35 +103,44 @@ def test_build_bitexact(oracle, kind, n):
 
 
 def check_wide_tree(b, ref, n):
-    """32-wide collapse: every leaf exactly once, every wide child box equals
-    the exact union of the leaf boxes below it, no unfinished collapse round."""
+    """32-wide collapse (vectorised, any n): every wide child box equals the
+    exact box of what it points at (a leaf's padded AABB, or the union of the
+    child wide node's boxes), every leaf appears exactly once, every wide node
+    but the root is referenced exactly once and is reachable from the root,
+    the root's union is the scene box, no collapse error was flagged."""
     info = b.debug_views()["wide_info"].cpu().numpy()
     assert info[3] == 0
     wf, wi = b.wide_nodes()
     wf, wi = wf.cpu().numpy(), wi.cpu().numpy()
-    seen = np.zeros(n, int)
-
-    def walk(w):
-        lo = np.full(3, np.inf, np.float32); hi = np.full(3, -np.inf, np.float32)
-        for k in range(32):
-            ch = wi[w, 6, k]
-            if ch == 0x7FFFFFFF:
-                continue
-            cb = wf[w, :6, k]
-            if ch < 0:
-                seen[~ch] += 1
-                sub = ref.leaf_boxes[~ch]
-            else:
-                sub = walk(ch)
-            assert np.array_equal(cb, sub)
-            lo = np.minimum(lo, sub[:3]); hi = np.maximum(hi, sub[3:])
-        return np.concatenate([lo, hi])
-    if n >= 1 and n <= 300_000:
-        import sys
-        sys.setrecursionlimit(10000)
-        root = walk(0)
-        assert np.array_equal(root, ref.root)
-        assert np.all(seen == 1)
+    W = wf.shape[0]
+    ch = wi[:, 6, :]                                   # [W, 32]
+    box = wf[:, :6, :].transpose(0, 2, 1)              # [W, 32, 6]
+    empty = ch == 0x7FFFFFFF
+    leaf = (ch < 0) & ~empty
+    inner = (ch >= 0) & ~empty
+    # leaves exactly once
+    lid = ~ch[leaf]
+    assert np.array_equal(np.sort(lid), np.arange(n))
+    assert np.array_equal(box[leaf], ref.leaf_boxes[lid])
+    # union of each wide node's live child boxes
+    lo = np.where(empty[..., None], np.inf, box[..., :3]).min(1)
+    hi = np.where(empty[..., None], -np.inf, box[..., 3:]).max(1)
+    uni = np.concatenate([lo, hi], 1).astype(np.float32)
+    cid = ch[inner]
+    assert np.array_equal(np.sort(cid), np.arange(1, W))   # each non-root node once
+    assert np.array_equal(box[inner], uni[cid])
+    assert np.array_equal(uni[0], ref.root)
+    # reachability from the root (no detached cycles)
+    seen = np.zeros(W, bool)
+    seen[0] = True
+    front = np.array([0])
+    while front.size:
+        c = ch[front]
+        nxt = c[(c >= 0) & (c != 0x7FFFFFFF)]
+        assert not seen[nxt].any()
+        seen[nxt] = True
+        front = nxt
+    assert seen.all()
 
 
 def test_camera_rays_bitexact(oracle):
@@ -248,7 +258,13 @@ def test_forward_full_size_sampled(oracle, name):
 # backward (a11-a12)
 # ---------------------------------------------------------------------------
 
-def grad_check(gpu, ref, tol=GRAD_TOL):
+def grad_check(gpu, ref, tol=GRAD_TOL, rel_floor=1e-2):
+    """North star: per-parameter gradient relative error <= 1e-3 (fp32).  Two
+    bars per group (last pin row): the group's max error
+    relative to its largest reference value, and the ELEMENTWISE relative
+    error of every element whose reference magnitude is at least
+    rel_floor x the group's largest (below that, fp32 atomics reorder sums of
+    much larger terms, so only the group-relative bar applies)."""
     for k, r in ref.items():
         if r.size == 0:
             continue
@@ -259,6 +275,11 @@ def grad_check(gpu, ref, tol=GRAD_TOL):
             continue
         err = np.abs(gv - r).max() / scale
         assert err <= tol, (k, err)
+        big = np.abs(r) >= rel_floor * scale
+        rel = np.abs(gv[big] - r[big]) / np.abs(r[big])
+        worst = int(np.argmax(rel))
+        assert rel[worst] <= tol, (k, "elementwise", float(rel[worst]), float(r[big][worst]),
+                                   float(gv[big][worst]), int(big.sum()))
 
 
 @pytest.mark.parametrize("seed,deg,sg,n", [(0, 3, 7, 60), (1, 1, 2, 150), (2, 0, 0, 40)])

@@ -161,6 +161,46 @@ def test_single_gaussian_closed_form(oracle, aniso):
         assert np.allclose(r["rgb"][0], c * (1 - T) + T, atol=1e-12)
 
 
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_density_weighted_colour_colocated(oracle, mode):
+    """Eq. 10-11: the colour of a sample is the DENSITY-weighted
+    mean c_k = sum_l sigma_l(x) c_l / sum_l sigma_l(x).  Co-located Gaussians
+    (same mu, q, s; k-sigma supports, so identical chords) have
+    sigma_l(x) = sigma~_l G(x), hence c_k = sum sigma~_l c_l / sum sigma~_l at
+    EVERY sample and, by telescoping Eq. 4, pixel = c_bar (1 - T) + T bg
+    exactly.  Weighting by G alone (unweighted mean of the c_l), or by
+    sigma~ twice, fails this."""
+    rng = np.random.default_rng(31)
+    dens = [7.0, 23.0, 2.5]
+    cols = np.array([[0.9, 0.1, 0.3], [0.2, 0.8, 0.5], [0.05, 0.4, 0.95]])
+    q = rng.normal(size=4); q /= np.linalg.norm(q)
+    sv = np.float32([0.12, 0.07, 0.2])
+    n = 3
+    sc = synth.Scene(np.zeros((n, 3), np.float32) + np.float32([0.1, -0.05, 0.02]),
+                     np.tile(np.float32(q), (n, 1)), np.tile(sv, (n, 1)),
+                     np.float32(dens), (cols / Y00).astype(np.float32)[:, None, :],
+                     np.zeros((n, 0, 3), np.float32), np.zeros((n, 0), np.float32),
+                     np.zeros((n, 0, 3), np.float32), 0, 0)
+    bg = (0.3, 0.6, 0.1)
+    p = synth.RenderParams(dt=2e-3, slab_samples=8, sigma_eps=0.1, t_eps=0.0, background=bg,
+                           radius_mode=1, k_sigma=3.0)
+    o, d = synth.random_rays(32, 64, radius=2.0, jitter=0.15)
+    r = oracle.render(sc, p, o, d, mode=mode)
+    # c~ is stored in fp32: the colour the oracle sees is fp32(c/Y00) * Y00
+    c_eff = (cols / Y00).astype(np.float32).astype(np.float64) * Y00
+    w = np.float32(dens).astype(np.float64)
+    cbar = (w[:, None] * c_eff).sum(0) / w.sum()
+    T = r["T"][:, None]
+    hit = r["T"] < 1.0
+    assert hit.sum() >= 20
+    bg32 = np.float32(bg).astype(np.float64)      # rg_config.background is fp32
+    expect = cbar[None, :] * (1.0 - T) + T * bg32[None, :]
+    assert np.abs(r["rgb"] - expect).max() <= 1e-12
+    # the unweighted mean differs by far more than the tolerance on these rays
+    wrong = c_eff.mean(0)[None, :] * (1.0 - T) + T * bg32[None, :]
+    assert np.abs(r["rgb"][hit] - wrong[hit]).max() > 1e-2
+
+
 def test_conservation_white_scene(oracle):
     """c == 1 everywhere, bg = 0: C + T = 1."""
     sc = synth.random_scene(20, 40, sh_degree=0)
