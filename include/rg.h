@@ -76,6 +76,11 @@ typedef struct {
   int32_t basis;         /* basis function phi (supplementary P:456-515, L33):
                             RG_BASIS_* below; non-Gaussian bases need radius_mode 0 and
                             slab_samples >= 5 (else RG_ERR_NOT_IMPLEMENTED) */
+  int32_t list_capacity; /* forward kernel-variant hint, results identical either way:
+                            0 = the 64-slot per-ray active list; > 64 = a 544-slot list
+                            (hit_capacity < 544, Gaussian basis, slab_samples >= 5) that
+                            holds whole truncated slab sets (K-saturated scenes such as
+                            C4) instead of re-querying the BVH for every slab */
 } rg_config;
 
 enum { RG_BASIS_GAUSSIAN = 0, RG_BASIS_BUMP = 1, RG_BASIS_WENDLAND = 2,
@@ -91,7 +96,15 @@ typedef struct {
 /* Pinhole camera: one ray through each pixel centre of the
    rectangle [x0,x1) x [y0,y1); rays are numbered row-major inside the
    rectangle.  c2w is HOST data (passed by value to the kernel): 3x4 row-major
-   [right | down | forward | eye]. */
+   [right | down | forward | eye].
+   Interleaved tile sharding (rays are independent):
+   tile > 0 cuts the rectangle into tile x tile squares numbered row-major
+   (ragged squares at the right and bottom edges) and this call renders only
+   the squares k with k % shards == shard.  Rays are then numbered
+   i * tile^2 + ly * tile + lx for the i-th owned square and the pixel (lx, ly)
+   inside it; slots of a ragged square outside the rectangle are rendered as
+   misses (rgb = background, T = 1, replay = -1) and get no gradient.
+   rg_camera_ray_count gives the number of ray slots. */
 typedef struct {
   int32_t width, height, x0, y0, x1, y1;
   float fx, fy, cx, cy;
@@ -100,8 +113,15 @@ typedef struct {
                             a 2x2 grid at offsets 1/4, 3/4; L29).  Rays are
                             numbered pixel * spp + (sx + 2 sy); rg_supersample_resolve /
                             rg_supersample_spread map between rays and pixels. */
+  int32_t tile;          /* 0: the whole rectangle; else the square size (even, 2..256;
+                            spp must be 1) of the interleaved tile sharding above */
+  int32_t shard, shards; /* owned squares: k % shards == shard (0 <= shard < shards) */
   int32_t pad_;
 } rg_camera;
+
+/* Number of rays (ray slots) rg_render_forward / rg_camera_rays produce for cam
+   (host; 0 for an invalid camera). */
+int64_t rg_camera_ray_count(const rg_camera* cam);
 
 /* BVH handle filled by rg_build_bvh: device pointers into the caller's
    workspace.  Valid until the workspace is reused or the parameters change
@@ -131,9 +151,11 @@ typedef struct {
   unsigned long long overflows;      /* slabs truncated to K */
   unsigned long long fetches;        /* BVH traversals */
   unsigned long long node_visits;    /* internal nodes visited */
-  unsigned long long stack_overflows;
+  unsigned long long stack_overflows; /* restart-query stack overflows (subtrees dropped) */
   unsigned long long nonfinite_grads;
-  unsigned long long pad_[5];
+  unsigned long long restarts;       /* persistent-traversal restarts after a frontier or
+                                        candidate overflow (exact: no key is lost) */
+  unsigned long long pad_[4];
 } rg_stats;
 
 /* static string for a status code (host) */
@@ -171,7 +193,8 @@ rg_status rg_refit_bvh(const rg_gaussians* g, const rg_config* cfg, void* ws, si
                        rg_bvh* bvh, void* stream);
 
 /* ---- rays -------------------------------------------------------------- */
-/* Writes the camera's rays (ARITH-7) to device o/d [R,3]. */
+/* Writes the camera's rays (ARITH-7) to device o/d [R,3], R = rg_camera_ray_count
+   (ray slots outside the rectangle of a tile-sharded camera get o = d = 0). */
 rg_status rg_camera_rays(const rg_camera* cam, float* origin, float* dir, void* stream);
 
 /* ---- forward (a6-a10) ---------------------------------------------------- */

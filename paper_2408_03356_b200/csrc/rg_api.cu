@@ -28,6 +28,7 @@ bool config_ok(const rg_config* c) {
   if (!isfinite(c->t_near)) return false;
   if (c->basis < 0 || c->basis > 5) return false;
   if (c->basis != 0 && c->radius_mode != 0) return false;
+  if (c->list_capacity < 0) return false;
   return true;
 }
 
@@ -55,6 +56,11 @@ bool rays_ok(const rg_rays* r, const rg_camera* cam) {
   if (cam->x0 < 0 || cam->y0 < 0 || cam->x1 < cam->x0 || cam->y1 < cam->y0) return false;
   if (!(cam->fx != 0.0f) || !(cam->fy != 0.0f)) return false;
   if (cam->spp != 1 && cam->spp != 4) return false;
+  if (cam->tile != 0) {
+    if (cam->tile < 2 || cam->tile > 256 || (cam->tile & 1) || cam->spp != 1) return false;
+    if (cam->shards < 1 || cam->shard < 0 || cam->shard >= cam->shards) return false;
+  }
+  if (camera_ray_slots(*cam) > 0x7FFFFFFF) return false;
   return true;
 }
 
@@ -244,9 +250,14 @@ rg_status rg_densify_apply(const rg_gaussians* g, const rg_param_arrays* in,
                            static_cast<cudaStream_t>(stream)) == cudaSuccess ? RG_OK : RG_ERR_CUDA;
 }
 
+int64_t rg_camera_ray_count(const rg_camera* cam) {
+  if (!cam || !rays_ok(nullptr, cam)) return 0;
+  return camera_ray_slots(*cam);
+}
+
 rg_status rg_camera_rays(const rg_camera* cam, float* origin, float* dir, void* stream) {
   if (!cam || !rays_ok(nullptr, cam)) return RG_ERR_INVALID_ARG;
-  const int n = (cam->x1 - cam->x0) * (cam->y1 - cam->y0);
+  const int64_t n = camera_ray_slots(*cam);
   if (n > 0 && (!origin || !dir)) return RG_ERR_INVALID_ARG;
   return launch_camera_rays(*cam, origin, dir, static_cast<cudaStream_t>(stream)) == cudaSuccess
              ? RG_OK
@@ -261,7 +272,7 @@ rg_status rg_render_forward(const rg_gaussians* g, const rg_bvh* bvh, const rg_c
   if (!gaussians_ok(g) || !config_ok(cfg) || !bvh_ok(bvh, g) || !rays_ok(rays, cam))
     return RG_ERR_INVALID_ARG;
   if (cfg->basis != 0 && cfg->slab_samples < 5) return RG_ERR_NOT_IMPLEMENTED;
-  const int64_t n = rays ? rays->n : (int64_t)(cam->x1 - cam->x0) * (cam->y1 - cam->y0) * cam->spp;
+  const int64_t n = rays ? rays->n : camera_ray_slots(*cam);
   if (n > 0 && (!rgb || !T || !replay)) return RG_ERR_INVALID_ARG;
   if (debug_records && (debug_rays < 0 || debug_cap < 1 || !debug_counts))
     return RG_ERR_INVALID_ARG;
@@ -297,7 +308,7 @@ rg_status rg_render_backward(const rg_gaussians* g, const rg_bvh* bvh, const rg_
   if (!gaussians_ok(g) || !config_ok(cfg) || !bvh_ok(bvh, g) || !rays_ok(rays, cam) || !grads)
     return RG_ERR_INVALID_ARG;
   if (cfg->basis != 0 && cfg->slab_samples < 5) return RG_ERR_NOT_IMPLEMENTED;
-  const int64_t n = rays ? rays->n : (int64_t)(cam->x1 - cam->x0) * (cam->y1 - cam->y0) * cam->spp;
+  const int64_t n = rays ? rays->n : camera_ray_slots(*cam);
   if (n > 0 && (!rgb || !replay || !d_rgb)) return RG_ERR_INVALID_ARG;
   if (!ws || (reinterpret_cast<uintptr_t>(ws) & 15) != 0) return RG_ERR_INVALID_ARG;
   if (ws_bytes < rg_backward_workspace_bytes(g->n, g->sh_degree, g->sg_count))

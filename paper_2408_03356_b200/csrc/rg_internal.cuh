@@ -212,6 +212,30 @@ __device__ __forceinline__ void camera_ray(const rg_camera& cam, int px, int py,
   o = make_float3(M[3], M[7], M[11]);
 }
 
+// camera ray slots (rg.h): the rectangle x spp, or the owned squares x tile^2
+__host__ __device__ inline int64_t camera_squares_x(const rg_camera& c) {
+  return c.tile > 0 ? ((int64_t)(c.x1 - c.x0) + c.tile - 1) / c.tile : 0;
+}
+__host__ __device__ inline int64_t camera_owned_squares(const rg_camera& c) {
+  if (c.tile <= 0) return 0;
+  const int64_t nsq = camera_squares_x(c) * (((int64_t)(c.y1 - c.y0) + c.tile - 1) / c.tile);
+  return c.shard < nsq ? (nsq - c.shard + c.shards - 1) / c.shards : 0;
+}
+__host__ __device__ inline int64_t camera_ray_slots(const rg_camera& c) {
+  if (c.tile > 0) return camera_owned_squares(c) * c.tile * c.tile;
+  return (int64_t)(c.x1 - c.x0) * (c.y1 - c.y0) * c.spp;
+}
+// tile-sharded slot -> pixel of the rectangle (false: outside, a miss)
+__host__ __device__ inline bool camera_tile_pixel(const rg_camera& c, int64_t slot, int& px, int& py) {
+  const int64_t t2 = (int64_t)c.tile * c.tile;
+  const int64_t i = slot / t2, r = slot - i * t2;
+  const int64_t k = c.shard + i * c.shards;
+  const int64_t nsx = camera_squares_x(c);
+  px = (int)((k % nsx) * c.tile + r % c.tile);
+  py = (int)((k / nsx) * c.tile + r / c.tile);
+  return px < c.x1 - c.x0 && py < c.y1 - c.y0;
+}
+
 // ARITH-9
 __device__ __forceinline__ float sample_t(int k, float dt, float t0) {
   return fma_(add_((float)k, 0.5f), dt, t0);

@@ -29,6 +29,8 @@
 #include "rg_internal.cuh"
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 namespace rg {
 
 namespace {
@@ -69,7 +71,7 @@ constexpr int kStkBwd = 192;
 constexpr unsigned kFull = 0xffffffffu;
 
 struct Counters {
-  uint32_t slabs, pairs, evals, samples, overflows, fetches, nodes, stackov;
+  uint32_t slabs, pairs, evals, samples, overflows, fetches, nodes, stackov, restarts;
 };
 
 struct RenderArgs {
@@ -106,16 +108,68 @@ struct RenderArgs {
 
 // per-slot entry (AoS, three float4 so a lane reads a slot with LDS.128):
 //   e0 = {t_entry, t_exit, t_mid, c0}   e1 = {c1, c2, r, g}   e2 = {b, pos, idx, -}
-template <int STK>
+// per-ray state of the persistent traversal (stream_next, below)
+struct Stream {
+  int nf, qn, ch, cn;                 // frontier size, queued leaves, candidate head / count
+  unsigned long long lim, c0;         // completeness bound, restart cursor
+  bool valid;
+};
+
+template <int STK, int NCAP, int CCAP, int KA = kA, int SLOTS = kSlots>
 struct WarpMemT {
   static constexpr int kStack = STK;
-  float4 e0[kSlots], e1[kSlots], e2[kSlots];
-  uint32_t stk[STK];   // stacked wide node ids
-  uint16_t stn[STK];  // their boxes' entry distances as 16-bit order keys (fp16 rounded
-                       // down): pop-time selection and pruning
-  uint32_t lq[96];     // fetch: queued leaves awaiting the exact test (< 32 + 2 x 32)
+  static constexpr int kNCap = NCAP;
+  static constexpr int kCCap = CCAP;
+  static constexpr int kList = KA;     // active-list capacity
+  static constexpr int kTr = KA;       // first transient slot (restart-query scratch)
+  float4 e0[SLOTS], e1[SLOTS], e2[SLOTS];
+  union {
+    struct {             // restart query (fetch)
+      uint32_t stk[STK];   // stacked wide node ids
+      uint16_t stn[STK];   // their boxes' entry distances as 16-bit order keys (fp16 rounded
+                           // down): pop-time selection and pruning
+    } r;
+    struct {             // persistent per-ray traversal (stream_next); clobbered by fetch
+      uint32_t nk[NCAP];   // node frontier: fkey of a lower bound on every t_entry below
+      uint32_t nid[NCAP];  //   the node, and the wide node id (unsorted)
+      unsigned long long ck[CCAP];   // exact-tested candidates, sorted by (t_entry key, index)
+      uint32_t cp[CCAP];   //   and their Morton positions
+      uint32_t lqk[NCAP > 1 ? 96 : 1];   // box-entry lower bounds of the queued leaves (fkey)
+    } s;
+  } u;
+  uint32_t lq[96];     // queued leaves awaiting the exact test (< 32 + 2 x 32)
+  Stream sst;          // stream_next state between refills (registers only inside the call)
   alignas(16) float Y[16];   // Y(d) of the ray (zero past the degree), read as float4 by the scatter
 };
+// Persistent per-ray traversal (stream_next) for the forward refills: built, measured
+// and kept as a compile-time option (RG_STREAM=1), OFF by default: it cut C1 node visits
+// by 35% but was slower (C1 forward 7.1 -> 9.5-10.2 ms, C3 334 -> 554 ms: its frontier
+// bookkeeping costs more per visit and C3 rays hit ~1000 distinct wide nodes anyway, so
+// the restarts it removes were not the cost)
+#ifndef RG_STREAM
+#define RG_STREAM 0
+#endif
+#ifndef RG_NCAP
+#define RG_NCAP 192
+#endif
+#ifndef RG_CCAP
+#define RG_CCAP 96
+#endif
+#ifndef RG_STREAM_FROM
+#define RG_STREAM_FROM 0       // forward refills served by restart queries before the stream
+#endif
+constexpr bool kStream = RG_STREAM != 0;
+constexpr int kNCap = kStream ? RG_NCAP : 1;   // forward node-frontier capacity (stream_next)
+constexpr int kCCap = kStream ? RG_CCAP : 32;  // forward candidate capacity (stream_next)
+static_assert(kCCap % 32 == 0 && kCCap <= 128, "candidate merge reads CCAP/32 entries per lane");
+using WMFwd = WarpMemT<kStkFwd, kNCap, kCCap>;
+using WMBwd = WarpMemT<kStkBwd, 1, 1>;     // the backward refills by restart queries only
+// forward "large list" variant (rg_config.list_capacity > 64): an active list that holds
+// every member of a slab up to K = 519 (C4 stress: per-slab sets of ~1000, K = 512), so
+// truncated slabs take the K held smallest keys instead of streaming the rest of every
+// slab with restart queries (C4: 7750 -> ~100 queries per ray); two 4-warp blocks per SM
+constexpr int kABig = 520;
+using WMBig = WarpMemT<320, 1, 32, kABig, kABig + 32>;
 struct WarpAcc {
   float4 a[kSlots];    // Sw, Sw1, Sw2, dc_r
   float2 b[kSlots];    // dc_g, dc_b
@@ -155,6 +209,7 @@ struct Ray {
   float3 o, d, inv, oinv;
 };
 
+
 // entry distance <-> order-preserving 16-bit key (fp16 rounded toward -inf:
 // a decoded key never exceeds the distance, so pruning on it is conservative)
 __device__ __forceinline__ uint16_t stn_enc(float t) {
@@ -178,8 +233,8 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
   const unsigned lt_mask = (1u << lane) - 1u;
   if (lane == 0) cnt.fetches++;
   // candidate sort scratch aliases the transient slots, dead during every fetch
-  unsigned long long* const kscr = reinterpret_cast<unsigned long long*>(&M.e0[kTrans]);
-  uint32_t* const pscr = reinterpret_cast<uint32_t*>(&M.e1[kTrans]);
+  unsigned long long* const kscr = reinterpret_cast<unsigned long long*>(&M.e0[WM::kTr]);
+  uint32_t* const pscr = reinterpret_cast<uint32_t*>(&M.e1[WM::kTr]);
   key = ~0ull;
   pos = 0;
   int nk = 0;
@@ -188,7 +243,7 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
   const float slack = 1e-5f * (fabsf(seg_lo) + fabsf(seg_hi)) + 1e-6f;
   const float lo_s = seg_lo - slack, hi_s = seg_hi + slack;
   int sp = 1, qn = 0;
-  if (lane == 0) { M.stk[0] = 0; M.stn[0] = stn_enc(-INFINITY); }
+  if (lane == 0) { M.u.r.stk[0] = 0; M.u.r.stn[0] = stn_enc(-INFINITY); }
   __syncwarp();
   // Exact leaf tests are batched: box-passing leaves are queued in shared
   // memory and tested 32 at a time (all lanes busy), then the candidates are
@@ -264,7 +319,7 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
     {
       const int nwin = min(sp, 32);
       unsigned k16 = 0xFFFFu, nid = 0;
-      if ((int)lane < nwin) { k16 = M.stn[sp - 1 - (int)lane]; nid = M.stk[sp - 1 - (int)lane]; }
+      if ((int)lane < nwin) { k16 = M.u.r.stn[sp - 1 - (int)lane]; nid = M.u.r.stk[sp - 1 - (int)lane]; }
       // (key, lane) packed: one reduction yields the minimum and its lane (ties
       // to the lowest lane; a key reduction + ballot + ffs was 2.2% slower)
       const unsigned kl = (k16 << 5) | lane;
@@ -289,7 +344,7 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       // remove the popped entries: the surviving top entries (lanes 0, 1) fill the
       // holes the popped ones leave further down
       if (srcB < 0) {
-        if (lane == 0 && srcA != 0) { M.stk[sp - 1 - srcA] = nid; M.stn[sp - 1 - srcA] = (uint16_t)k16; }
+        if (lane == 0 && srcA != 0) { M.u.r.stk[sp - 1 - srcA] = nid; M.u.r.stn[sp - 1 - srcA] = (uint16_t)k16; }
         sp -= 1;
       } else {
         const bool m0 = srcA != 0 && srcB != 0, m1 = srcA != 1 && srcB != 1;
@@ -297,7 +352,7 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
         int hole = -1;
         if (lane == 0 && m0) hole = h1;
         if (lane == 1 && m1) hole = m0 ? h2 : h1;
-        if (hole >= 2) { M.stk[sp - 1 - hole] = nid; M.stn[sp - 1 - hole] = (uint16_t)k16; }
+        if (hole >= 2) { M.u.r.stk[sp - 1 - hole] = nid; M.u.r.stn[sp - 1 - hole] = (uint16_t)k16; }
         sp -= 2;
       }
       __syncwarp();
@@ -343,11 +398,11 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       if (sp + np <= WM::kStack) {
         if (hitA && childA >= 0) {
           const int r = sp + __popc(imA & lt_mask);
-          M.stk[r] = (uint32_t)childA; M.stn[r] = stn_enc(tnA);
+          M.u.r.stk[r] = (uint32_t)childA; M.u.r.stn[r] = stn_enc(tnA);
         }
         if (hitB && childB >= 0) {
           const int r = sp + npA + __popc(imB & lt_mask);
-          M.stk[r] = (uint32_t)childB; M.stn[r] = stn_enc(tnB);
+          M.u.r.stk[r] = (uint32_t)childB; M.u.r.stn[r] = stn_enc(tnB);
         }
         sp += np;
 #ifdef RG_STACK_PROBE
@@ -362,6 +417,320 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
   }
   while (qn > 0) flush(min(qn, 32));
   return nk;
+}
+
+// ---------------------------------------------------------------------------
+// Persistent per-ray traversal of the forward refills: an incremental
+// best-first search (Hjaltason & Samet's incremental nearest neighbour) that
+// emits the ray's Gaussians in exact key order (t_entry bits, index) and
+// expands every wide node at most once per ray -- the restart query `fetch`
+// re-descends from the root for every refill (C3 rays refill 12.5 times and
+// revisit the nodes of every Gaussian still alive).  State kept in shared
+// memory between the refills of a ray:
+//   NF  unexpanded wide nodes, each with a lower bound on every t_entry below it
+//       (the box entry minus the box-test slack);
+//   LQ  box-passing leaves queued for the batched exact test, with the same bound;
+//   CF  exact-tested candidates, sorted by key.
+// A candidate is emitted only when its key lies below every NF / LQ bound, so
+// the emission order is the exact key order and the per-slab sets are those of
+// the restart query.  A frontier or candidate overflow drops the largest new
+// entries and lowers `lim`: the state is complete only below lim, and reaching
+// lim restarts from the root with the last emitted key as the cursor (bounded
+// memory, still exact).  `fetch` (restart queries of the overflow paths)
+// clobbers this state: the caller then clears `valid`.
+
+
+template <class WM>
+__device__ __forceinline__ void stream_restart(WM& M, Stream& st, unsigned long long cursor) {
+  if (lane_id() == 0) { M.u.s.nk[0] = 0u; M.u.s.nid[0] = 0u; }
+  st.nf = 1; st.qn = 0; st.ch = 0; st.cn = 0;
+  st.lim = ~0ull; st.c0 = cursor; st.valid = true;
+  __syncwarp();
+}
+
+// exact test of the first n queued leaves, merge of the hits into CF
+template <class WM>
+__device__ __forceinline__ void stream_flush(const SceneView& S, WM& M, Stream& st, const Ray& R,
+                                             float tlo, float t1, int n) {
+  constexpr int CCAP = WM::kCCap;
+  const unsigned lane = lane_id();
+  unsigned long long* const kscr = reinterpret_cast<unsigned long long*>(&M.e0[WM::kTr]);
+  uint32_t* const pscr = reinterpret_cast<uint32_t*>(&M.e1[WM::kTr]);
+  __syncwarp();
+  const uint32_t cp = (int)lane < n ? M.lq[lane] : 0u;
+  bool cand = false;
+  unsigned long long ck = ~0ull;
+  if ((int)lane < n) {
+    const float4* gp = S.geom + 4 * (size_t)cp;
+    const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2), g3 = __ldg(gp + 3);
+    PairGeom pg;
+    if (isect_exact(g0, g1, g2, g3, R.o, R.d, pg) && pg.tx >= tlo && pg.te <= t1) {
+      ck = ((unsigned long long)fkey(pg.te) << 32) | (uint32_t)__float_as_int(g3.z);
+      cand = ck > st.c0 && ck < st.lim;
+      if (!cand) ck = ~0ull;
+    }
+  }
+  // drop the consumed queue entries
+  {
+    const int rem = st.qn - n;   // < 64 left over
+    const uint32_t mv = (int)lane < rem ? M.lq[n + lane] : 0u;
+    const uint32_t mv2 = (int)lane + 32 < rem ? M.lq[n + 32 + lane] : 0u;
+    const uint32_t mk = (int)lane < rem ? M.u.s.lqk[n + lane] : 0u;
+    const uint32_t mk2 = (int)lane + 32 < rem ? M.u.s.lqk[n + 32 + lane] : 0u;
+    __syncwarp();
+    if ((int)lane < rem) { M.lq[lane] = mv; M.u.s.lqk[lane] = mk; }
+    if ((int)lane + 32 < rem) { M.lq[32 + lane] = mv2; M.u.s.lqk[32 + lane] = mk2; }
+    st.qn = rem;
+  }
+  const unsigned cmask = __ballot_sync(kFull, cand);
+  if (!cmask) { __syncwarp(); return; }
+  const int nc = __popc(cmask);
+  // rank sort of the new candidates into kscr/pscr [0, nc)
+  {
+    int crank = 0;
+    unsigned mm = cmask;
+    while (mm) {
+      const int b = __ffs(mm) - 1;
+      mm &= mm - 1;
+      const unsigned long long kb = shfl64(ck, b);
+      crank += (cand && kb < ck) ? 1 : 0;
+    }
+    if (cand) { kscr[crank] = ck; pscr[crank] = cp; }
+  }
+  __syncwarp();
+  // merge with the sorted CF [ch, ch + cn): destination = own rank + rank in the other list
+  unsigned long long ok[CCAP / 32];
+  uint32_t op[CCAP / 32];
+  int od[CCAP / 32];
+#pragma unroll
+  for (int t = 0; t < CCAP / 32; ++t) {
+    const int i = (int)lane + 32 * t;
+    ok[t] = ~0ull; op[t] = 0u; od[t] = CCAP;
+    if (i < st.cn) {
+      ok[t] = M.u.s.ck[st.ch + i];
+      op[t] = M.u.s.cp[st.ch + i];
+      int lo = 0, len = nc;               // new keys < ok[t]
+      while (len > 0) {
+        const int half = len >> 1;
+        if (kscr[lo + half] < ok[t]) { lo += half + 1; len -= half + 1; } else { len = half; }
+      }
+      od[t] = i + lo;
+    }
+  }
+  unsigned long long nk_ = ~0ull;
+  uint32_t np_ = 0u;
+  int nd = CCAP;
+  if ((int)lane < nc) {
+    nk_ = kscr[lane];
+    np_ = pscr[lane];
+    int lo = 0, len = st.cn;              // old keys < nk_
+    while (len > 0) {
+      const int half = len >> 1;
+      if (M.u.s.ck[st.ch + lo + half] < nk_) { lo += half + 1; len -= half + 1; } else { len = half; }
+    }
+    nd = (int)lane + lo;
+  }
+  __syncwarp();
+  unsigned long long dropped = ~0ull;
+#pragma unroll
+  for (int t = 0; t < CCAP / 32; ++t) {
+    if (od[t] < CCAP) { M.u.s.ck[od[t]] = ok[t]; M.u.s.cp[od[t]] = op[t]; }
+    else if (ok[t] < dropped) dropped = ok[t];
+  }
+  if (nd < CCAP) { M.u.s.ck[nd] = nk_; M.u.s.cp[nd] = np_; }
+  else if (nk_ < dropped) dropped = nk_;
+  const int tot = st.cn + nc;
+  st.ch = 0;
+  st.cn = min(tot, CCAP);
+  if (tot > CCAP) {            // complete only below the smallest dropped key
+    unsigned long long v = dropped;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o = shfl64x(v, off);
+      v = o < v ? o : v;
+    }
+    if (v < st.lim) st.lim = v;
+  }
+  __syncwarp();
+}
+
+// next `want` (<= 32) keys of the ray after `cursor` (lane l < return value
+// holds the l-th key and its position); fewer than `want` = exhausted
+template <class WM>
+__device__ int stream_next(const SceneView& S, WM& M, const Ray& R, float tlo, float t1,
+                           unsigned long long cursor, int want, unsigned long long& key,
+                           uint32_t& pos, Counters& cnt) {
+  constexpr int NCAP = WM::kNCap;
+  const unsigned lane = lane_id();
+  const unsigned lt_mask = (1u << lane) - 1u;
+  if (lane == 0) cnt.fetches++;
+  key = ~0ull;
+  pos = 0;
+  int got = 0;
+  Stream st = M.sst;
+  if (!st.valid) stream_restart(M, st, cursor);
+  const float slack = 1e-5f * (fabsf(tlo) + fabsf(t1)) + 1e-6f;
+  const float hi_s = t1 + slack;
+  float lo_b = tlo;
+  if (st.c0 != 0ull) lo_b = fmaxf(lo_b, fkey_inv((uint32_t)(st.c0 >> 32)));
+  lo_b -= slack;
+  while (true) {
+    // lower bounds: the two smallest node keys (with slots) and the smallest queued leaf
+    unsigned a1 = ~0u, a2 = ~0u;
+    int s1 = 0, s2 = 0;
+    for (int j = (int)lane; j < st.nf; j += 32) {
+      const unsigned k = M.u.s.nk[j];
+      if (k < a1) { a2 = a1; s2 = s1; a1 = k; s1 = j; }
+      else if (k < a2) { a2 = k; s2 = j; }
+    }
+    unsigned qmin = ~0u;
+    for (int j = (int)lane; j < st.qn; j += 32) qmin = min(qmin, M.u.s.lqk[j]);
+    const unsigned mN = __reduce_min_sync(kFull, a1);
+    const unsigned mQ = __reduce_min_sync(kFull, qmin);
+    const unsigned m = min(mN, mQ);
+    const bool open_any = st.nf > 0 || st.qn > 0;
+    unsigned long long bound = open_any ? ((unsigned long long)m << 32) : ~0ull;
+    if (st.lim < bound) bound = st.lim;
+    // emit the candidates below every bound (CF is sorted: a prefix)
+    {
+      const bool can = (int)lane < min(st.cn, 32) && M.u.s.ck[st.ch + (int)lane] < bound;
+      const int e = min(__popc(__ballot_sync(kFull, can)), want - got);
+      if ((int)lane >= got && (int)lane < got + e) {
+        key = M.u.s.ck[st.ch + (int)lane - got];
+        pos = M.u.s.cp[st.ch + (int)lane - got];
+      }
+      st.ch += e;
+      st.cn -= e;
+      got += e;
+      if (got == want) break;
+    }
+    // everything still open lies at or beyond lim: drop it
+    if (open_any && st.lim != ~0ull && ((unsigned long long)m << 32) >= st.lim) {
+      st.nf = 0;
+      st.qn = 0;
+      continue;
+    }
+    if (!open_any) {
+      if (st.lim == ~0ull) break;                       // exhausted
+      // complete only below lim, and every key below lim has been emitted: restart
+      // from the root after max(last emitted key, lim - 1)
+      const unsigned long long last = got > 0 ? shfl64(key, got - 1) : cursor;
+      const unsigned long long c0n = last > st.lim - 1 ? last : st.lim - 1;
+      if (c0n <= st.c0) {
+        // no progress since the last restart (a frontier that cannot hold the ray's
+        // nearby nodes): finish this call with a restart query (always terminates)
+        unsigned long long fk;
+        uint32_t fp;
+        const int g2 = fetch(S, M, R, tlo, t1, last, want - got, fk, fp, cnt);
+        const int src = (int)lane - got;
+        const unsigned long long mk = shfl64(fk, src & 31);
+        const uint32_t mp = __shfl_sync(kFull, fp, src & 31);
+        if (src >= 0 && src < g2) { key = mk; pos = mp; }
+        got += g2;
+        st.valid = false;                               // fetch reused the traversal memory
+        break;
+      }
+      stream_restart(M, st, c0n);
+      lo_b = fmaxf(tlo, fkey_inv((uint32_t)(c0n >> 32))) - slack;
+      if (lane == 0) cnt.restarts++;
+      continue;
+    }
+    // exact-test queued leaves when they bound the emission or fill a batch
+    if (st.qn > 0 && (mQ <= mN || st.qn >= 32)) {
+      stream_flush(S, M, st, R, tlo, t1, min(st.qn, 32));
+      continue;
+    }
+    // expand the nearest node and, if there is one, the second nearest
+    const int srcA = __ffs(__ballot_sync(kFull, a1 == mN)) - 1;
+    const int slotA = __shfl_sync(kFull, s1, srcA);
+    const unsigned c2 = (int)lane == srcA ? a2 : a1;
+    const int sl2 = (int)lane == srcA ? s2 : s1;
+    const unsigned mN2 = __reduce_min_sync(kFull, c2);
+    int slotB = -1;
+    if (mN2 != ~0u && ((unsigned long long)mN2 << 32) < st.lim) {
+      const int srcB = __ffs(__ballot_sync(kFull, c2 == mN2)) - 1;
+      slotB = __shfl_sync(kFull, sl2, srcB);
+    }
+    const int nodeA = (int)M.u.s.nid[slotA];
+    const int nodeB = slotB >= 0 ? (int)M.u.s.nid[slotB] : -1;
+    __syncwarp();
+    if (lane == 0) {        // remove the popped slots (the larger first): the last entry fills
+      int h1 = slotA, h2 = slotB;
+      if (h2 > h1) { const int t = h1; h1 = h2; h2 = t; }
+      int nf = st.nf;
+      if (h1 != nf - 1) { M.u.s.nk[h1] = M.u.s.nk[nf - 1]; M.u.s.nid[h1] = M.u.s.nid[nf - 1]; }
+      --nf;
+      if (h2 >= 0) {
+        if (h2 != nf - 1) { M.u.s.nk[h2] = M.u.s.nk[nf - 1]; M.u.s.nid[h2] = M.u.s.nid[nf - 1]; }
+        --nf;
+      }
+    }
+    st.nf -= nodeB >= 0 ? 2 : 1;
+    __syncwarp();
+    if (lane == 0) cnt.nodes += nodeB >= 0 ? 2 : 1;
+    const bool two = nodeB >= 0;
+    const WideNode& WA = S.wide[nodeA];
+    const WideNode& WB = S.wide[two ? nodeB : nodeA];
+    const int childA = __ldg(&WA.child[lane]);
+    const float alx = __ldg(&WA.lox[lane]), aly = __ldg(&WA.loy[lane]), alz = __ldg(&WA.loz[lane]);
+    const float ahx = __ldg(&WA.hix[lane]), ahy = __ldg(&WA.hiy[lane]), ahz = __ldg(&WA.hiz[lane]);
+    int childB = kWideEmpty;
+    float blx = 0.f, bly = 0.f, blz = 0.f, bhx = 0.f, bhy = 0.f, bhz = 0.f;
+    if (two) {
+      childB = __ldg(&WB.child[lane]);
+      blx = __ldg(&WB.lox[lane]); bly = __ldg(&WB.loy[lane]); blz = __ldg(&WB.loz[lane]);
+      bhx = __ldg(&WB.hix[lane]); bhy = __ldg(&WB.hiy[lane]); bhz = __ldg(&WB.hiz[lane]);
+    }
+    float tnA, tfA, tnB, tfB;
+    box_t(alx, aly, alz, ahx, ahy, ahz, R.inv, R.oinv, tnA, tfA);
+    box_t(blx, bly, blz, bhx, bhy, bhz, R.inv, R.oinv, tnB, tfB);
+    const uint32_t kA_ = fkey(tnA - slack), kB_ = fkey(tnB - slack);
+    const unsigned lim_hi = (unsigned)(st.lim >> 32);
+    const bool hitA = childA != kWideEmpty && tnA <= tfA && tfA >= lo_b && tnA <= hi_s && kA_ <= lim_hi;
+    const bool hitB = childB != kWideEmpty && tnB <= tfB && tfB >= lo_b && tnB <= hi_s && kB_ <= lim_hi;
+    {   // queue box-passing leaves (A's, then B's)
+      const unsigned lmA = __ballot_sync(kFull, hitA && childA < 0);
+      const unsigned lmB = __ballot_sync(kFull, hitB && childB < 0);
+      if (lmA | lmB) {
+        if (hitA && childA < 0) {
+          const int r = st.qn + __popc(lmA & lt_mask);
+          M.lq[r] = (uint32_t)(~childA); M.u.s.lqk[r] = kA_;
+        }
+        if (hitB && childB < 0) {
+          const int r = st.qn + __popc(lmA) + __popc(lmB & lt_mask);
+          M.lq[r] = (uint32_t)(~childB); M.u.s.lqk[r] = kB_;
+        }
+        st.qn += __popc(lmA) + __popc(lmB);
+      }
+    }
+    {   // internal children join the frontier; those beyond its capacity lower lim
+      const unsigned imA = __ballot_sync(kFull, hitA && childA >= 0);
+      const unsigned imB = __ballot_sync(kFull, hitB && childB >= 0);
+      if (imA | imB) {
+        const int npA = __popc(imA), np = npA + __popc(imB);
+        unsigned dk = ~0u;
+        if (hitA && childA >= 0) {
+          const int r = st.nf + __popc(imA & lt_mask);
+          if (r < NCAP) { M.u.s.nk[r] = kA_; M.u.s.nid[r] = (uint32_t)childA; } else dk = kA_;
+        }
+        if (hitB && childB >= 0) {
+          const int r = st.nf + npA + __popc(imB & lt_mask);
+          if (r < NCAP) { M.u.s.nk[r] = kB_; M.u.s.nid[r] = (uint32_t)childB; } else dk = min(dk, kB_);
+        }
+        if (st.nf + np > NCAP) {
+          const unsigned dmin = __reduce_min_sync(kFull, dk);
+          const unsigned long long l2 = (unsigned long long)dmin << 32;
+          if (l2 < st.lim) st.lim = l2;
+        }
+        st.nf = min(st.nf + np, NCAP);
+      }
+    }
+    __syncwarp();
+  }
+  __syncwarp();
+  if (lane == 0) M.sst = st;
+  __syncwarp();
+  return got;
 }
 
 // c_l(d) = sum_m c~_m Y_m(d) + sum_j k_j e^{lambda_j (d.p_j - 1)} (Eq. 14-15):
@@ -719,11 +1088,13 @@ __device__ __forceinline__ int skip_to(float te, int s, int B, float dt, float t
 
 __device__ __forceinline__ void flush_stats(rg_stats* st, const Counters& c, bool hit) {
   const unsigned lane = lane_id();
-  const uint32_t v[10] = {lane == 0 ? 1u : 0u, (lane == 0 && hit) ? 1u : 0u, c.slabs, c.pairs,
-                          c.evals, c.samples, c.overflows, c.fetches, c.nodes, c.stackov};
+  // rg_stats fields 0..9, then restarts at field 11 (field 10 = nonfinite_grads)
+  const uint32_t v[11] = {lane == 0 ? 1u : 0u, (lane == 0 && hit) ? 1u : 0u, c.slabs, c.pairs,
+                          c.evals, c.samples, c.overflows, c.fetches, c.nodes, c.stackov,
+                          c.restarts};
   unsigned long long* dst = reinterpret_cast<unsigned long long*>(st);
 #pragma unroll
-  for (int k = 0; k < 10; ++k) {
+  for (int k = 0; k < 11; ++k) {
     const uint32_t s = __reduce_add_sync(kFull, v[k]);
 #ifdef RG_STACK_PROBE
     if (k == 9) {
@@ -731,7 +1102,7 @@ __device__ __forceinline__ void flush_stats(rg_stats* st, const Counters& c, boo
       continue;
     }
 #endif
-    if (lane == 0 && s) atomicAdd(dst + k, (unsigned long long)s);
+    if (lane == 0 && s) atomicAdd(dst + (k < 10 ? k : k + 1), (unsigned long long)s);
   }
 }
 
@@ -755,24 +1126,54 @@ __device__ __forceinline__ void dbg_put(const RenderArgs& P, int ray, int& dbg_n
   dbg_n = min(P.dbg_cap, dbg_n + n);
 }
 
+// number of held entries with t_entry <= x (the list is sorted by key)
+template <int KA, class WM>
+__device__ __forceinline__ int held_le(const WM& M, int count, float x) {
+  if constexpr (KA == 64) {
+    const unsigned m0 = __ballot_sync(kFull, (int)lane_id() < count && M.e0[lane_id()].x <= x);
+    const unsigned m1 =
+        __ballot_sync(kFull, (int)lane_id() + 32 < count && M.e0[lane_id() + 32].x <= x);
+    return __popc(m0) + __popc(m1);
+  } else {
+    int lo = 0, len = count;      // warp-uniform binary search (broadcast loads)
+    while (len > 0) {
+      const int half = len >> 1;
+      if (M.e0[lo + half].x <= x) { lo += half + 1; len -= half + 1; } else { len = half; }
+    }
+    return lo;
+  }
+}
+
 // INSTR: counters (rg_stats) and the debug dump; the uninstrumented variant
 // compiles them out (8 fewer live registers through the march)
-template <bool BWD, int GW, bool INSTR, int BASIS>
-__global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FWD) k_render(const RenderArgs P) {
+template <bool BWD, int GW, bool INSTR, int BASIS, int KA = kA>
+__global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kA ? RG_MIN_BLOCKS_FWD : 2))
+    k_render(const RenderArgs P) {
+  static_assert(KA == kA || !BWD, "the large-list variant is forward only");
   // static shared memory (fwd 35.6 KB, bwd 48.0 KB <= the 48 KB static limit): constant
   // shared-window offsets; the dynamic (extern) form made the compiler re-derive the
   // window base (S2UR SR_CgaCtaId + ULEA) at loop heads of the hot loops
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const unsigned lane = lane_id();
   const int wid = threadIdx.x >> 5;
-  using WM = WarpMemT<BWD ? kStkBwd : kStkFwd>;
+  using WM = std::conditional_t<BWD, WMBwd, std::conditional_t<KA == kA, WMFwd, WMBig>>;
   WM& M = reinterpret_cast<WM*>(smem_raw)[wid];
   WarpAcc& A = reinterpret_cast<WarpAcc*>(smem_raw + sizeof(WM) * kWarps)[BWD ? wid : 0];
   int ray;
   Ray R;
+  bool inside = true;             // false: a tile-sharding slot outside the rectangle (a miss)
   if (P.cam_mode) {
     const int tile = blockIdx.x;
-    if (P.cam.spp == 1) {         // block = 2x2 pixel tile, warp = pixel
+    if (P.cam.tile > 0) {         // interleaved tile sharding: block = 2x2 pixels of a square
+      const int h = P.cam.tile >> 1;
+      const int i = tile / (h * h), r = tile - i * (h * h);
+      const int lx = 2 * (r % h) + (wid & 1), ly = 2 * (r / h) + (wid >> 1);
+      ray = i * P.cam.tile * P.cam.tile + ly * P.cam.tile + lx;
+      int px, py;
+      inside = camera_tile_pixel(P.cam, ray, px, py);
+      camera_ray(P.cam, P.cam.x0 + (inside ? px : 0), P.cam.y0 + (inside ? py : 0), 0.5f, 0.5f,
+                 R.o, R.d);
+    } else if (P.cam.spp == 1) {  // block = 2x2 pixel tile, warp = pixel
       const int px = 2 * (tile % P.tiles_x) + (wid & 1);
       const int py = 2 * (tile / P.tiles_x) + (wid >> 1);
       if (px >= P.rw || py >= P.rh) return;
@@ -807,7 +1208,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
     replay_in = P.replay_in[ray];
   }
   float t0 = 0.f, t1 = 0.f;
-  const bool hit = P.S.n > 0 && clip_exact(P.S.root_box, R.o, R.d, c.t_near, t0, t1);
+  const bool hit = inside && P.S.n > 0 && clip_exact(P.S.root_box, R.o, R.d, c.t_near, t0, t1);
   if (hit && !(BWD && gr0 == 0.f && gr1 == 0.f && gr2 == 0.f)) {
     R.inv = make_float3(1.0f / R.d.x, 1.0f / R.d.y, 1.0f / R.d.z);
     R.oinv = make_float3(R.o.x * R.inv.x, R.o.y * R.inv.y, R.o.z * R.inv.z);
@@ -836,6 +1237,9 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
     bool wlog = !BWD && log_ok;
     int wcur = 0;
     int fix_used = 0;   // forward: pair slots used in the ray's own block
+    if (lane == 0) M.sst.valid = false;   // forward: persistent traversal restarts on first use
+    __syncwarp();
+    int nref = 0;                         // forward refills of this ray so far
     int s = 0;
     while (true) {
       const int k0 = s * B;
@@ -843,7 +1247,30 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
       const float tlo = fma_((float)k0, c.dt, t0);
       const float thi = fminf(t1, fma_((float)(k0 + B), c.dt, t0));
       // ---- expire Gaussians whose support ended before this slab
-      {
+      if constexpr (KA != kA) {   // large list: chunked compaction from the first expired entry
+        int nc = 0;
+        bool moved = false;
+        for (int h = 0; 32 * h < count; ++h) {
+          const int e = 32 * h + (int)lane;
+          float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0, v2 = v0;
+          bool keep = false;
+          if (e < count) {
+            v0 = M.e0[e];
+            keep = !(v0.y < tlo);
+          }
+          const unsigned km = __ballot_sync(kFull, keep);
+          const int nin = min(32, count - 32 * h);
+          if (!moved && __popc(km) == nin) { nc += nin; continue; }
+          moved = true;
+          if (keep) { v1 = M.e1[e]; v2 = M.e2[e]; }
+          const int dst = nc + __popc(km & ((1u << lane) - 1u));
+          __syncwarp();
+          if (keep) { M.e0[dst] = v0; M.e1[dst] = v1; M.e2[dst] = v2; }
+          nc += __popc(km);
+          __syncwarp();
+        }
+        count = nc;
+      } else {
         unsigned gone0 = 0, gone1 = 0;
         {
           const int e = (int)lane;
@@ -902,8 +1329,8 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
       const bool win = (GW == 8) && (B == 8);
       const float thr = win ? fminf(t1, fma_((float)(k0 + 4 * B), c.dt, t0)) : thi;
       // ---- refill in key order until every Gaussian entering by thr is held
-      while (!exhausted && count < kA && (count == 0 || M.e0[count - 1].x <= thr)) {
-        const int want = min(32, kA - count);
+      while (!exhausted && count < KA && (count == 0 || M.e0[count - 1].x <= thr)) {
+        const int want = min(32, KA - count);
         unsigned long long key = 0;
         uint32_t pos = 0;
         int got;
@@ -918,7 +1345,19 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             M.e2[count + lane] = src[2];
           }
         } else {
-          got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
+          if constexpr (BWD) {
+            got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
+          } else {
+            // the first RG_STREAM_FROM refills of a ray by restart queries (most C1 rays
+            // need one or two), later ones by the persistent traversal
+            if constexpr (!kStream || KA != kA) {
+              got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
+            } else {
+              if (nref < RG_STREAM_FROM) got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
+              else got = stream_next(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
+            }
+            ++nref;
+          }
           if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, count + (int)lane, R, pos);
           if (!BWD && log_ok) {
             // the ray's own pair_fix slots first (no allocation), then the shared
@@ -970,13 +1409,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
       if (win) {
         // ---- window of slabs s..s+3 when the held list is complete for it and no
         // slab can exceed K: lane k integrates sample 8s + k over all members
-        int n3;
-        {
-          const unsigned m0 = __ballot_sync(kFull, (int)lane < count && M.e0[lane].x <= thr);
-          const unsigned m1 =
-              __ballot_sync(kFull, (int)lane + 32 < count && M.e0[lane + 32].x <= thr);
-          n3 = __popc(m0) + __popc(m1);
-        }
+        const int n3 = held_le<KA>(M, count, thr);
         if ((n3 < count || exhausted) && n3 <= K) {
           const float tk = sample_t(k0 + (int)lane, c.dt, t0);
           const bool val = tk < t1;
@@ -1063,26 +1496,25 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             const float lo_w = fma_((float)(k0 + 8 * w), c.dt, t0);
             if (!(sample_t(k0 + 8 * w, c.dt, t0) < t1)) break;
             const float hi_w = fminf(t1, fma_((float)(k0 + 8 * w + 8), c.dt, t0));
-            const unsigned q0 = __ballot_sync(
-                kFull, (int)lane < n3 && M.e0[lane].x <= hi_w && M.e0[lane].y >= lo_w);
-            const unsigned q1 = __ballot_sync(
-                kFull, (int)lane + 32 < n3 && M.e0[lane + 32].x <= hi_w && M.e0[lane + 32].y >= lo_w);
-            if ((q0 | q1) && lane == 0) cnt.slabs++;
-            if (dbg && (q0 | q1)) {
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const unsigned qm = h ? q1 : q0;
+            bool any_w = false;
+            for (int h = 0; 32 * h < n3; ++h) {
+              const int e = 32 * h + (int)lane;
+              const unsigned qm = __ballot_sync(
+                  kFull, e < n3 && M.e0[e].x <= hi_w && M.e0[e].y >= lo_w);
+              any_w |= qm != 0u;
+              if (dbg && qm) {
                 if ((qm >> lane) & 1u) {
                   const int r = dbg_n + __popc(qm & ((1u << lane) - 1u));
                   if (r < P.dbg_cap) {
                     int32_t* rr = P.dbg_rec + 2 * ((size_t)ray * P.dbg_cap + r);
                     rr[0] = s + w;
-                    rr[1] = (int32_t)__float_as_uint(M.e2[h * 32 + lane].z);
+                    rr[1] = (int32_t)__float_as_uint(M.e2[e].z);
                   }
                 }
                 dbg_n = min(P.dbg_cap, dbg_n + __popc(qm));
               }
             }
+            if (any_w && lane == 0) cnt.slabs++;
           }
           {
             const uint32_t evs = __reduce_add_sync(kFull, inwin ? ev : 0u);
@@ -1179,20 +1611,20 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
           continue;
         }
       }
-      int n_in;
-      {
-        const unsigned m0 = __ballot_sync(kFull, (int)lane < count && M.e0[lane].x <= thi);
-        const unsigned m1 = __ballot_sync(kFull, (int)lane + 32 < count && M.e0[lane + 32].x <= thi);
-        n_in = __popc(m0) + __popc(m1);
-      }
+      const int n_in = held_le<KA>(M, count, thi);
       const int n_use = min(n_in, K);
-      const bool more = (n_in == kA) && !exhausted && (K > kA);
+      const bool more = (n_in == KA) && !exhausted && (K > KA);
       if (n_in > K) {
         if (lane == 0) cnt.overflows++;
-      } else if (!BWD && n_in == K && n_in == kA && !exhausted) {
+      } else if (!BWD && n_in == K && n_in == KA && !exhausted) {
         unsigned long long pk;
         uint32_t pp;
         if (fetch(P.S, M, R, tlo, thi, cursor, 1, pk, pp, cnt) > 0 && lane == 0) cnt.overflows++;
+      }
+      if (!BWD && (more || (n_in == K && n_in == KA && !exhausted))) {
+        __syncwarp();                        // a restart query reused the traversal memory
+        if (lane == 0) M.sst.valid = false;
+        __syncwarp();
       }
       if (dbg) dbg_put(P, ray, dbg_n, s, n_use, M, 0);
       for (int g0 = 0; g0 < B; g0 += GW) {
@@ -1210,10 +1642,10 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : RG_MIN_BLOCKS_FW
             unsigned long long key;
             uint32_t pos;
             const int got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
-            if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, kTrans + (int)lane, R, pos);
+            if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, KA + (int)lane, R, pos);
             __syncwarp();
-            eval_range<GW, BASIS>(M, kA, kA + got, L, tk, val, sg, sr, sgg, sb, ev);
-            if (dbg && g0 == 0) dbg_put(P, ray, dbg_n, s, got, M, kA);
+            eval_range<GW, BASIS>(M, KA, KA + got, L, tk, val, sg, sr, sgg, sb, ev);
+            if (dbg && g0 == 0) dbg_put(P, ray, dbg_n, s, got, M, KA);
             if (g0 == 0 && lane == 0) cnt.pairs += got;
             remaining -= got;
             if (got > 0) cur2 = shfl64(key, got - 1);
@@ -1362,12 +1794,16 @@ __global__ void __launch_bounds__(256) k_finalize(const float* gbuf, int gstride
                       2.f * (x * z - w * y), 2.f * (y * z + w * x), 1.f - 2.f * (x * x + y * y)};
   float dR[9];
   float ds[3];
+  // a row that received no geometry gradient (never hit: e.g. an inactive, possibly
+  // non-finite, Gaussian) converts to exact zeros, not 0 * NaN
+  bool any = false;
+  for (int k = 4; k < 13; ++k) any |= row[k] != 0.f;
   for (int a = 0; a < 3; ++a) {
     ds[a] = 0.f;
     for (int b = 0; b < 3; ++b) {
       const float dM = row[4 + 3 * a + b];   // M_ab = R_ba / s_a
-      ds[a] -= dM * R[3 * b + a] / (s[a] * s[a]);
-      dR[3 * b + a] = dM / s[a];
+      ds[a] -= any ? dM * R[3 * b + a] / (s[a] * s[a]) : 0.f;
+      dR[3 * b + a] = any ? dM / s[a] : 0.f;
     }
   }
   // d R / d q (polynomial ARITH-1 differentiated)
@@ -1380,6 +1816,7 @@ __global__ void __launch_bounds__(256) k_finalize(const float* gbuf, int gstride
           dR[5] * (2 * z) + dR[6] * (-2 * w) + dR[7] * (2 * z) + dR[8] * (-4 * y);
   dq[3] = dR[0] * (-4 * z) + dR[1] * (-2 * w) + dR[2] * (2 * x) + dR[3] * (2 * w) +
           dR[4] * (-4 * z) + dR[5] * (2 * y) + dR[6] * (2 * x) + dR[7] * (2 * y);
+  if (!any) dq[0] = dq[1] = dq[2] = dq[3] = 0.f;
   uint32_t bad = 0;
   auto put = [&](float* base, size_t k, float v) {
     if (!isfinite(v)) ++bad;
@@ -1426,14 +1863,21 @@ __global__ void __launch_bounds__(256) k_finalize_app(const float* gbuf, int gst
   if (bad && lane == 0 && stats) atomicAdd(&stats->nonfinite_grads, (unsigned long long)bad);
 }
 
-__global__ void k_camera_rays(const rg_camera cam, float* o, float* d) {
-  const int rw = cam.x1 - cam.x0, rh = cam.y1 - cam.y0;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rw * rh * cam.spp) return;
-  const int pix = r / cam.spp, s = r - pix * cam.spp;
-  float3 oo, dd;
-  camera_ray(cam, cam.x0 + pix % rw, cam.y0 + pix / rw, sub_off(cam.spp, s & 1),
-             sub_off(cam.spp, s >> 1), oo, dd);
+__global__ void k_camera_rays(const rg_camera cam, float* o, float* d, int64_t n) {
+  const int rw = cam.x1 - cam.x0;
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  float3 oo = make_float3(0.f, 0.f, 0.f), dd = oo;
+  if (cam.tile > 0) {
+    int px, py;
+    if (camera_tile_pixel(cam, r, px, py))
+      camera_ray(cam, cam.x0 + px, cam.y0 + py, 0.5f, 0.5f, oo, dd);
+  } else {
+    const int64_t pix = r / cam.spp;
+    const int s = (int)(r - pix * cam.spp);
+    camera_ray(cam, cam.x0 + (int)(pix % rw), cam.y0 + (int)(pix / rw), sub_off(cam.spp, s & 1),
+               sub_off(cam.spp, s >> 1), oo, dd);
+  }
   o[3 * r] = oo.x; o[3 * r + 1] = oo.y; o[3 * r + 2] = oo.z;
   d[3 * r] = dd.x; d[3 * r + 1] = dd.y; d[3 * r + 2] = dd.z;
 }
@@ -1471,10 +1915,13 @@ void ray_grid(RenderArgs& A, const rg_rays* rays, const rg_camera* cam, dim3& gr
     A.cam = *cam;
     A.rw = cam->x1 - cam->x0;
     A.rh = cam->y1 - cam->y0;
-    A.n_rays = A.rw * A.rh * cam->spp;
+    A.n_rays = (int)camera_ray_slots(*cam);
     A.tiles_x = (A.rw + 1) / 2;
-    grid = cam->spp == 1 ? dim3((unsigned)(A.tiles_x * ((A.rh + 1) / 2)))
-                         : dim3((unsigned)(A.rw * A.rh));     // spp = 4: one block per pixel
+    if (cam->tile > 0)            // owned squares x (tile/2)^2 blocks of 2x2 pixels
+      grid = dim3((unsigned)(camera_owned_squares(*cam) * (cam->tile / 2) * (cam->tile / 2)));
+    else
+      grid = cam->spp == 1 ? dim3((unsigned)(A.tiles_x * ((A.rh + 1) / 2)))
+                           : dim3((unsigned)(A.rw * A.rh));   // spp = 4: one block per pixel
   } else {
     A.cam_mode = 0;
     A.ro = rays->origin;
@@ -1485,15 +1932,15 @@ void ray_grid(RenderArgs& A, const rg_rays* rays, const rg_camera* cam, dim3& gr
 }
 
 // dynamic shared memory above the 48 KB default needs a per-kernel opt-in
-template <bool BWD, int GW, bool INSTR, int BASIS>
+template <bool BWD, int GW, bool INSTR, int BASIS, int KA = kA>
 void launch_one(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
   static bool opted = false;
   if (!opted) {
-    cudaFuncSetAttribute(k_render<BWD, GW, INSTR, BASIS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(k_render<BWD, GW, INSTR, BASIS, KA>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     opted = true;
   }
-  k_render<BWD, GW, INSTR, BASIS><<<grid, kBlock, smem, st>>>(A);
+  k_render<BWD, GW, INSTR, BASIS, KA><<<grid, kBlock, smem, st>>>(A);
 }
 
 template <bool BWD, int GW, int BASIS>
@@ -1502,9 +1949,22 @@ void launch_gw(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
   else launch_one<BWD, GW, false, BASIS>(A, grid, smem, st);
 }
 
+constexpr size_t kSmemBig = sizeof(WMBig) * kWarps;
+static_assert(2 * (kSmemBig + 1024) <= 228 * 1024, "two large-list blocks per SM");
+
 template <bool BWD>
 void launch_render(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
   const int B = A.c.slab_samples;
+  // forward large-list variant (rg_config.list_capacity, Gaussian basis, B >= 5)
+  if constexpr (!BWD) {
+    if (A.c.list_capacity > kA && A.c.basis == 0 && B >= 5 && A.c.hit_capacity < kABig) {
+      if (A.stats != nullptr || A.dbg_rec != nullptr)
+        launch_one<false, 8, true, 0, kABig>(A, grid, kSmemBig, st);
+      else
+        launch_one<false, 8, false, 0, kABig>(A, grid, kSmemBig, st);
+      return;
+    }
+  }
   // non-Gaussian bases (NEXT-3) are instantiated for GW = 8 only (B >= 5; the API
   // rejects them otherwise)
   if (B >= 5) {
@@ -1521,8 +1981,8 @@ void launch_render(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st)
   else launch_gw<BWD, 1, 0>(A, grid, smem, st);
 }
 
-constexpr size_t kSmemFwd = sizeof(WarpMemT<kStkFwd>) * kWarps;
-constexpr size_t kSmemBwd = (sizeof(WarpMemT<kStkBwd>) + sizeof(WarpAcc)) * kWarps;
+constexpr size_t kSmemFwd = sizeof(WMFwd) * kWarps;
+constexpr size_t kSmemBwd = (sizeof(WMBwd) + sizeof(WarpAcc)) * kWarps;
 // 4 resident backward blocks must fit the 196 KB shared-memory carve-out (1 KB
 // reserved per block): a larger carve-out halves L1 and costs ~6% (measured)
 static_assert(kSmemBwd <= 48 * 1024 + 128, "backward block exceeds the 196 KB carve-out budget");
@@ -1548,8 +2008,11 @@ void set_log(RenderArgs& A, const void* log, size_t log_bytes, int n_rays) {
 }  // namespace
 
 cudaError_t launch_camera_rays(const rg_camera& cam, float* o, float* d, cudaStream_t st) {
-  const int n = (cam.x1 - cam.x0) * (cam.y1 - cam.y0) * cam.spp;
-  if (n > 0) { k_camera_rays<<<(n + 255) / 256, 256, 0, st>>>(cam, o, d); count_launches(1); }
+  const int64_t n = camera_ray_slots(cam);
+  if (n > 0) {
+    k_camera_rays<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(cam, o, d, n);
+    count_launches(1);
+  }
   return cudaGetLastError();
 }
 

@@ -19,7 +19,7 @@ __all__ = ["RGError", "Config", "Gaussians", "BVH", "lib", "build_bvh", "camera_
            "render_forward", "render_backward", "l1_loss_grad", "camera_struct", "STAT_KEYS"]
 
 STAT_KEYS = ("rays", "rays_hit", "slabs", "pairs", "evals", "samples", "overflows", "fetches",
-             "node_visits", "stack_overflows", "nonfinite_grads")
+             "node_visits", "stack_overflows", "nonfinite_grads", "restarts")
 
 
 class RGError(RuntimeError):
@@ -42,7 +42,7 @@ class _Config(C.Structure):
     _fields_ = [("dt", C.c_float), ("slab_samples", C.c_int32), ("sigma_eps", C.c_float),
                 ("t_eps", C.c_float), ("hit_capacity", C.c_int32), ("radius_mode", C.c_int32),
                 ("k_sigma", C.c_float), ("t_near", C.c_float), ("background", C.c_float * 3),
-                ("basis", C.c_int32)]
+                ("basis", C.c_int32), ("list_capacity", C.c_int32)]
 
 
 class _AdamConfig(C.Structure):
@@ -60,7 +60,8 @@ class _Camera(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("x0", C.c_int32), ("y0", C.c_int32),
                 ("x1", C.c_int32), ("y1", C.c_int32), ("fx", C.c_float), ("fy", C.c_float),
                 ("cx", C.c_float), ("cy", C.c_float), ("c2w", C.c_float * 12),
-                ("spp", C.c_int32), ("pad_", C.c_int32)]
+                ("spp", C.c_int32), ("tile", C.c_int32), ("shard", C.c_int32),
+                ("shards", C.c_int32), ("pad_", C.c_int32)]
 
 
 class _BVH(C.Structure):
@@ -75,7 +76,7 @@ EXPORTS = ("rg_status_string", "rg_version", "rg_kernel_launches", "rg_bvh_works
            "rg_refit_bvh", "rg_adam_step", "rg_dssim_workspace_bytes", "rg_l1_dssim_loss_grad",
            "rg_supersample_resolve", "rg_supersample_spread", "rg_densify_accumulate",
            "rg_densify_workspace_bytes", "rg_densify_plan", "rg_densify_apply",
-           "rg_camera_rays", "rg_render_forward", "rg_backward_workspace_bytes",
+           "rg_camera_ray_count", "rg_camera_rays", "rg_render_forward", "rg_backward_workspace_bytes",
            "rg_render_backward", "rg_l1_loss_grad", "rg_fetch_log_bytes")
 
 _lib = None
@@ -126,6 +127,8 @@ def lib(load_only: bool = False):
     L.rg_densify_plan.argtypes = [P, P, P, C.c_float, C.c_float, C.c_float, C.c_float, P, P, SZ, P, P]
     L.rg_densify_apply.restype = C.c_int
     L.rg_densify_apply.argtypes = [P, P, P, P, P, P, I32, P, P]
+    L.rg_camera_ray_count.restype = C.c_int64
+    L.rg_camera_ray_count.argtypes = [P]
     L.rg_camera_rays.restype = C.c_int
     L.rg_camera_rays.argtypes = [P, P, P, P]
     L.rg_render_forward.restype = C.c_int
@@ -176,11 +179,13 @@ class Config:
     background: tuple = (1.0, 1.0, 1.0)
     basis: int = 0            # RG_BASIS_*: 0 Gaussian, 1 Bump, 2 Wendland, 3 inverse
                               # multiquadric, 4 inverse quadratic, 5 C0-Matern
+    list_capacity: int = 0    # forward kernel-variant hint (rg.h): > 64 = large active list
 
     @classmethod
     def of(cls, p) -> "Config":
         return cls(p.dt, p.slab_samples, p.sigma_eps, p.t_eps, p.hit_capacity, p.radius_mode,
-                   p.k_sigma, p.t_near, tuple(p.background), getattr(p, "basis", 0))
+                   p.k_sigma, p.t_near, tuple(p.background), getattr(p, "basis", 0),
+                   getattr(p, "list_capacity", 0))
 
     def struct(self) -> _Config:
         c = _Config()
@@ -190,6 +195,7 @@ class Config:
         for i in range(3):
             c.background[i] = self.background[i]
         c.basis = self.basis
+        c.list_capacity = self.list_capacity
         return c
 
 
@@ -329,7 +335,16 @@ def camera_struct(cam) -> _Camera:
     for i in range(12):
         s.c2w[i] = flat[i]
     s.spp = int(getattr(cam, "spp", 1))
+    s.tile = int(getattr(cam, "tile", 0))
+    s.shard = int(getattr(cam, "shard", 0))
+    s.shards = int(getattr(cam, "shards", 1))
     return s
+
+
+def camera_ray_count(cam) -> int:
+    """ray slots of a camera (rg_camera_ray_count; 0 if the camera is invalid)"""
+    cs = camera_struct(cam)
+    return int(lib().rg_camera_ray_count(C.byref(cs)))
 
 
 def camera_rays(cam, device="cuda"):
@@ -367,7 +382,10 @@ def _ray_args(rays, camera, device):
         r.origin, r.dir = _ptr(o), _ptr(d)
         return C.byref(r), None, r.n, (r, o, d)
     cs = camera_struct(camera)
-    return None, C.byref(cs), camera.n_rays, (cs,)
+    n = int(lib().rg_camera_ray_count(C.byref(cs)))
+    if n != camera.n_rays:
+        raise RGError(f"invalid camera (ray slots {n} vs {camera.n_rays})")
+    return None, C.byref(cs), n, (cs,)
 
 
 def check_stats(stats, what="render"):

@@ -70,15 +70,39 @@ class Camera:
     c2w: np.ndarray                 # [3,4] f32
     rect: tuple | None = None       # (x0, y0, x1, y1) pixel rectangle, default full
     spp: int = 1                    # rays per pixel: 1, or 4 (RayGauss4x)
+    tile: int = 0                   # > 0: interleaved tile sharding (rg.h rg_camera): this
+    shard: int = 0                  #   camera covers the tile x tile squares k of the
+    shards: int = 1                 #   rectangle with k % shards == shard
 
     @property
     def x0y0x1y1(self):
         return self.rect if self.rect is not None else (0, 0, self.width, self.height)
 
+    def owned_squares(self):
+        """(kx, ky) of the squares a tile-sharded camera covers, in ray order"""
+        x0, y0, x1, y1 = self.x0y0x1y1
+        nsx = -(-(x1 - x0) // self.tile)
+        nsy = -(-(y1 - y0) // self.tile)
+        return [(k % nsx, k // nsx) for k in range(self.shard, nsx * nsy, self.shards)]
+
     @property
     def n_rays(self) -> int:
         x0, y0, x1, y1 = self.x0y0x1y1
+        if self.tile > 0:
+            return len(self.owned_squares()) * self.tile * self.tile
         return (x1 - x0) * (y1 - y0) * self.spp
+
+    def slot_pixels(self):
+        """tile sharding: rectangle-relative row-major pixel index of every ray slot,
+        -1 for slots of ragged squares outside the rectangle (index bookkeeping only)"""
+        x0, y0, x1, y1 = self.x0y0x1y1
+        w, h, t = x1 - x0, y1 - y0, self.tile
+        out = []
+        for kx, ky in self.owned_squares():
+            ly, lx = np.meshgrid(np.arange(t), np.arange(t), indexing="ij")
+            px, py = kx * t + lx.reshape(-1), ky * t + ly.reshape(-1)
+            out.append(np.where((px < w) & (py < h), py * w + px, -1))
+        return np.concatenate(out) if out else np.zeros(0, np.int64)
 
 
 @dataclass
@@ -94,6 +118,7 @@ class RenderParams:
     background: tuple = (1.0, 1.0, 1.0)
     basis: int = 0              # basis function: 0 Gaussian, 1 Bump, 2 Wendland,
                                 # 3 inverse multiquadric, 4 inverse quadratic, 5 C0-Matern
+    list_capacity: int = 0      # CUDA kernel-variant hint (rg.h rg_config); no effect on results
 
     def replace(self, **kw) -> "RenderParams":
         d = dict(self.__dict__)
@@ -388,7 +413,7 @@ def workload(name: str, *, n=None, views=None) -> Workload:
         sc = scene_stress(n=n or 5_000_000)
         cams = [orbit_camera(3.5, 20.0, 15.0, 1920, 1080, 960.0 / math.tan(math.radians(25.0)))]
         p = RenderParams(dt=2.5e-4, slab_samples=8, sigma_eps=0.01, t_eps=1e-4,
-                         hit_capacity=512, background=(0.0, 0.0, 0.0))
+                         hit_capacity=512, background=(0.0, 0.0, 0.0), list_capacity=520)
         return Workload(name, sc, cams, p, "C4: 5M overlapping Gaussians, 1920x1080")
     raise KeyError(name)
 

@@ -65,8 +65,8 @@ def test_workspace_sizes_and_validation():
 def test_struct_sizes_match_header():
     from paper_2408_03356_b200 import rg
     assert C.sizeof(rg._Gaussians) == 16 + 8 * 8
-    assert C.sizeof(rg._Config) == 48
-    assert C.sizeof(rg._Camera) == 24 + 16 + 48 + 8
+    assert C.sizeof(rg._Config) == 52
+    assert C.sizeof(rg._Camera) == 24 + 16 + 48 + 20
     assert C.sizeof(rg._BVH) == 16 + 10 * 8
 
 
@@ -85,3 +85,28 @@ def test_binding_refuses_without_cuda():
         pytest.skip("GPU present")
     with pytest.raises(rg.RGError):
         rg.camera_rays(None)
+
+
+@pytest.mark.parametrize("tile,shards", [(0, 1), (16, 1), (16, 3), (6, 4), (2, 7)])
+def test_camera_ray_count_tile_sharding(tile, shards):
+    """rg_camera_ray_count (host, no GPU) = the slot count of the interleaved
+    tile sharding of rg.h; every pixel of the rectangle is in exactly one
+    shard's slots; invalid tilings are rejected (0)."""
+    import dataclasses
+    import numpy as np
+    from paper_2408_03356_b200 import rg, synth
+    cam = synth.orbit_camera(2.2, 40, 20, 45, 37, 50.0)
+    cam.rect = (2, 1, 43, 36)
+    seen = np.zeros(41 * 35, int)
+    for r in range(shards):
+        c = dataclasses.replace(cam, tile=tile, shard=r, shards=shards)
+        assert rg.camera_ray_count(c) == c.n_rays
+        if tile:
+            pix = c.slot_pixels()
+            assert len(pix) == c.n_rays
+            seen[pix[pix >= 0]] += 1
+    if tile:
+        assert np.all(seen == 1)
+    for bad in (dict(tile=3), dict(tile=16, shard=2, shards=2), dict(tile=16, shards=0),
+                dict(tile=16, spp=4)):
+        assert rg.camera_ray_count(dataclasses.replace(cam, **bad)) == 0

@@ -193,13 +193,15 @@ def test_forward_slab_sizes(oracle, B):
     assert (ref["s_term"] >= 0).any()
 
 
-@pytest.mark.parametrize("K", [3, 32, 40, 100])
-def test_forward_overflow_truncation(oracle, K):
+@pytest.mark.parametrize("K,lc", [(3, 0), (32, 0), (40, 0), (100, 0), (3, 520), (40, 520),
+                                  (100, 520)])
+def test_forward_overflow_truncation(oracle, K, lc):
     """Per-slab sets larger than K (and larger than the active list) keep the
-    K smallest (t_entry, index) exactly (L7)."""
+    K smallest (t_entry, index) exactly (L7); lc = rg_config.list_capacity
+    (544: the large-list kernel variant, which holds whole truncated sets)."""
     sc = synth.random_scene(950, 400, sh_degree=0, density_range=(0.3, 2.0),
                             scale_range=(0.1, 0.3), extent=0.3)
-    p = synth.RenderParams(dt=4e-3, slab_samples=8, t_eps=1e-4, hit_capacity=K)
+    p = synth.RenderParams(dt=4e-3, slab_samples=8, t_eps=1e-4, hit_capacity=K, list_capacity=lc)
     o, d = oracle.camera_rays(synth.orbit_camera(2.2, 10, 25, 12, 12, 14.0))
     rg_, ref, ok = _fwd_case(oracle, sc, p, o, d, debug_rays=144, cap=60000)
     assert ref["counters"]["overflows"] > 0
