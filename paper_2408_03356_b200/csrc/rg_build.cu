@@ -194,14 +194,23 @@ __global__ void __launch_bounds__(kThreads) k_radix_hist(const uint32_t* keys, i
   hist[threadIdx.x * tiles + blockIdx.x] = h[threadIdx.x];   // digit-major
 }
 
-// exclusive scan of hist[256*tiles] in place, one block of 1024 threads
+// exclusive scan of hist[256*tiles] in place, one block of 1024 threads; the
+// counts are first staged in shared memory by coalesced loads (all in flight at
+// once: the per-thread serial loads of a contiguous run were latency-bound)
+constexpr int kScanStage = 49152;        // staged counts (192 KB, n <= 786k); larger totals read global
 __global__ void __launch_bounds__(1024) k_radix_scan(uint32_t* hist, int total) {
+  extern __shared__ uint32_t stage[];
   __shared__ uint32_t part[1024];
   const int t = threadIdx.x;
+  const bool staged = total <= kScanStage;
+  if (staged)
+    for (int i = t; i < total; i += 1024) stage[i] = hist[i];
+  __syncthreads();
+  const uint32_t* src = staged ? stage : hist;
   const int per = (total + 1023) / 1024;
   const int b = t * per, e = min(total, b + per);
   uint32_t s = 0;
-  for (int i = b; i < e; ++i) s += hist[i];
+  for (int i = b; i < e; ++i) s += src[i];
   part[t] = s;
   __syncthreads();
   for (int off = 1; off < 1024; off <<= 1) {
@@ -212,9 +221,13 @@ __global__ void __launch_bounds__(1024) k_radix_scan(uint32_t* hist, int total) 
   }
   uint32_t run = part[t] - s;
   for (int i = b; i < e; ++i) {
-    const uint32_t v = hist[i];
-    hist[i] = run;
+    const uint32_t v = src[i];
+    if (staged) stage[i] = run; else hist[i] = run;
     run += v;
+  }
+  if (staged) {
+    __syncthreads();
+    for (int i = t; i < total; i += 1024) hist[i] = stage[i];
   }
 }
 
@@ -517,10 +530,19 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
       if (!cm) break;
       const float area = internal ? box_area(b) : -2.f;
       int rank = 0;                                   // by area, descending (ties: lane)
-      for (unsigned mm = cm; mm; mm &= mm - 1) {
-        const int o = __ffs(mm) - 1;
-        const float ao = __shfl_sync(full, area, o);
-        rank += (ao > area) || (ao == area && o < lane);
+      if (RG_COLLAPSE_OPEN == 1) {
+        // only rank 0 opens: the largest area, lowest lane on ties (one reduction
+        // instead of a 32-step rank loop; the same entry, hence the same tree)
+        const int key = ord_enc(area);
+        const int kmax = __reduce_max_sync(full, key);
+        const int first = __ffs(__ballot_sync(full, key == kmax)) - 1;
+        rank = lane == first ? 0 : 1;
+      } else {
+        for (unsigned mm = cm; mm; mm &= mm - 1) {
+          const int o = __ffs(mm) - 1;
+          const float ao = __shfl_sync(full, area, o);
+          rank += (ao > area) || (ao == area && o < lane);
+        }
       }
       // one opening per round reproduces the greedy cut of the thread variant (opening
       // several per round measured a worse tree: forward +7%)
@@ -649,10 +671,19 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
   k_morton<<<blocks, kThreads, 0, st>>>(g, flags, bounds,
                                         reinterpret_cast<uint32_t*>(ws + L.codes), ka, va);
   uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);
+  const size_t scan_smem = 256 * (size_t)L.tiles <= (size_t)kScanStage ? 4 * 256 * (size_t)L.tiles : 0;
+  {
+    static bool opted = false;          // > 48 KB of dynamic shared memory needs an opt-in
+    if (!opted) {
+      cudaFuncSetAttribute(k_radix_scan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           4 * kScanStage);
+      opted = true;
+    }
+  }
   auto radix_pass = [&](const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo,
                         int shift) {
     k_radix_hist<<<L.tiles, kThreads, 0, st>>>(ki, n, shift, hist, L.tiles);
-    k_radix_scan<<<1, 1024, 0, st>>>(hist, 256 * L.tiles);
+    k_radix_scan<<<1, 1024, scan_smem, st>>>(hist, 256 * L.tiles);
     k_radix_scatter<<<L.tiles, kThreads, 0, st>>>(ki, vi, ko, vo, n, shift, hist, L.tiles);
   };
   // stable LSD sort by (code, fine code, index) (L34): first the 21-bit fine code

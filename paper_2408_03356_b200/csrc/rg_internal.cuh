@@ -35,8 +35,10 @@ __host__ __device__ inline int app_floats(int deg, int lobes) {
 __host__ __device__ inline int app_stride(int deg, int lobes) {
   return (app_floats(deg, lobes) + 3) & ~3;
 }
-// Morton-ordered gradient row (floats): [0..2] dL/dmu, [3] dL/dsigma~,
-// [4..12] dL/dM, [13..15] pad, then SH grads channel-major [3][ncp]
+// Morton-ordered gradient row (floats): [0..2] v = sum (Sw x' + Sw1 d), [3] dL/dsigma~,
+// [4..9] the symmetric S = sum (Sw x'x'^T + Sw1 (x'd^T + dx'^T) + Sw2 dd^T) as
+// (S00, S01, S02, S11, S12, S22) -- k_finalize forms dL/dmu = M^T M v and
+// dL/dM = -M S -- [10..15] pad, then SH grads channel-major [3][ncp]
 // (ncp = (deg+1)^2 rounded up to 4), then SG grads lobe-major [G][8]
 // (k0,k1,k2,lambda | p0,p1,p2,-), so that every float4 of the appearance part
 // is one SH channel x 4 coefficients or one half of one lobe.

@@ -992,39 +992,31 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, c
     const float Sw = acc.x, Sw1 = acc.y, Sw2 = acc.z;
     const float4 x0 = M.e0[e];
     const int pos = __float_as_int(M.e2[e].y);
-    const float4* gp = S.geom + 4 * (size_t)pos;
-    const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2), g3 = __ldg(gp + 3);
-    const float Mm[9] = {g1.x, g1.y, g1.z, g1.w, g2.x, g2.y, g2.z, g2.w, g3.x};
+    const float4 g0 = __ldg(S.geom + 4 * (size_t)pos);
     const float tm = x0.z;
     const float xp[3] = {offset_at(R.o.x, g0.x, tm, R.d.x), offset_at(R.o.y, g0.y, tm, R.d.y),
                          offset_at(R.o.z, g0.z, tm, R.d.z)};
     const float dv[3] = {R.d.x, R.d.y, R.d.z};
-    float u[3], dl[3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      u[r] = Mm[3 * r] * xp[0] + Mm[3 * r + 1] * xp[1] + Mm[3 * r + 2] * xp[2];
-      dl[r] = Mm[3 * r] * dv[0] + Mm[3 * r + 1] * dv[1] + Mm[3 * r + 2] * dv[2];
-    }
-    float gm[3];
-#pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      float t = 0.f;
-#pragma unroll
-      for (int r = 0; r < 3; ++r) t += Mm[3 * r + b] * (Sw * u[r] + Sw1 * dl[r]);
-      gm[b] = t;
-    }
-    float dM[9];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-        dM[3 * r + b] = -(Sw * u[r] * xp[b] + Sw1 * (u[r] * dv[b] + dl[r] * xp[b]) +
-                          Sw2 * dl[r] * dv[b]);
+    // M-free sufficient statistics (linear in the pair's moments, summed over rays):
+    //   v = Sw x' + Sw1 d,  S = Sw x'x'^T + Sw1 (x'd^T + d x'^T) + Sw2 d d^T (symmetric);
+    // k_finalize forms dL/dmu = M^T M v and dL/dM = -M S once per Gaussian
+    const float v0 = fmaf(Sw, xp[0], Sw1 * dv[0]);
+    const float v1 = fmaf(Sw, xp[1], Sw1 * dv[1]);
+    const float v2 = fmaf(Sw, xp[2], Sw1 * dv[2]);
+    const float h0 = fmaf(Sw2, dv[0], Sw1 * xp[0]);   // Sw1 x' + Sw2 d
+    const float h1 = fmaf(Sw2, dv[1], Sw1 * xp[1]);
+    const float h2 = fmaf(Sw2, dv[2], Sw1 * xp[2]);
+    // S_ab = x'_a (Sw x'_b + Sw1 d_b) + d_a (Sw1 x'_b + Sw2 d_b) = x'_a v_b + d_a h_b
+    const float s00 = fmaf(xp[0], v0, dv[0] * h0);
+    const float s01 = fmaf(xp[0], v1, dv[0] * h1);
+    const float s02 = fmaf(xp[0], v2, dv[0] * h2);
+    const float s11 = fmaf(xp[1], v1, dv[1] * h1);
+    const float s12 = fmaf(xp[1], v2, dv[1] * h2);
+    const float s22 = fmaf(xp[2], v2, dv[2] * h2);
     float4* row = reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride);
-    atomicAdd(row + 0, make_float4(gm[0], gm[1], gm[2], (BASIS == 0 ? Sw : A.c[e]) / g0.w));
-    atomicAdd(row + 1, make_float4(dM[0], dM[1], dM[2], dM[3]));
-    atomicAdd(row + 2, make_float4(dM[4], dM[5], dM[6], dM[7]));
-    atomicAdd(row + 3, make_float4(dM[8], 0.f, 0.f, 0.f));
+    atomicAdd(row + 0, make_float4(v0, v1, v2, (BASIS == 0 ? Sw : A.c[e]) / g0.w));
+    atomicAdd(row + 1, make_float4(s00, s01, s02, s11));
+    atomicAdd(row + 2, make_float4(s12, s22, 0.f, 0.f));
   }
   // SG lobes: lane = (pair, lobe, half) item, so several pairs' record loads are in
   // flight per instruction (the per-pair loop below waits on one pair at a time)
@@ -1194,6 +1186,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kA ? RG_M
   const rg_config& c = P.c;
   const int B = c.slab_samples;
   const int K = c.hit_capacity;
+  const float inv_dt = 1.0f / c.dt;
   float C0 = 0.f, C1 = 0.f, C2 = 0.f, k0c = 0.f, k1c = 0.f, k2c = 0.f;
   float tau = 0.f, tauc = 0.f, T = 1.f;
   int replay = -1;
@@ -1371,6 +1364,13 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kA ? RG_M
               if (lane == 0 && got > 0) off = atomicAdd(P.arena_ctr, (unsigned long long)got);
               off = shfl64(off, 0) + (unsigned long long)P.n_rays * P.pair_fix;
               fits = (long long)(off + got) <= P.arena_cap;
+            }
+            if (lp + 2 > kLogWords - nwin && nwin > 0 && lp + 2 <= kLogWords) {
+              // fetch records are required, stored windows optional (recomputed by the
+              // backward): drop the last stored windows (the stored ones stay a prefix
+              // of the ray's windows; no further window is stored)
+              nwin = kLogWords - (lp + 2) < nwin ? kLogWords - (lp + 2) : nwin;
+              wlog = false;
             }
             if (lp + 2 > kLogWords - nwin || !fits) {
               log_ok = false;
@@ -1551,9 +1551,11 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kA ? RG_M
                 const float4 q = M.e1[e];
                 const float cbv = M.e2[e].x;
                 const float sge = BASIS != 0 ? M.e2[e].w : 0.f;
+                // conservative sample range (+-1; the exact test below decides): a
+                // reciprocal multiply, not two IEEE divisions per member and window
                 const float kf = (float)k0 + 0.5f;
-                int kl = (int)floorf((a.x - t0) / c.dt - kf) - 1;
-                int kh = (int)ceilf((a.y - t0) / c.dt - kf) + 1;
+                int kl = (int)floorf((a.x - t0) * inv_dt - kf) - 1;
+                int kh = (int)ceilf((a.y - t0) * inv_dt - kf) + 1;
                 kl = max(kl, part0);
                 kh = min(kh, min(last, part0 + P2 - 1));
 #pragma unroll kMemberUnroll
@@ -1797,11 +1799,26 @@ __global__ void __launch_bounds__(256) k_finalize(const float* gbuf, int gstride
   // a row that received no geometry gradient (never hit: e.g. an inactive, possibly
   // non-finite, Gaussian) converts to exact zeros, not 0 * NaN
   bool any = false;
-  for (int k = 4; k < 13; ++k) any |= row[k] != 0.f;
+  for (int k = 0; k < 10; ++k) any |= (k != 3) && row[k] != 0.f;
+  // the backward accumulates v = sum (Sw x' + Sw1 d) and the symmetric
+  // S = sum (Sw x'x'^T + Sw1 (x'd^T + d x'^T) + Sw2 d d^T) (scatter_batch):
+  // dL/dmu = M^T M v, dL/dM = -M S, with M_ab = R_ba / s_a
+  float Mx[9];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) Mx[3 * a + b] = R[3 * b + a] / s[a];
+  const float Sm[9] = {row[4], row[5], row[6], row[5], row[7], row[8], row[6], row[8], row[9]};
+  float gmu[3] = {0.f, 0.f, 0.f};
+  if (any) {
+    float mv[3];
+    for (int a = 0; a < 3; ++a) mv[a] = Mx[3 * a] * row[0] + Mx[3 * a + 1] * row[1] + Mx[3 * a + 2] * row[2];
+    for (int b = 0; b < 3; ++b) gmu[b] = Mx[b] * mv[0] + Mx[3 + b] * mv[1] + Mx[6 + b] * mv[2];
+  }
   for (int a = 0; a < 3; ++a) {
     ds[a] = 0.f;
     for (int b = 0; b < 3; ++b) {
-      const float dM = row[4 + 3 * a + b];   // M_ab = R_ba / s_a
+      // dL/dM_ab = -(M S)_ab
+      const float dM = any ? -(Mx[3 * a] * Sm[b] + Mx[3 * a + 1] * Sm[3 + b] + Mx[3 * a + 2] * Sm[6 + b])
+                           : 0.f;
       ds[a] -= any ? dM * R[3 * b + a] / (s[a] * s[a]) : 0.f;
       dR[3 * b + a] = any ? dM / s[a] : 0.f;
     }
@@ -1822,7 +1839,7 @@ __global__ void __launch_bounds__(256) k_finalize(const float* gbuf, int gstride
     if (!isfinite(v)) ++bad;
     if (base) base[k] += v;
   };
-  for (int a = 0; a < 3; ++a) put(out.mean, 3 * (size_t)i + a, row[a]);
+  for (int a = 0; a < 3; ++a) put(out.mean, 3 * (size_t)i + a, gmu[a]);
   put(out.density, i, row[3]);
   for (int a = 0; a < 3; ++a) put(out.scale, 3 * (size_t)i + a, ds[a]);
   for (int a = 0; a < 4; ++a) put(out.quat, 4 * (size_t)i + a, dq[a]);

@@ -20,6 +20,7 @@ ap.add_argument("--ppr", type=int, default=0)
 ap.add_argument("--rect", type=int, nargs=4, default=None)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--nobwd", action="store_true")
+ap.add_argument("--lc", type=int, default=None, help="rg_config.list_capacity override")
 a = ap.parse_args()
 wl = synth.workload(a.name)
 sc, cam, p = wl.scene, wl.cameras[0], wl.params
@@ -27,6 +28,8 @@ if a.rect:
     cam.rect = tuple(a.rect)
 g = rg.Gaussians.from_scene(sc)
 cfg = rg.Config.of(p)
+if a.lc is not None:
+    cfg.list_capacity = a.lc
 
 
 def ev():
