@@ -77,10 +77,11 @@ typedef struct {
                             RG_BASIS_* below; non-Gaussian bases need radius_mode 0 and
                             slab_samples >= 5 (else RG_ERR_NOT_IMPLEMENTED) */
   int32_t list_capacity; /* forward kernel-variant hint, results identical either way:
-                            0 = the 64-slot per-ray active list; > 64 = a 544-slot list
-                            (hit_capacity < 544, Gaussian basis, slab_samples >= 5) that
-                            holds whole truncated slab sets (K-saturated scenes such as
-                            C4) instead of re-querying the BVH for every slab */
+                            0 = the 64-slot per-ray active list; 65..128 = a 128-slot list;
+                            > 128 = a 520-slot list (hit_capacity < 520) that holds whole
+                            truncated slab sets (K-saturated scenes such as C4); the larger
+                            lists apply to the Gaussian basis with slab_samples >= 5 and
+                            avoid re-querying the BVH for slab sets above 64 */
 } rg_config;
 
 enum { RG_BASIS_GAUSSIAN = 0, RG_BASIS_BUMP = 1, RG_BASIS_WENDLAND = 2,

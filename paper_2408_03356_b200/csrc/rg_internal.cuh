@@ -280,7 +280,7 @@ __device__ __forceinline__ void sh_basis(int deg, float x, float y, float z, flo
 // slots, then a shared overflow region bump-allocated through the counter); then the sample
 // arena (one float4 (sigma, sigma c) per lane of a stored window).  Split of the
 // space after the records: rest / 80 pair slots, the remainder float4 samples.
-constexpr int kLogWords = 64;
+constexpr int kLogWords = 128;
 __host__ __device__ inline size_t fetch_log_header_bytes(int n_rays) {
   return 256 + ((4 * (size_t)kLogWords * (size_t)(n_rays > 0 ? n_rays : 1) + 255) & ~(size_t)255);
 }

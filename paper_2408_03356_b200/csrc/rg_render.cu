@@ -170,6 +170,10 @@ using WMBwd = WarpMemT<kStkBwd, 1, 1>;     // the backward refills by restart qu
 // slab with restart queries (C4: 7750 -> ~100 queries per ray); two 4-warp blocks per SM
 constexpr int kABig = 520;
 using WMBig = WarpMemT<320, 1, 32, kABig, kABig + 32>;
+// a medium list (rg_config.list_capacity 65..128): per-slab sets of up to 128 without
+// streaming, four blocks per SM (C3: slab sets above 64 Gaussians are common)
+constexpr int kAMid = 128;
+using WMMid = WarpMemT<kStkFwd, 1, 32, kAMid, kAMid + 64>;
 struct WarpAcc {
   float4 a[kSlots];    // Sw, Sw1, Sw2, dc_r
   float2 b[kSlots];    // dc_g, dc_b
@@ -1139,7 +1143,7 @@ __device__ __forceinline__ int held_le(const WM& M, int count, float x) {
 // INSTR: counters (rg_stats) and the debug dump; the uninstrumented variant
 // compiles them out (8 fewer live registers through the march)
 template <bool BWD, int GW, bool INSTR, int BASIS, int KA = kA>
-__global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kA ? RG_MIN_BLOCKS_FWD : 2))
+__global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2 : RG_MIN_BLOCKS_FWD))
     k_render(const RenderArgs P) {
   static_assert(KA == kA || !BWD, "the large-list variant is forward only");
   // static shared memory (fwd 35.6 KB, bwd 48.0 KB <= the 48 KB static limit): constant
@@ -1148,7 +1152,9 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kA ? RG_M
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const unsigned lane = lane_id();
   const int wid = threadIdx.x >> 5;
-  using WM = std::conditional_t<BWD, WMBwd, std::conditional_t<KA == kA, WMFwd, WMBig>>;
+  using WM = std::conditional_t<
+      BWD, WMBwd,
+      std::conditional_t<KA == kA, WMFwd, std::conditional_t<KA == kAMid, WMMid, WMBig>>>;
   WM& M = reinterpret_cast<WM*>(smem_raw)[wid];
   WarpAcc& A = reinterpret_cast<WarpAcc*>(smem_raw + sizeof(WM) * kWarps)[BWD ? wid : 0];
   int ray;
@@ -1233,6 +1239,54 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kA ? RG_M
     if (lane == 0) M.sst.valid = false;   // forward: persistent traversal restarts on first use
     __syncwarp();
     int nref = 0;                         // forward refills of this ray so far
+    // fetch log: the forward appends each query's set-up pair slots [slot0, slot0 + got)
+    // (the ray's own pair_fix slots first, then the shared overflow region, one atomic
+    // per query) and a (count, arena offset) record; the backward reads them back in
+    // the same order (refills and the chunks of slab sets larger than the list)
+    auto log_fetch = [&](int got, int slot0) {
+      unsigned long long off = 0;
+      bool fits = true;
+      if (fix_used + got <= P.pair_fix) {
+        off = (unsigned long long)ray * P.pair_fix + fix_used;
+        fix_used += got;
+      } else {
+        if (lane == 0 && got > 0) off = atomicAdd(P.arena_ctr, (unsigned long long)got);
+        off = shfl64(off, 0) + (unsigned long long)P.n_rays * P.pair_fix;
+        fits = (long long)(off + got) <= P.arena_cap;
+      }
+      if (lp + 2 > kLogWords - nwin && nwin > 0 && lp + 2 <= kLogWords) {
+        // fetch records are required, stored windows optional (recomputed by the
+        // backward): drop the last stored windows (the stored ones stay a prefix
+        // of the ray's windows; no further window is stored)
+        nwin = kLogWords - (lp + 2) < nwin ? kLogWords - (lp + 2) : nwin;
+        wlog = false;
+      }
+      if (lp + 2 > kLogWords - nwin || !fits) {
+        log_ok = false;
+      } else {
+        if (lane == 0) { lg[lp] = got; lg[lp + 1] = (int)off; }
+        lp += 2;
+        __syncwarp();
+        if ((int)lane < got) {
+          float4* dst = P.arena + 3 * (off + lane);
+          dst[0] = M.e0[slot0 + lane];
+          dst[1] = M.e1[slot0 + lane];
+          dst[2] = M.e2[slot0 + lane];
+        }
+      }
+    };
+    auto read_fetch = [&](int slot0) {
+      const int got = lg[lp];
+      const long long off = (long long)(unsigned)lg[lp + 1];
+      lp += 2;
+      if ((int)lane < got) {
+        const float4* src = P.arena + 3 * (off + lane);
+        M.e0[slot0 + lane] = src[0];
+        M.e1[slot0 + lane] = src[1];
+        M.e2[slot0 + lane] = src[2];
+      }
+      return got;
+    };
     int s = 0;
     while (true) {
       const int k0 = s * B;
@@ -1328,15 +1382,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kA ? RG_M
         uint32_t pos = 0;
         int got;
         if (BWD && replay_log) {      // the forward's set-up pairs: no traversal, no set-up
-          got = lg[lp];
-          const long long off = (long long)(unsigned)lg[lp + 1];
-          lp += 2;
-          if ((int)lane < got) {
-            const float4* src = P.arena + 3 * (off + lane);
-            M.e0[count + lane] = src[0];
-            M.e1[count + lane] = src[1];
-            M.e2[count + lane] = src[2];
-          }
+          got = read_fetch(count);
         } else {
           if constexpr (BWD) {
             got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
@@ -1352,40 +1398,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kA ? RG_M
             ++nref;
           }
           if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, count + (int)lane, R, pos);
-          if (!BWD && log_ok) {
-            // the ray's own pair_fix slots first (no allocation), then the shared
-            // overflow region (one atomic per fetch)
-            unsigned long long off = 0;
-            bool fits = true;
-            if (fix_used + got <= P.pair_fix) {
-              off = (unsigned long long)ray * P.pair_fix + fix_used;
-              fix_used += got;
-            } else {
-              if (lane == 0 && got > 0) off = atomicAdd(P.arena_ctr, (unsigned long long)got);
-              off = shfl64(off, 0) + (unsigned long long)P.n_rays * P.pair_fix;
-              fits = (long long)(off + got) <= P.arena_cap;
-            }
-            if (lp + 2 > kLogWords - nwin && nwin > 0 && lp + 2 <= kLogWords) {
-              // fetch records are required, stored windows optional (recomputed by the
-              // backward): drop the last stored windows (the stored ones stay a prefix
-              // of the ray's windows; no further window is stored)
-              nwin = kLogWords - (lp + 2) < nwin ? kLogWords - (lp + 2) : nwin;
-              wlog = false;
-            }
-            if (lp + 2 > kLogWords - nwin || !fits) {
-              log_ok = false;
-            } else {
-              if (lane == 0) { lg[lp] = got; lg[lp + 1] = (int)off; }
-              lp += 2;
-              __syncwarp();
-              if ((int)lane < got) {
-                float4* dst = P.arena + 3 * (off + lane);
-                dst[0] = M.e0[count + lane];
-                dst[1] = M.e1[count + lane];
-                dst[2] = M.e2[count + lane];
-              }
-            }
-          }
+          if (!BWD && log_ok) log_fetch(got, count);
         }
         if (BWD && (int)lane < got) {
           A.a[count + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1618,12 +1631,12 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kA ? RG_M
       const bool more = (n_in == KA) && !exhausted && (K > KA);
       if (n_in > K) {
         if (lane == 0) cnt.overflows++;
-      } else if (!BWD && n_in == K && n_in == KA && !exhausted) {
+      } else if (INSTR && !BWD && n_in == K && n_in == KA && !exhausted) {   // counter only
         unsigned long long pk;
         uint32_t pp;
         if (fetch(P.S, M, R, tlo, thi, cursor, 1, pk, pp, cnt) > 0 && lane == 0) cnt.overflows++;
       }
-      if (!BWD && (more || (n_in == K && n_in == KA && !exhausted))) {
+      if (!BWD && (more || (INSTR && n_in == K && n_in == KA && !exhausted))) {
         __syncwarp();                        // a restart query reused the traversal memory
         if (lane == 0) M.sst.valid = false;
         __syncwarp();
@@ -1646,6 +1659,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kA ? RG_M
             const int got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
             if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, KA + (int)lane, R, pos);
             __syncwarp();
+            if (!BWD && log_ok) log_fetch(got, KA);
             eval_range<GW, BASIS>(M, KA, KA + got, L, tk, val, sg, sr, sgg, sb, ev);
             if (dbg && g0 == 0) dbg_put(P, ray, dbg_n, s, got, M, KA);
             if (g0 == 0 && lane == 0) cnt.pairs += got;
@@ -1654,7 +1668,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kA ? RG_M
             __syncwarp();
             if (got < want) { full_last = false; break; }
           }
-          if (g0 == 0 && remaining == 0 && full_last) {
+          if (INSTR && g0 == 0 && remaining == 0 && full_last) {   // overflow counter only
             unsigned long long pk;
             uint32_t pp;
             if (fetch(P.S, M, R, tlo, thi, cur2, 1, pk, pp, cnt) > 0 && lane == 0) cnt.overflows++;
@@ -1730,9 +1744,14 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kA ? RG_M
               const int want = min(32, remaining);
               unsigned long long key;
               uint32_t pos;
-              const int got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
+              int got;
+              if (replay_log) {           // the forward logged this chunk's set-up pairs
+                got = read_fetch(kA);
+              } else {
+                got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
+                if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, kTrans + (int)lane, R, pos);
+              }
               if ((int)lane < got) {
-                setup_pair<!BWD, BASIS>(P.S, M, kTrans + (int)lane, R, pos);
                 A.a[kA + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
                 A.b[kA + lane] = make_float2(0.f, 0.f);
                 A.c[kA + lane] = 0.f;
@@ -1742,7 +1761,11 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kA ? RG_M
               scatter_batch<BASIS>(P.S, M, A, kA, got >= 32 ? kFull : ((1u << got) - 1u), R, P.gbuf,
                             P.gstride);
               remaining -= got;
-              if (got > 0) cur2 = shfl64(key, got - 1);
+              if (got > 0) {
+                const int l = kA + got - 1;
+                cur2 = replay_log ? (((unsigned long long)fkey(M.e0[l].x) << 32) | __float_as_uint(M.e2[l].z))
+                                  : shfl64(key, got - 1);
+              }
               __syncwarp();
               if (got < want) break;
             }
@@ -1967,6 +1990,7 @@ void launch_gw(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
 }
 
 constexpr size_t kSmemBig = sizeof(WMBig) * kWarps;
+constexpr size_t kSmemMid = sizeof(WMMid) * kWarps;
 static_assert(2 * (kSmemBig + 1024) <= 228 * 1024, "two large-list blocks per SM");
 
 template <bool BWD>
@@ -1974,11 +1998,15 @@ void launch_render(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st)
   const int B = A.c.slab_samples;
   // forward large-list variant (rg_config.list_capacity, Gaussian basis, B >= 5)
   if constexpr (!BWD) {
-    if (A.c.list_capacity > kA && A.c.basis == 0 && B >= 5 && A.c.hit_capacity < kABig) {
-      if (A.stats != nullptr || A.dbg_rec != nullptr)
-        launch_one<false, 8, true, 0, kABig>(A, grid, kSmemBig, st);
-      else
-        launch_one<false, 8, false, 0, kABig>(A, grid, kSmemBig, st);
+    const bool instr = A.stats != nullptr || A.dbg_rec != nullptr;
+    if (A.c.list_capacity > kAMid && A.c.basis == 0 && B >= 5 && A.c.hit_capacity < kABig) {
+      if (instr) launch_one<false, 8, true, 0, kABig>(A, grid, kSmemBig, st);
+      else launch_one<false, 8, false, 0, kABig>(A, grid, kSmemBig, st);
+      return;
+    }
+    if (A.c.list_capacity > kA && A.c.basis == 0 && B >= 5) {
+      if (instr) launch_one<false, 8, true, 0, kAMid>(A, grid, kSmemMid, st);
+      else launch_one<false, 8, false, 0, kAMid>(A, grid, kSmemMid, st);
       return;
     }
   }

@@ -194,7 +194,7 @@ def test_forward_slab_sizes(oracle, B):
 
 
 @pytest.mark.parametrize("K,lc", [(3, 0), (32, 0), (40, 0), (100, 0), (3, 520), (40, 520),
-                                  (100, 520)])
+                                  (100, 520), (40, 128), (100, 128), (300, 128)])
 def test_forward_overflow_truncation(oracle, K, lc):
     """Per-slab sets larger than K (and larger than the active list) keep the
     K smallest (t_entry, index) exactly (L7); lc = rg_config.list_capacity
@@ -204,7 +204,7 @@ def test_forward_overflow_truncation(oracle, K, lc):
     p = synth.RenderParams(dt=4e-3, slab_samples=8, t_eps=1e-4, hit_capacity=K, list_capacity=lc)
     o, d = oracle.camera_rays(synth.orbit_camera(2.2, 10, 25, 12, 12, 14.0))
     rg_, ref, ok = _fwd_case(oracle, sc, p, o, d, debug_rays=144, cap=60000)
-    assert ref["counters"]["overflows"] > 0
+    assert ref["counters"]["overflows"] > 0 or K >= 300
     if ok.all():
         assert rg_["stats"]["overflows"] == ref["counters"]["overflows"]
         assert rg_["stats"]["evals"] == ref["counters"]["evals"]
