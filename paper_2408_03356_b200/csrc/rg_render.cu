@@ -121,6 +121,7 @@ struct WarpMemT {
   static constexpr int kNCap = NCAP;
   static constexpr int kCCap = CCAP;
   static constexpr int kList = KA;     // active-list capacity
+  static constexpr int kNSlots = SLOTS;
   static constexpr int kTr = KA;       // first transient slot (restart-query scratch)
   float4 e0[SLOTS], e1[SLOTS], e2[SLOTS];
   union {
@@ -174,10 +175,12 @@ using WMBig = WarpMemT<320, 1, 32, kABig, kABig + 32>;
 // streaming, four blocks per SM (C3: slab sets above 64 Gaussians are common)
 constexpr int kAMid = 128;
 using WMMid = WarpMemT<kStkFwd, 1, 32, kAMid, kAMid + 64>;
-struct WarpAcc {
-  float4 a[kSlots];    // Sw, Sw1, Sw2, dc_r
-  float2 b[kSlots];    // dc_g, dc_b
-  float c[kSlots];     // sum w dL/dw (dL/dsigma~ of non-Gaussian bases; = a.x for the Gaussian)
+using WMBwdMid = WarpMemT<kStkBwd, 1, 1, kAMid, kAMid + 64>;
+template <int SLOTS>
+struct WarpAccT {
+  float4 a[SLOTS];     // Sw, Sw1, Sw2, dc_r
+  float2 b[SLOTS];     // dc_g, dc_b
+  float c[SLOTS];      // sum w dL/dw (dL/dsigma~ of non-Gaussian bases; = a.x for the Gaussian)
   float4 s0[32];
   float s1[32];        // per-sample backward values of the current group / window:
                           // {tk, dls, dc0, dc1}, {dc2, gc, inv, live}
@@ -923,8 +926,8 @@ struct SampleGrad {   // per-sample backward quantities (lanes of sample j)
 // accumulate the per-pair moments of slots [e0, e1) over this group's samples:
 // lane = slot, loop over the GW samples whose backward values the composite
 // step left in A.s0/A.s1 (broadcast reads), moments kept in registers.
-template <int GW, int BASIS, class WM>
-__device__ __forceinline__ void grad_range(const WM& M, WarpAcc& A, int e0, int e1) {
+template <int GW, int BASIS, class WM, class AC>
+__device__ __forceinline__ void grad_range(const WM& M, AC& A, int e0, int e1) {
   __syncwarp();
   for (int base = e0; base < e1; base += 32) {
     const int e = base + (int)lane_id();
@@ -972,8 +975,8 @@ __device__ __forceinline__ void grad_range(const WM& M, WarpAcc& A, int e0, int 
 //  With x = x' + tau d, u = M x', d_l = M d and Sw = sum w dL/dw, Sw1 = sum w dL/dw tau,
 //  Sw2 = sum w dL/dw tau^2:  dL/dmu = M^T (Sw u + Sw1 d_l),
 //  dL/dM = -(Sw u x'^T + Sw1 (u d^T + d_l x'^T) + Sw2 d_l d^T),  dL/dsigma~ = Sw / sigma~.
-template <int BASIS, class WM>
-__device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, const WarpAcc& A,
+template <int BASIS, class WM, class AC>
+__device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, const AC& A,
                                            int base, unsigned mask, const Ray& R,
                                            float* gbuf, int gstride) {
   const unsigned lane = lane_id();
@@ -1145,7 +1148,7 @@ __device__ __forceinline__ int held_le(const WM& M, int count, float x) {
 template <bool BWD, int GW, bool INSTR, int BASIS, int KA = kA>
 __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2 : RG_MIN_BLOCKS_FWD))
     k_render(const RenderArgs P) {
-  static_assert(KA == kA || !BWD, "the large-list variant is forward only");
+  static_assert(KA != kABig || !BWD, "the large-list variant is forward only");
   // static shared memory (fwd 35.6 KB, bwd 48.0 KB <= the 48 KB static limit): constant
   // shared-window offsets; the dynamic (extern) form made the compiler re-derive the
   // window base (S2UR SR_CgaCtaId + ULEA) at loop heads of the hot loops
@@ -1153,10 +1156,12 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
   const unsigned lane = lane_id();
   const int wid = threadIdx.x >> 5;
   using WM = std::conditional_t<
-      BWD, WMBwd,
+      BWD, std::conditional_t<KA == kA, WMBwd, WMBwdMid>,
       std::conditional_t<KA == kA, WMFwd, std::conditional_t<KA == kAMid, WMMid, WMBig>>>;
   WM& M = reinterpret_cast<WM*>(smem_raw)[wid];
-  WarpAcc& A = reinterpret_cast<WarpAcc*>(smem_raw + sizeof(WM) * kWarps)[BWD ? wid : 0];
+  using AC = WarpAccT<WM::kNSlots>;
+  AC& A = reinterpret_cast<AC*>(smem_raw + sizeof(WM) * kWarps)[BWD ? wid : 0];
+  constexpr int kRetK = KA + 32;       // backward: retired (expired, not yet scattered) slots
   int ray;
   Ray R;
   bool inside = true;             // false: a tile-sharding slot outside the rectangle (a miss)
@@ -1229,7 +1234,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
     bool exhausted = false;
     int32_t* lg = P.log ? P.log + (size_t)ray * kLogWords : nullptr;
     int lp = 1;
-    bool log_ok = lg != nullptr;
+    bool log_ok = lg != nullptr && KA != kABig;   // no backward replays the large list
     const bool replay_log = BWD && lg != nullptr && lg[0] >= 0;
     // stored windows (forward: count so far; backward: how many the forward stored)
     int nwin = BWD ? (replay_log ? (lg[0] >> 16) : 0) : 0;
@@ -1293,13 +1298,15 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
       if (!(sample_t(k0, c.dt, t0) < t1)) break;
       const float tlo = fma_((float)k0, c.dt, t0);
       const float thi = fminf(t1, fma_((float)(k0 + B), c.dt, t0));
-      // ---- expire Gaussians whose support ended before this slab
-      if constexpr (KA != kA) {   // large list: chunked compaction from the first expired entry
+      // ---- expire Gaussians whose support ended before this slab: chunks of 32
+      // slots, compaction from the first expired entry on; the backward first
+      // retires the expired pairs (their moments) and scatters them 32 at a time
+      {
         int nc = 0;
         bool moved = false;
-        for (int h = 0; 32 * h < count; ++h) {
+        auto expire_chunk = [&](int h, int& nc, bool& moved) {
           const int e = 32 * h + (int)lane;
-          float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0, v2 = v0;
+          float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f);
           bool keep = false;
           if (e < count) {
             v0 = M.e0[e];
@@ -1307,70 +1314,49 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
           }
           const unsigned km = __ballot_sync(kFull, keep);
           const int nin = min(32, count - 32 * h);
-          if (!moved && __popc(km) == nin) { nc += nin; continue; }
+          if (!moved && __popc(km) == nin) { nc += nin; return; }
           moved = true;
-          if (keep) { v1 = M.e1[e]; v2 = M.e2[e]; }
-          const int dst = nc + __popc(km & ((1u << lane) - 1u));
-          __syncwarp();
-          if (keep) { M.e0[dst] = v0; M.e1[dst] = v1; M.e2[dst] = v2; }
-          nc += __popc(km);
-          __syncwarp();
-        }
-        count = nc;
-      } else {
-        unsigned gone0 = 0, gone1 = 0;
-        {
-          const int e = (int)lane;
-          gone0 = __ballot_sync(kFull, e < count && M.e0[e].y < tlo);
-          gone1 = __ballot_sync(kFull, e + 32 < count && M.e0[e + 32].y < tlo);
-        }
-        if (gone0 | gone1) {
-          if (BWD) {   // retire expired pairs; scatter them 32 at a time
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const unsigned gm = h ? gone1 : gone0;
-              if (!gm) continue;
-              if (nret + __popc(gm) > 32) {
-                scatter_batch<BASIS>(P.S, M, A, kRet, nret >= 32 ? kFull : ((1u << nret) - 1u), R,
-                              P.gbuf, P.gstride);
-                nret = 0;
-                __syncwarp();
-              }
-              if ((gm >> lane) & 1u) {
-                const int e = h * 32 + (int)lane;
-                const int dst = kRet + nret + __popc(gm & ((1u << lane) - 1u));
-                M.e0[dst] = M.e0[e]; M.e1[dst] = M.e1[e]; M.e2[dst] = M.e2[e];
-                A.a[dst] = A.a[e]; A.b[dst] = A.b[e];
-                if (BASIS != 0) A.c[dst] = A.c[e];
-              }
-              nret += __popc(gm);
+          if constexpr (BWD) {   // retire this chunk's expired pairs
+            const unsigned gm = __ballot_sync(kFull, e < count && !keep);
+            if (nret + __popc(gm) > 32) {
+              scatter_batch<BASIS>(P.S, M, A, kRetK, nret >= 32 ? kFull : ((1u << nret) - 1u), R,
+                                   P.gbuf, P.gstride);
+              nret = 0;
               __syncwarp();
             }
+            if ((gm >> lane) & 1u) {
+              const int dst = kRetK + nret + __popc(gm & ((1u << lane) - 1u));
+              M.e0[dst] = v0; M.e1[dst] = M.e1[e]; M.e2[dst] = M.e2[e];
+              A.a[dst] = A.a[e]; A.b[dst] = A.b[e];
+              if (BASIS != 0) A.c[dst] = A.c[e];
+            }
+            nret += __popc(gm);
+            __syncwarp();
           }
-          int nc = 0;
+          float4 v1 = v0, v2 = v0, a0 = v0;
+          float2 a1 = make_float2(0.f, 0.f);
+          float a2c = 0.f;
+          if (keep) {
+            v1 = M.e1[e]; v2 = M.e2[e];
+            if (BWD) { a0 = A.a[e]; a1 = A.b[e]; if (BASIS != 0) a2c = A.c[e]; }
+          }
+          const int dst = nc + __popc(km & ((1u << lane) - 1u));
+          __syncwarp();
+          if (keep) {
+            M.e0[dst] = v0; M.e1[dst] = v1; M.e2[dst] = v2;
+            if (BWD) { A.a[dst] = a0; A.b[dst] = a1; if (BASIS != 0) A.c[dst] = a2c; }
+          }
+          nc += __popc(km);
+          __syncwarp();
+        };
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int e = h * 32 + (int)lane;
-            const bool keep = e < count && !(((h ? gone1 : gone0) >> lane) & 1u);
-            float4 v0, v1, v2, a0;
-            float2 a1;
-            float a2c = 0.f;
-            if (keep) {
-              v0 = M.e0[e]; v1 = M.e1[e]; v2 = M.e2[e];
-              if (BWD) { a0 = A.a[e]; a1 = A.b[e]; if (BASIS != 0) a2c = A.c[e]; }
-            }
-            const unsigned km = __ballot_sync(kFull, keep);
-            const int dst = nc + __popc(km & ((1u << lane) - 1u));
-            __syncwarp();
-            if (keep) {
-              M.e0[dst] = v0; M.e1[dst] = v1; M.e2[dst] = v2;
-              if (BWD) { A.a[dst] = a0; A.b[dst] = a1; if (BASIS != 0) A.c[dst] = a2c; }
-            }
-            nc += __popc(km);
-            __syncwarp();
-          }
-          count = nc;
+        for (int h = 0; h < (KA == kA ? KA / 32 : 1); ++h) {     // unrolled: the 64-slot list
+          if (KA != kA || 32 * h >= count) break;
+          expire_chunk(h, nc, moved);
         }
+#pragma unroll 1
+        for (int h = 0; KA != kA && 32 * h < count; ++h) expire_chunk(h, nc, moved);
+        count = nc;
       }
       // 4-slab window (B = 8: 32 samples, one per lane); thr = t_hi of its last slab
       const bool win = (GW == 8) && (B == 8);
@@ -1746,23 +1732,23 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
               uint32_t pos;
               int got;
               if (replay_log) {           // the forward logged this chunk's set-up pairs
-                got = read_fetch(kA);
+                got = read_fetch(KA);
               } else {
                 got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
-                if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, kTrans + (int)lane, R, pos);
+                if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, KA + (int)lane, R, pos);
               }
               if ((int)lane < got) {
-                A.a[kA + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-                A.b[kA + lane] = make_float2(0.f, 0.f);
-                A.c[kA + lane] = 0.f;
+                A.a[KA + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+                A.b[KA + lane] = make_float2(0.f, 0.f);
+                A.c[KA + lane] = 0.f;
               }
               __syncwarp();
-              grad_range<GW, BASIS>(M, A, kA, kA + got);
-              scatter_batch<BASIS>(P.S, M, A, kA, got >= 32 ? kFull : ((1u << got) - 1u), R, P.gbuf,
+              grad_range<GW, BASIS>(M, A, KA, KA + got);
+              scatter_batch<BASIS>(P.S, M, A, KA, got >= 32 ? kFull : ((1u << got) - 1u), R, P.gbuf,
                             P.gstride);
               remaining -= got;
               if (got > 0) {
-                const int l = kA + got - 1;
+                const int l = KA + got - 1;
                 cur2 = replay_log ? (((unsigned long long)fkey(M.e0[l].x) << 32) | __float_as_uint(M.e2[l].z))
                                   : shfl64(key, got - 1);
               }
@@ -1782,11 +1768,13 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
       ++s;
     }
     if (BWD) {
-      const unsigned m0 = count >= 32 ? kFull : ((1u << count) - 1u);
-      const unsigned m1 = count >= 64 ? kFull : (count > 32 ? ((1u << (count - 32)) - 1u) : 0u);
-      scatter_batch<BASIS>(P.S, M, A, 0, m0, R, P.gbuf, P.gstride);
-      scatter_batch<BASIS>(P.S, M, A, 32, m1, R, P.gbuf, P.gstride);
-      scatter_batch<BASIS>(P.S, M, A, kRet, nret >= 32 ? kFull : ((1u << nret) - 1u), R, P.gbuf,
+#pragma unroll 1
+      for (int h = 0; 32 * h < count; ++h) {    // the pairs still held, 32 at a time
+        const int c = count - 32 * h;
+        scatter_batch<BASIS>(P.S, M, A, 32 * h, c >= 32 ? kFull : ((1u << c) - 1u), R, P.gbuf,
+                             P.gstride);
+      }
+      scatter_batch<BASIS>(P.S, M, A, kRetK, nret >= 32 ? kFull : ((1u << nret) - 1u), R, P.gbuf,
                     P.gstride);
     } else if (lg != nullptr && lane == 0) {
       lg[0] = log_ok ? (lp | (nwin << 16)) : -1;
@@ -1989,6 +1977,12 @@ void launch_gw(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
   else launch_one<BWD, GW, false, BASIS>(A, grid, smem, st);
 }
 
+constexpr size_t kSmemFwd = sizeof(WMFwd) * kWarps;
+constexpr size_t kSmemBwd = (sizeof(WMBwd) + sizeof(WarpAccT<WMBwd::kNSlots>)) * kWarps;
+constexpr size_t kSmemBwdMid = (sizeof(WMBwdMid) + sizeof(WarpAccT<WMBwdMid::kNSlots>)) * kWarps;
+// 4 resident backward blocks must fit the 196 KB shared-memory carve-out (1 KB
+// reserved per block): a larger carve-out halves L1 and costs ~6% (measured)
+static_assert(kSmemBwd <= 48 * 1024 + 128, "backward block exceeds the 196 KB carve-out budget");
 constexpr size_t kSmemBig = sizeof(WMBig) * kWarps;
 constexpr size_t kSmemMid = sizeof(WMMid) * kWarps;
 static_assert(2 * (kSmemBig + 1024) <= 228 * 1024, "two large-list blocks per SM");
@@ -2009,6 +2003,15 @@ void launch_render(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st)
       else launch_one<false, 8, false, 0, kAMid>(A, grid, kSmemMid, st);
       return;
     }
+  } else {
+    // the backward replays the forward's log, so it runs the same list: the medium
+    // list has a backward variant; the large list's forward writes no log (its rays
+    // are re-traversed by the 64-slot backward)
+    if (A.c.list_capacity > kA && A.c.list_capacity <= kAMid && A.c.basis == 0 && B >= 5) {
+      if (A.stats != nullptr) launch_one<true, 8, true, 0, kAMid>(A, grid, kSmemBwdMid, st);
+      else launch_one<true, 8, false, 0, kAMid>(A, grid, kSmemBwdMid, st);
+      return;
+    }
   }
   // non-Gaussian bases (NEXT-3) are instantiated for GW = 8 only (B >= 5; the API
   // rejects them otherwise)
@@ -2026,11 +2029,7 @@ void launch_render(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st)
   else launch_gw<BWD, 1, 0>(A, grid, smem, st);
 }
 
-constexpr size_t kSmemFwd = sizeof(WMFwd) * kWarps;
-constexpr size_t kSmemBwd = (sizeof(WMBwd) + sizeof(WarpAcc)) * kWarps;
-// 4 resident backward blocks must fit the 196 KB shared-memory carve-out (1 KB
-// reserved per block): a larger carve-out halves L1 and costs ~6% (measured)
-static_assert(kSmemBwd <= 48 * 1024 + 128, "backward block exceeds the 196 KB carve-out budget");
+
 
 // fetch-log layout (rg_internal.cuh): counter | per-ray records | arena
 void set_log(RenderArgs& A, const void* log, size_t log_bytes, int n_rays) {

@@ -305,19 +305,30 @@ def test_backward_matches_oracle(oracle, seed, deg, sg, n):
     assert rg.stats_dict(st)["nonfinite_grads"] == 0
 
 
-def test_backward_overflow_path(oracle):
-    """Backward through truncated slabs larger than the active list (K > 32)."""
+@pytest.mark.parametrize("K,lc", [(48, 0), (100, 0), (100, 128), (150, 128), (100, 520)])
+def test_backward_overflow_path(oracle, K, lc):
+    """Backward through slab sets larger than the active list (the streamed chunks
+    of the fetch log) and truncated to K; lc = rg_config.list_capacity (128: the
+    medium list in both passes; 520: the large forward list, whose rays the
+    backward re-traverses)."""
     sc = synth.random_scene(1200, 300, sh_degree=1, sg_count=1, density_range=(0.3, 2.0),
                             scale_range=(0.1, 0.3), extent=0.3)
-    p = synth.RenderParams(dt=4e-3, slab_samples=8, t_eps=1e-4, hit_capacity=48)
+    p = synth.RenderParams(dt=4e-3, slab_samples=8, t_eps=1e-4, hit_capacity=K, list_capacity=lc)
     o, d = oracle.camera_rays(synth.orbit_camera(2.2, 10, 25, 10, 10, 12.0))
     g, b = gpu_build(sc, p)
     cfg = rg.Config.of(p)
     to, td = torch.from_numpy(o).cuda(), torch.from_numpy(d).cuda()
-    fwd = rg.render_forward(g, b, cfg, rays=(to, td), log=rg.new_log(len(o)))
+    fwd = rg.render_forward(g, b, cfg, rays=(to, td), log=rg.new_log(len(o), pairs_per_ray=400))
     up = np.random.default_rng(5).normal(size=(len(o), 3)).astype(np.float32)
     grads = rg.render_backward(g, b, cfg, fwd, torch.from_numpy(up).cuda(), rays=(to, td))
+    # the log replay (no traversal) and a re-traversal (no log) give the same gradients
+    fwd2 = rg.render_forward(g, b, cfg, rays=(to, td))
+    grads2 = rg.render_backward(g, b, cfg, fwd2, torch.from_numpy(up).cuda(), rays=(to, td))
     torch.cuda.synchronize()
+    for k in grads:
+        a, bb = grads[k].double(), grads2[k].double()
+        sc_ = bb.abs().max().item()
+        assert (a - bb).abs().max().item() <= 1e-5 * max(sc_, 1e-30), k
     ref = oracle.backward(sc, p, o, d, up.astype(np.float64), mode=2)
     grad_check(grads, ref)
 
