@@ -12,6 +12,25 @@
 
 #include "../../include/rg.h"
 
+// Device-side invariant checks (compute-sanitizer is closed on this GPU pool): a
+// build with -DRG_CHECKS (RG_DEFINES=RG_CHECKS python paper_2408_03356_b200/build.py)
+// traps on any shared-memory slot, stack, queue, log-word, arena or gradient-row
+// index outside its buffer; the GPU test suite is run against that build.
+#ifdef RG_CHECKS
+#include <cstdio>
+#define RG_CHECK(c)                                                                    \
+  do {                                                                                 \
+    if (!(c)) {                                                                        \
+      printf("RG_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);                  \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define RG_CHECK(c) \
+  do {              \
+  } while (0)
+#endif
+
 namespace rg {
 
 // ---------------------------------------------------------------------------

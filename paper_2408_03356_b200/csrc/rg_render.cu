@@ -140,6 +140,9 @@ struct WarpMemT {
   } u;
   uint32_t lq[96];     // queued leaves awaiting the exact test (< 32 + 2 x 32)
   Stream sst;          // stream_next state between refills (registers only inside the call)
+  // fetch-log bookkeeping of the ray (warp-uniform, rarely touched): kept here, not in
+  // registers, to relieve the register pressure of the march loops
+  struct { int lp, nwin, wcur, fix; int ok, wl; } ls;
   alignas(16) float Y[16];   // Y(d) of the ray (zero past the degree), read as float4 by the scatter
 };
 // Persistent per-ray traversal (stream_next) for the forward refills: built, measured
@@ -292,6 +295,7 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
         const unsigned long long kb = shfl64(ck, b);
         crank += (cand && kb < ck) ? 1 : 0;
       }
+      RG_CHECK(!cand || crank < 32);
       if (cand) { kscr[crank] = ck; pscr[crank] = cp; }
       __syncwarp();
       ck = (int)lane < ncand ? kscr[lane] : ~0ull;
@@ -391,6 +395,7 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       const unsigned lmB = __ballot_sync(kFull, hitB && childB < 0);
       if (lmA | lmB) {
         __syncwarp();
+        RG_CHECK(qn + __popc(lmA) + __popc(lmB) <= 96);
         if (hitA && childA < 0) M.lq[qn + __popc(lmA & lt_mask)] = (uint32_t)(~childA);
         if (hitB && childB < 0) M.lq[qn + __popc(lmA) + __popc(lmB & lt_mask)] = (uint32_t)(~childB);
         qn += __popc(lmA) + __popc(lmB);
@@ -858,6 +863,7 @@ __device__ __forceinline__ float basis_psi(float w, float qq, float sig) {
 template <bool VEC, int BASIS, class WM>
 __device__ RG_SETUP_ATTR void setup_pair(const SceneView& S, WM& M, int sl, const Ray& R,
                                         uint32_t pos) {
+  RG_CHECK(sl >= 0 && sl < WM::kNSlots && (int)pos < S.n);
   const float4* gp = S.geom + 4 * (size_t)pos;
   const float4 g0 = __ldg(gp), g1 = __ldg(gp + 1), g2 = __ldg(gp + 2), g3 = __ldg(gp + 3);
   PairGeom pg;
@@ -900,6 +906,7 @@ template <int GW, int BASIS, class WM>
 __device__ __forceinline__ void eval_range(const WM& M, int e0, int e1, const Lanes<GW>& L,
                                            float tk, bool val, float& s, float& r, float& g,
                                            float& b, uint32_t& evals) {
+  float2 rg2 = make_float2(r, g);
 #pragma unroll 2
   for (int e = e0 + L.esub; e < e1; e += Lanes<GW>::ER) {
     const float4 a = M.e0[e];
@@ -911,12 +918,13 @@ __device__ __forceinline__ void eval_range(const WM& M, int e0, int e1, const La
       float qq;
       const float w = basis_w<BASIS>(tau, a, q, sge, qq);
       s += w;
-      r = fmaf(w, q.z, r);
-      g = fmaf(w, q.w, g);
+      rg2 = __ffma2_rn(make_float2(w, w), make_float2(q.z, q.w), rg2);
       b = fmaf(w, cb, b);
       ++evals;
     }
   }
+  r = rg2.x;
+  g = rg2.y;
 }
 
 struct SampleGrad {   // per-sample backward quantities (lanes of sample j)
@@ -1020,6 +1028,7 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, c
     const float s11 = fmaf(xp[1], v1, dv[1] * h1);
     const float s12 = fmaf(xp[1], v2, dv[1] * h2);
     const float s22 = fmaf(xp[2], v2, dv[2] * h2);
+    RG_CHECK(pos >= 0 && pos < S.n);
     float4* row = reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride);
     atomicAdd(row + 0, make_float4(v0, v1, v2, (BASIS == 0 ? Sw : A.c[e]) / g0.w));
     atomicAdd(row + 1, make_float4(s00, s01, s02, s11));
@@ -1233,14 +1242,21 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
     unsigned long long cursor = 0;
     bool exhausted = false;
     int32_t* lg = P.log ? P.log + (size_t)ray * kLogWords : nullptr;
-    int lp = 1;
-    bool log_ok = lg != nullptr && KA != kABig;   // no backward replays the large list
+    if (lane == 0) {
+      M.ls.lp = 1; M.ls.wcur = 0; M.ls.fix = 0;
+      M.ls.ok = lg != nullptr && KA != kABig;       // no backward replays the large list
+    }
+    __syncwarp();
+    int& lp = M.ls.lp;
+    int& log_ok = M.ls.ok;
     const bool replay_log = BWD && lg != nullptr && lg[0] >= 0;
     // stored windows (forward: count so far; backward: how many the forward stored)
-    int nwin = BWD ? (replay_log ? (lg[0] >> 16) : 0) : 0;
-    bool wlog = !BWD && log_ok;
-    int wcur = 0;
-    int fix_used = 0;   // forward: pair slots used in the ray's own block
+    int& nwin = M.ls.nwin;
+    int& wlog = M.ls.wl;
+    int& wcur = M.ls.wcur;
+    int& fix_used = M.ls.fix;   // forward: pair slots used in the ray's own block
+    nwin = BWD ? (replay_log ? (lg[0] >> 16) : 0) : 0;
+    wlog = !BWD && log_ok;
     if (lane == 0) M.sst.valid = false;   // forward: persistent traversal restarts on first use
     __syncwarp();
     int nref = 0;                         // forward refills of this ray so far
@@ -1269,6 +1285,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
       if (lp + 2 > kLogWords - nwin || !fits) {
         log_ok = false;
       } else {
+        RG_CHECK(lp + 1 < kLogWords - nwin && (long long)(off + got) <= P.arena_cap);
         if (lane == 0) { lg[lp] = got; lg[lp + 1] = (int)off; }
         lp += 2;
         __syncwarp();
@@ -1281,8 +1298,10 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
       }
     };
     auto read_fetch = [&](int slot0) {
+      RG_CHECK(lp + 1 < kLogWords);
       const int got = lg[lp];
       const long long off = (long long)(unsigned)lg[lp + 1];
+      RG_CHECK(got >= 0 && got <= 32 && slot0 + got <= WM::kNSlots && off + got <= P.arena_cap);
       lp += 2;
       if ((int)lane < got) {
         const float4* src = P.arena + 3 * (off + lane);
@@ -1326,6 +1345,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
             }
             if ((gm >> lane) & 1u) {
               const int dst = kRetK + nret + __popc(gm & ((1u << lane) - 1u));
+              RG_CHECK(dst < WM::kNSlots);
               M.e0[dst] = v0; M.e1[dst] = M.e1[e]; M.e2[dst] = M.e2[e];
               A.a[dst] = A.a[e]; A.b[dst] = A.b[e];
               if (BASIS != 0) A.c[dst] = A.c[e];
@@ -1419,12 +1439,14 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
           bool stored = false;
           if (BWD && !INSTR) {
             if (wcur < nwin) {
+              RG_CHECK(kLogWords - 1 - wcur > 0 && (long long)lg[kLogWords - 1 - wcur] * 32 + 32 <= P.samp_cap);
               const float4 v = P.samp[(size_t)lg[kLogWords - 1 - wcur] * 32 + lane];
               sg = v.x; sr = v.y; sgg = v.z; sb = v.w;
               stored = true;
             }
             ++wcur;
           }
+          float2 srg = make_float2(sr, sgg);   // (r, g) sums: one packed FFMA2 per member
 #pragma unroll kEvalUnroll
           for (int e = 0; e < (stored ? 0 : n3); ++e) {
             const float4 a = M.e0[e];
@@ -1436,12 +1458,13 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
               float qq;
               const float w = basis_w<BASIS>(tau_, a, q, sge, qq);
               sg += w;
-              sr = fmaf(w, q.z, sr);
-              sgg = fmaf(w, q.w, sgg);
+              srg = __ffma2_rn(make_float2(w, w), make_float2(q.z, q.w), srg);
               sb = fmaf(w, cbv, sb);
               ++ev;
             }
           }
+          sr = srg.x;
+          sgg = srg.y;
           if (!BWD && wlog && log_ok) {   // store this window's sums for the backward
             unsigned long long off = 0;
             if (lane == 0) off = atomicAdd(P.samp_ctr, 32ull);
@@ -1450,6 +1473,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
             if (kLogWords - nwin - lp < 9 || (long long)(off + 32) > P.samp_cap) {
               wlog = false;
             } else {
+              RG_CHECK(kLogWords - 1 - nwin > lp);
               if (lane == 0) lg[kLogWords - 1 - nwin] = (int)(off >> 5);
               P.samp[off + lane] = make_float4(sg, sr, sgg, sb);
               ++nwin;
@@ -1543,7 +1567,8 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
             for (int base = 0; base < n3; base += P2) {
               const int e = base + ((int)lane & (P2 - 1));
               const int part0 = (int)lane & ~(P2 - 1);   // first sample of this lane's part
-              float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f, a6 = 0.f;
+              float a0 = 0.f, a1 = 0.f, a2 = 0.f, a5 = 0.f, a6 = 0.f;
+              float2 a34 = make_float2(0.f, 0.f);   // (dc_r, dc_g) moments: packed FFMA2
               float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
               if (e < n3) {
                 a = M.e0[e];
@@ -1571,13 +1596,13 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
                     a0 += wd;
                     a1 = fmaf(wd, tau_, a1);
                     a2 = fmaf(wd * tau_, tau_, a2);
-                    a3 = fmaf(w, s0.z, a3);
-                    a4 = fmaf(w, s0.w, a4);
+                    a34 = __ffma2_rn(make_float2(w, w), make_float2(s0.z, s0.w), a34);
                     a5 = fmaf(w, b2, a5);
                     if (BASIS != 0) a6 = fmaf(w, dldw, a6);
                   }
                 }
               }
+              float a3 = a34.x, a4 = a34.y;
               for (int off = P2; off < 32; off <<= 1) {
                 a0 += __shfl_xor_sync(kFull, a0, off);
                 a1 += __shfl_xor_sync(kFull, a1, off);
