@@ -671,14 +671,15 @@ def next_section(ctx, args, g, sc, p, cfg, cam, wl, bws, gws, gb, fo, flog, tgt_
     }
 
 
-def relaunch_distributed(n):
-    """python bench.py --gpus N (no torchrun environment): re-run under torch.distributed.run"""
+def relaunch_distributed(n, script=None, argv=None):
+    """python bench.py --gpus N (no torchrun environment): re-run under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1 at a free port)"""
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
-           *sys.argv[1:]]
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(script or __file__), *(sys.argv[1:] if argv is None else argv)]
     return subprocess.call(cmd)
 
 

@@ -1158,9 +1158,9 @@ template <bool BWD, int GW, bool INSTR, int BASIS, int KA = kA>
 __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2 : RG_MIN_BLOCKS_FWD))
     k_render(const RenderArgs P) {
   static_assert(KA != kABig || !BWD, "the large-list variant is forward only");
-  // static shared memory (fwd 35.6 KB, bwd 48.0 KB <= the 48 KB static limit): constant
-  // shared-window offsets; the dynamic (extern) form made the compiler re-derive the
-  // window base (S2UR SR_CgaCtaId + ULEA) at loop heads of the hot loops
+  // dynamic shared memory: per-warp WarpMem (+ WarpAcc in the backward) at fixed
+  // offsets; the compiler re-derives the window base (S2R SR_CgaCtaId + LEA) at some
+  // loop heads, but the static form measured slower (backward +2.3%)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const unsigned lane = lane_id();
   const int wid = threadIdx.x >> 5;

@@ -179,3 +179,15 @@ def test_sharded_adam_equals_full_adam():
         for k in rgd.GROUPS:
             assert np.allclose(res[r][k], act[k], rtol=2e-6, atol=1e-7), (r, k)
     assert all(np.array_equal(res[0][k], res[1][k]) for k in rgd.GROUPS)   # replicas identical
+
+
+def test_bench_relaunch_world2_tile_plumbing():
+    """bench.py's `--gpus N` re-launch (torch.distributed.run, 127.0.0.1) at world
+    size 2 on CPU/gloo, running the tile-sharding plumbing check: per-rank
+    rg_camera tile cameras of the C1 and C3 views, rg_camera_ray_count (host) =
+    the slot count, and the ranks' slots cover every pixel exactly once."""
+    import bench
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    rc = bench.relaunch_distributed(2, script=os.path.join(root, "tools", "dist_tile_check.py"),
+                                    argv=[])
+    assert rc == 0
