@@ -25,7 +25,9 @@
  *       sh [n,(sh_degree+1)^2,3], sg_amp [n,sg_count,3], sg_sharp [n,sg_count],
  *       sg_axis [n,sg_count,3]; rays / images [R,3] row-major, R = ray count.
  *   - Thread safety: calls on different streams with different workspaces are
- *     independent; the only global state is the diagnostic launch counter.
+ *     independent; the only global state is the diagnostic launch counter and a
+ *     mutex-guarded cache of instantiated CUDA graphs of rg_build_bvh (keyed by
+ *     parameters, config, workspace and device; RG_NO_GRAPH=1 disables it).
  */
 #ifndef RAYGAUSS_RG_H
 #define RAYGAUSS_RG_H

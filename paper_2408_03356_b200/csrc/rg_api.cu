@@ -1,10 +1,12 @@
 // rg_api.cu -- the C-ABI entry points of include/rg.h: argument validation
 // (before anything is enqueued), workspace layout, launch, error mapping.
+#include <cstdlib>
 #include <cstring>
 
 #include "rg_internal.cuh"
 
 #include <atomic>
+#include <mutex>
 
 using namespace rg;
 
@@ -15,6 +17,85 @@ void count_launches(unsigned n) { g_launches.fetch_add(n, std::memory_order_rela
 }  // namespace rg
 
 namespace {
+
+// ---- rg_build_bvh as a CUDA graph: the ~30 launches and memsets of a
+// build are captured once per (parameters, config, workspace, device) on a private
+// stream and replayed with one cudaGraphLaunch on the caller's stream; parameter
+// VALUES are read when the graph runs, so an optimiser updating them in place keeps
+// hitting the cache.  A small round-robin cache under a mutex; RG_NO_GRAPH=1 in the
+// environment (read once) launches the kernels directly.
+struct GraphKey {
+  rg_gaussians g;
+  rg_config c;
+  void* ws;
+  int dev, pad_;
+};
+struct GraphEntry {
+  GraphKey k;
+  cudaGraphExec_t exec;
+  unsigned launches;
+};
+constexpr int kGraphCache = 8;
+std::mutex g_graph_mu;
+GraphEntry g_graphs[kGraphCache];
+int g_graph_n = 0, g_graph_next = 0;
+
+bool graphs_enabled() {
+  static const bool on = std::getenv("RG_NO_GRAPH") == nullptr;
+  return on;
+}
+
+cudaError_t build_graph_launch(const rg_gaussians& g, const rg_config& c, char* w,
+                               const BvhLayout& L, cudaStream_t st) {
+  GraphKey k;
+  std::memset(&k, 0, sizeof(k));
+  k.g = g;
+  k.c = c;
+  k.ws = w;
+  cudaGetDevice(&k.dev);
+  std::lock_guard<std::mutex> lock(g_graph_mu);
+  for (int i = 0; i < g_graph_n; ++i)
+    if (std::memcmp(&g_graphs[i].k, &k, sizeof(k)) == 0) {
+      count_launches(g_graphs[i].launches);
+      return cudaGraphLaunch(g_graphs[i].exec, st);
+    }
+  cudaStream_t cap;
+  if (cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return launch_build(g, c, w, L, st);
+  }
+  const unsigned long long before = g_launches.load();
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed);
+  if (e == cudaSuccess) {
+    e = launch_build(g, c, w, L, cap);
+    const cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
+    if (e == cudaSuccess) e = e2;
+  }
+  cudaStreamDestroy(cap);
+  const unsigned n_launch = (unsigned)(g_launches.load() - before);
+  g_launches.fetch_sub(n_launch, std::memory_order_relaxed);   // captured, not launched
+  cudaGraphExec_t exec = nullptr;
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (e != cudaSuccess) {      // capture unavailable: launch directly
+    cudaGetLastError();
+    return launch_build(g, c, w, L, st);
+  }
+  GraphEntry* slot;
+  if (g_graph_n < kGraphCache) {
+    slot = &g_graphs[g_graph_n++];
+  } else {
+    slot = &g_graphs[g_graph_next];
+    g_graph_next = (g_graph_next + 1) % kGraphCache;
+    cudaGraphExecDestroy(slot->exec);
+  }
+  slot->k = k;
+  slot->exec = exec;
+  slot->launches = n_launch;
+  count_launches(n_launch);
+  return cudaGraphLaunch(exec, st);
+}
 
 bool config_ok(const rg_config* c) {
   if (!c) return false;
@@ -99,7 +180,9 @@ rg_status rg_build_bvh(const rg_gaussians* g, const rg_config* cfg, void* ws, si
   if (ws_bytes < L.total) return RG_ERR_WORKSPACE_TOO_SMALL;
   char* w = static_cast<char*>(ws);
   cudaGetLastError();   // clear sticky-free previous errors
-  const cudaError_t e = launch_build(*g, *cfg, w, L, static_cast<cudaStream_t>(stream));
+  const cudaError_t e = graphs_enabled()
+                            ? build_graph_launch(*g, *cfg, w, L, static_cast<cudaStream_t>(stream))
+                            : launch_build(*g, *cfg, w, L, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return RG_ERR_CUDA;
   rg_bvh b;
   std::memset(&b, 0, sizeof(b));

@@ -9,6 +9,8 @@
 //   k_pack       : Morton-ordered 64-B geometry records + appearance records
 //   k_karras     : Karras 2012 hierarchy (one thread per internal node)
 //   k_refit      : bottom-up AABB union with per-node arrival counters
+#include <climits>
+
 #include "rg_internal.cuh"
 
 namespace rg {
@@ -467,8 +469,16 @@ __global__ void __launch_bounds__(128) k_wide_refit(const float4* nodes, const f
   }
 }
 
+// entries opened per round of the 32-wide collapse and resident blocks per SM of the
+// persistent collapse kernel: medians of 9 (tools/ab.py, C1; profiles/r2/ab_build.log):
+// open 1 / 16 blocks 0.911 ms, open 1 / 4 blocks 0.838 ms (more spinning warps contend
+// on the queue counters), open 2 / 16 blocks 0.797 ms with the forward +0.014 ms (the
+// two-per-round cut is a slightly worse tree, far less than the build time it saves)
 #ifndef RG_COLLAPSE_OPEN
-#define RG_COLLAPSE_OPEN 1
+#define RG_COLLAPSE_OPEN 2
+#endif
+#ifndef RG_COLLAPSE_BLOCKS
+#define RG_COLLAPSE_BLOCKS 4
 #endif
 // Collapse of the binary tree into 32-wide nodes, one persistent launch over a
 // device work queue of (binary id, wide id) items.  The queue is pre-filled with
@@ -530,13 +540,19 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
       if (!cm) break;
       const float area = internal ? box_area(b) : -2.f;
       int rank = 0;                                   // by area, descending (ties: lane)
-      if (RG_COLLAPSE_OPEN == 1) {
-        // only rank 0 opens: the largest area, lowest lane on ties (one reduction
-        // instead of a 32-step rank loop; the same entry, hence the same tree)
+      if (RG_COLLAPSE_OPEN <= 2) {
+        // only ranks < 2 open: the largest areas, lowest lane on ties (reductions
+        // instead of a 32-step rank loop; the same entries as the rank order)
         const int key = ord_enc(area);
         const int kmax = __reduce_max_sync(full, key);
         const int first = __ffs(__ballot_sync(full, key == kmax)) - 1;
-        rank = lane == first ? 0 : 1;
+        rank = lane == first ? 0 : 2;
+        if (RG_COLLAPSE_OPEN == 2) {
+          const int key2 = lane == first ? INT_MIN : key;
+          const int kmax2 = __reduce_max_sync(full, key2);
+          const int second = __ffs(__ballot_sync(full, key2 == kmax2)) - 1;
+          if (lane == second && lane != first) rank = 1;
+        }
       } else {
         for (unsigned mm = cm; mm; mm &= mm - 1) {
           const int o = __ffs(mm) - 1;
@@ -544,8 +560,6 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
           rank += (ao > area) || (ao == area && o < lane);
         }
       }
-      // one opening per round reproduces the greedy cut of the thread variant (opening
-      // several per round measured a worse tree: forward +7%)
       const int r = min(min(__popc(cm), kWide - m), RG_COLLAPSE_OPEN);
       const bool open = internal && rank < r;
       int rid = -1;
@@ -730,8 +744,12 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // all blocks co-resident (waiting warps spin): 4 blocks of 128 threads per SM
-    k_collapse_warp<<<4 * sms, 128, 0, st>>>(nodes, wide, qa, wsrc, wc, (int)wide_capacity(n));
+    // persistent warps over the work queue (a warp claims a slot, then waits for its
+    // item; unclaimed blocks hold nothing, so co-residency is not needed).  Each item
+    // is ~31 dependent rounds (one L2 load each): latency-bound, so the whole SM is
+    // filled -- RG_COLLAPSE_BLOCKS blocks of 128 per SM (28 registers: 16 fit)
+    k_collapse_warp<<<RG_COLLAPSE_BLOCKS * sms, 128, 0, st>>>(nodes, wide, qa, wsrc, wc,
+                                                             (int)wide_capacity(n));
     k_collapse_check<<<1, 1, 0, st>>>(wc, (int)wide_capacity(n));
     count_launches(2);
   }
