@@ -38,6 +38,9 @@ namespace {
 #ifndef RG_EVAL_UNROLL
 #define RG_EVAL_UNROLL 4         // forward window evaluation loop (sweep: 1 +2%, 2 +0.8%)
 #endif
+#ifndef RG_SG_HALF_ITEMS
+#define RG_SG_HALF_ITEMS 0       // backward SG scatter items: 0 = (pair, lobe), 1 = (pair, lobe, half)
+#endif
 #ifndef RG_MEMBER_UNROLL
 #define RG_MEMBER_UNROLL 2       // backward member loop
 #endif
@@ -285,15 +288,29 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
     if (!cmask) return;
     uint32_t cpos;
     const int ncand = __popc(cmask);
-    // sort the candidates by rank (O(#candidates)): place, then read back in order
+    // sort the candidates by rank (O(#candidates)): place, then read back in order;
+    // when their t_entry keys are distinct (the common case) the 32-bit high halves
+    // decide every comparison (one shuffle per step instead of two)
     {
       int crank = 0;
       unsigned mm = cmask;
-      while (mm) {
-        const int b = __ffs(mm) - 1;
-        mm &= mm - 1;
-        const unsigned long long kb = shfl64(ck, b);
-        crank += (cand && kb < ck) ? 1 : 0;
+      const uint32_t hi = (uint32_t)(ck >> 32);
+      const unsigned same = __match_any_sync(kFull, cand ? hi : 0xFFFFFFFFu);
+      const bool distinct = __all_sync(kFull, !cand || __popc(same) == 1);
+      if (distinct) {
+        while (mm) {
+          const int b = __ffs(mm) - 1;
+          mm &= mm - 1;
+          const uint32_t hb = __shfl_sync(kFull, hi, b);   // every lane shuffles
+          crank += (cand && hb < hi) ? 1 : 0;
+        }
+      } else {
+        while (mm) {
+          const int b = __ffs(mm) - 1;
+          mm &= mm - 1;
+          const unsigned long long kb = shfl64(ck, b);
+          crank += (cand && kb < ck) ? 1 : 0;
+        }
       }
       RG_CHECK(!cand || crank < 32);
       if (cand) { kscr[crank] = ck; pscr[crank] = cp; }
@@ -1034,8 +1051,9 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, c
     atomicAdd(row + 1, make_float4(s00, s01, s02, s11));
     atomicAdd(row + 2, make_float4(s12, s22, 0.f, 0.f));
   }
-  // SG lobes: lane = (pair, lobe, half) item, so several pairs' record loads are in
-  // flight per instruction (the per-pair loop below waits on one pair at a time)
+#if RG_SG_HALF_ITEMS
+  // SG lobes: lane = (pair, lobe, half) item (RG_SG_HALF_ITEMS=1): every half
+  // re-evaluates its lobe, twice the items of the per-lobe form
   if (S.lobes > 0) {
     const int per = 2 * S.lobes;
     const float inv_per = 1.0f / (float)per;
@@ -1068,6 +1086,39 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, c
       }
     }
   }
+#else
+  // SG lobes: lane = (pair, lobe) item, so several pairs' record loads are in flight
+  // per instruction (the per-pair loop below waits on one pair at a time); the item
+  // evaluates its lobe once and issues both halves (k, lambda | p) of its gradient
+  if (S.lobes > 0) {
+    const int per = S.lobes;
+    const float inv_per = 1.0f / (float)per;
+    const int nitems = (32 - __clz(mask)) * per;
+    const int c0 = 3 * qsh;                           // first SG chunk of the row
+    for (int it = (int)lane; it - (int)lane < nitems; it += 32) {
+      int b = (int)((float)it * inv_per);             // it / per (small ints), corrected
+      if (b * per > it) --b;
+      if ((b + 1) * per <= it) ++b;
+      const int c = it - b * per;
+      if (it < nitems && ((mask >> b) & 1u)) {
+        const int e = base + b;
+        const float4 acc = A.a[e];
+        const float2 acb = A.b[e];
+        const float d0 = acc.w, d1 = acb.x, d2 = acb.y;
+        const int pos = __float_as_int(M.e2[e].y);
+        const float* q = S.app + (size_t)pos * S.app_stride + kShFloats + 7 * c;
+        const float lam = __ldg(q + 3);
+        const float dpm = R.d.x * __ldg(q + 4) + R.d.y * __ldg(q + 5) + R.d.z * __ldg(q + 6) - 1.0f;
+        const float ej = ex2_approx(lam * dpm * kLog2e);
+        const float kd = (d0 * __ldg(q) + d1 * __ldg(q + 1) + d2 * __ldg(q + 2)) * ej;
+        const float kdl = kd * lam;
+        float4* dst = reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + c0 + 2 * c;
+        atomicAdd(dst, make_float4(d0 * ej, d1 * ej, d2 * ej, kd * dpm));
+        atomicAdd(dst + 1, make_float4(kdl * R.d.x, kdl * R.d.y, kdl * R.d.z, 0.f));
+      }
+    }
+  }
+#endif
   // SH: one coalesced burst per pair, lane = (channel, 4 coefficients):
   // dL/dc~_m = dc[ch] Y_m(d), Y(d) from shared memory (zero past the degree)
   const int ch = (int)lane < 3 * qsh ? (int)lane / qsh : -1;
@@ -1142,6 +1193,15 @@ __device__ __forceinline__ int held_le(const WM& M, int count, float x) {
     const unsigned m1 =
         __ballot_sync(kFull, (int)lane_id() + 32 < count && M.e0[lane_id() + 32].x <= x);
     return __popc(m0) + __popc(m1);
+  } else if constexpr (KA <= 128) {
+    // independent chunk ballots (a binary search is a chain of dependent loads)
+    int n = 0;
+#pragma unroll
+    for (int h = 0; h < KA / 32; ++h) {
+      const int e = 32 * h + (int)lane_id();
+      n += __popc(__ballot_sync(kFull, e < count && M.e0[e].x <= x));
+    }
+    return n;
   } else {
     int lo = 0, len = count;      // warp-uniform binary search (broadcast loads)
     while (len > 0) {
@@ -1382,7 +1442,11 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
       const bool win = (GW == 8) && (B == 8);
       const float thr = win ? fminf(t1, fma_((float)(k0 + 4 * B), c.dt, t0)) : thi;
       // ---- refill in key order until every Gaussian entering by thr is held
-      while (!exhausted && count < KA && (count == 0 || M.e0[count - 1].x <= thr)) {
+      // (large list: when more than K held entries already enter by t_hi, the slab's
+      // truncated set -- the K smallest keys -- and its overflow are decided without
+      // a query; refills wait until fewer remain, so they come in larger batches)
+      while (!exhausted && count < KA && (count == 0 || M.e0[count - 1].x <= thr) &&
+             !(KA == kABig && held_le<KA>(M, count, thi) > K)) {
         const int want = min(32, KA - count);
         unsigned long long key = 0;
         uint32_t pos = 0;
