@@ -38,6 +38,12 @@ namespace {
 #ifndef RG_EVAL_UNROLL
 #define RG_EVAL_UNROLL 4         // forward window evaluation loop (sweep: 1 +2%, 2 +0.8%)
 #endif
+#ifndef RG_P2_MIN
+#define RG_P2_MIN 8              // backward window pass: smallest member group (4 or 8 lanes)
+#endif
+#ifndef RG_SH_ONE_PAIR
+#define RG_SH_ONE_PAIR 0         // backward SH scatter: 0 = two pairs per iteration (half-warps)
+#endif
 #ifndef RG_SG_HALF_ITEMS
 #define RG_SG_HALF_ITEMS 0       // backward SG scatter items: 0 = (pair, lobe), 1 = (pair, lobe, half)
 #endif
@@ -1108,7 +1114,10 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, c
   }
 #endif
   // SH: one coalesced burst per pair, lane = (channel, 4 coefficients):
-  // dL/dc~_m = dc[ch] Y_m(d), Y(d) from shared memory (zero past the degree)
+  // dL/dc~_m = dc[ch] Y_m(d), Y(d) from shared memory (zero past the degree).
+  // A burst is 3 * pad4(nc) / 4 <= 12 lanes, so each half-warp takes a pair
+  // (RG_SH_ONE_PAIR=1: one pair per iteration, 20 lanes idle)
+#if RG_SH_ONE_PAIR
   const int ch = (int)lane < 3 * qsh ? (int)lane / qsh : -1;
   float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
   if (ch >= 0) y = *reinterpret_cast<const float4*>(&M.Y[4 * ((int)lane - ch * qsh)]);
@@ -1123,6 +1132,27 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, c
                 make_float4(dsel * y.x, dsel * y.y, dsel * y.z, dsel * y.w));
     }
   }
+#else
+  const int l16 = (int)lane & 15;
+  const bool upper = lane >= 16u;
+  const int ch = l16 < 3 * qsh ? l16 / qsh : -1;
+  float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (ch >= 0) y = *reinterpret_cast<const float4*>(&M.Y[4 * (l16 - ch * qsh)]);
+  while (mask) {
+    const int b0 = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const int b1 = mask ? __ffs(mask) - 1 : -1;
+    if (b1 >= 0) mask &= mask - 1;
+    const int b = upper ? b1 : b0;
+    if (b >= 0 && ch >= 0) {
+      const int e = base + b;
+      const int pos = __float_as_int(M.e2[e].y);
+      const float dsel = ch == 0 ? A.a[e].w : (ch == 1 ? A.b[e].x : A.b[e].y);
+      atomicAdd(reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride) + 4 + l16,
+                make_float4(dsel * y.x, dsel * y.y, dsel * y.z, dsel * y.w));
+    }
+  }
+#endif
 }
 
 __device__ __forceinline__ int skip_to(float te, int s, int B, float dt, float t0, float t1) {
@@ -1615,7 +1645,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
             __syncwarp();
             // lane = (member, part): P2 members per pass, each member's window samples
             // split into 32/P2 parts of P2 samples; parts reduced by xor shuffles
-            const int P2 = n3 <= 8 ? 8 : (n3 <= 16 ? 16 : 32);
+            const int P2 = (RG_P2_MIN <= 4 && n3 <= 4) ? 4 : (n3 <= 8 ? 8 : (n3 <= 16 ? 16 : 32));
             for (int base = 0; base < n3; base += P2) {
               const int e = base + ((int)lane & (P2 - 1));
               const int part0 = (int)lane & ~(P2 - 1);   // first sample of this lane's part
