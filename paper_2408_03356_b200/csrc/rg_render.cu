@@ -39,7 +39,7 @@ namespace {
 #define RG_EVAL_UNROLL 4         // forward window evaluation loop (sweep: 1 +2%, 2 +0.8%)
 #endif
 #ifndef RG_P2_MIN
-#define RG_P2_MIN 8              // backward window pass: smallest member group (4 or 8 lanes)
+#define RG_P2_MIN 4              // backward window pass: smallest member group (4 or 8 lanes)
 #endif
 #ifndef RG_SH_ONE_PAIR
 #define RG_SH_ONE_PAIR 0         // backward SH scatter: 0 = two pairs per iteration (half-warps)
