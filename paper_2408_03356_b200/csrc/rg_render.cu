@@ -38,6 +38,15 @@ namespace {
 #ifndef RG_EVAL_UNROLL
 #define RG_EVAL_UNROLL 4         // forward window evaluation loop (sweep: 1 +2%, 2 +0.8%)
 #endif
+#ifndef RG_EVAL_BRANCHFREE
+#define RG_EVAL_BRANCHFREE 1     // window evaluation predicated, not branched (medians of 9:
+#endif                           // forward 7.243 -> 6.797 ms; profiles/r2/ab_eval_branchfree.log)
+#ifndef RG_GRAD_BRANCHFREE
+#define RG_GRAD_BRANCHFREE 1     // backward member loop predicated (medians of 9: backward
+#endif                           // 5.558 -> 5.025 ms; profiles/r2/ab_grad_branchfree.log)
+#ifndef RG_RANGE_BRANCHFREE
+#define RG_RANGE_BRANCHFREE 1    // per-slab-path evaluation (eval_range) predicated
+#endif
 #ifndef RG_P2_MIN
 #define RG_P2_MIN 4              // backward window pass: smallest member group (4 or 8 lanes)
 #endif
@@ -899,10 +908,10 @@ __device__ RG_SETUP_ATTR void setup_pair(const SceneView& S, WM& M, int sl, cons
   }
 }
 
-// 1 - exp(-x) without cancellation for small x
+// 1 - exp(-x) without cancellation for small x (both forms, then a select: no branch)
 __device__ __forceinline__ float alpha_of(float x, float e) {
-  if (x < 0.0625f) return x * (1.f - 0.5f * x * (1.f - (1.f / 3.f) * x * (1.f - 0.25f * x)));
-  return 1.0f - e;
+  const float ser = x * (1.f - 0.5f * x * (1.f - (1.f / 3.f) * x * (1.f - 0.25f * x)));
+  return x < 0.0625f ? ser : 1.0f - e;
 }
 
 // lane -> (entry subset esub, sample j) for one group of GW samples
@@ -918,6 +927,27 @@ __device__ __forceinline__ void eval_range(const WM& M, int e0, int e1, const La
                                            float tk, bool val, float& s, float& r, float& g,
                                            float& b, uint32_t& evals) {
   float2 rg2 = make_float2(r, g);
+#if RG_RANGE_BRANCHFREE
+  if (BASIS == 0) {
+#pragma unroll 2
+    for (int e = e0 + L.esub; e < e1; e += Lanes<GW>::ER) {
+      const float4 a = M.e0[e];
+      const float4 q = M.e1[e];
+      const float cb = M.e2[e].x;
+      const float tau = tk - a.z;
+      const float wv = ex2_approx(fmaf(tau, fmaf(q.y, tau, q.x), a.w));
+      const bool in = val && a.x <= tk && tk <= a.y;
+      const float w = in ? wv : 0.f;
+      s += w;
+      rg2 = __ffma2_rn(make_float2(w, w), make_float2(q.z, q.w), rg2);
+      b = fmaf(w, cb, b);
+      evals += in ? 1u : 0u;
+    }
+    r = rg2.x;
+    g = rg2.y;
+    return;
+  }
+#endif
 #pragma unroll 2
   for (int e = e0 + L.esub; e < e1; e += Lanes<GW>::ER) {
     const float4 a = M.e0[e];
@@ -1529,6 +1559,25 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
             ++wcur;
           }
           float2 srg = make_float2(sr, sgg);   // (r, g) sums: one packed FFMA2 per member
+#if RG_EVAL_BRANCHFREE
+          // predicated form: every lane evaluates, the exact interval test (L2) selects
+          if (BASIS == 0) {
+#pragma unroll kEvalUnroll
+            for (int e = 0; e < (stored ? 0 : n3); ++e) {
+              const float4 a = M.e0[e];
+              const float4 q = M.e1[e];
+              const float cbv = M.e2[e].x;
+              const float tau_ = tk - a.z;
+              const float wv = ex2_approx(fmaf(tau_, fmaf(q.y, tau_, q.x), a.w));
+              const bool in = val && a.x <= tk && tk <= a.y;
+              const float w = in ? wv : 0.f;
+              sg += w;
+              srg = __ffma2_rn(make_float2(w, w), make_float2(q.z, q.w), srg);
+              sb = fmaf(w, cbv, sb);
+              ev += in ? 1u : 0u;
+            }
+          } else
+#endif
 #pragma unroll kEvalUnroll
           for (int e = 0; e < (stored ? 0 : n3); ++e) {
             const float4 a = M.e0[e];
@@ -1664,6 +1713,26 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
                 int kh = (int)ceilf((a.y - t0) * inv_dt - kf) + 1;
                 kl = max(kl, part0);
                 kh = min(kh, min(last, part0 + P2 - 1));
+#if RG_GRAD_BRANCHFREE
+                if (BASIS == 0) {
+#pragma unroll kMemberUnroll
+                  for (int k = kl; k <= kh; ++k) {
+                    const float4 s0 = A.s0[k];
+                    const float tkk = s0.x;
+                    const float b2 = A.s1[k];
+                    const float tau_ = tkk - a.z;
+                    const float wv = ex2_approx(fmaf(tau_, fmaf(q.y, tau_, q.x), a.w));
+                    const float w = (a.x <= tkk && tkk <= a.y) ? wv : 0.f;
+                    const float dldw = fmaf(s0.z, q.z, fmaf(s0.w, q.w, fmaf(b2, cbv, s0.y)));
+                    const float wd = w * dldw;
+                    a0 += wd;
+                    a1 = fmaf(wd, tau_, a1);
+                    a2 = fmaf(wd * tau_, tau_, a2);
+                    a34 = __ffma2_rn(make_float2(w, w), make_float2(s0.z, s0.w), a34);
+                    a5 = fmaf(w, b2, a5);
+                  }
+                } else
+#endif
 #pragma unroll kMemberUnroll
                 for (int k = kl; k <= kh; ++k) {
                   const float4 s0 = A.s0[k];
