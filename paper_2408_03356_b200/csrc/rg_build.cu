@@ -315,16 +315,25 @@ __global__ void __launch_bounds__(kThreads) k_pack_app(rg_gaussians g, const uin
        p += (gridDim.x * blockDim.x) >> 5) {
     const size_t i = order[p];
     float* ap = app + (size_t)p * stride;
-    for (int f = lane; f < stride; f += 32) {
-      float v = 0.0f;
+    // <= 100 floats per row: up to 4 per lane, all loads issued before the stores
+    constexpr int kPer = (kShFloats + 7 * kMaxLobes + 3 + 31) / 32;
+    float v[kPer];
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int f = lane + 32 * t;
+      v[t] = 0.0f;
       if (f < nc3) {
-        v = g.sh[i * nc3 + f];
+        v[t] = g.sh[i * nc3 + f];
       } else if (f >= kShFloats && f < kShFloats + 7 * G) {
         const int j = (f - kShFloats) / 7, r = (f - kShFloats) - 7 * j;
         const size_t ij = i * G + j;
-        v = r < 3 ? g.sg_amp[3 * ij + r] : (r == 3 ? g.sg_sharp[ij] : g.sg_axis[3 * ij + r - 4]);
+        v[t] = r < 3 ? g.sg_amp[3 * ij + r] : (r == 3 ? g.sg_sharp[ij] : g.sg_axis[3 * ij + r - 4]);
       }
-      ap[f] = v;
+    }
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int f = lane + 32 * t;
+      if (f < stride) ap[f] = v[t];
     }
   }
 }

@@ -44,9 +44,13 @@ namespace {
 #ifndef RG_GRAD_BRANCHFREE
 #define RG_GRAD_BRANCHFREE 1     // backward member loop predicated (medians of 9: backward
 #endif                           // 5.558 -> 5.025 ms; profiles/r2/ab_grad_branchfree.log)
-#ifndef RG_RANGE_BRANCHFREE
-#define RG_RANGE_BRANCHFREE 1    // per-slab-path evaluation (eval_range) predicated
+#ifndef RG_TWO_UNCOND
+#define RG_TWO_UNCOND 0          // restart query: the second node's loads without a branch
 #endif
+#ifndef RG_RANGE_BRANCHFREE
+#define RG_RANGE_BRANCHFREE 1    // per-slab-path evaluation (eval_range) predicated in the
+#endif                           // backward (medians of 9: backward 5.18 -> 5.02 ms; the
+                                 // forward is faster branched, 6.93 vs 6.79 ms)
 #ifndef RG_P2_MIN
 #define RG_P2_MIN 4              // backward window pass: smallest member group (4 or 8 lanes)
 #endif
@@ -395,6 +399,14 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
     const int childA = __ldg(&WA.child[lane]);
     const float alx = __ldg(&WA.lox[lane]), aly = __ldg(&WA.loy[lane]), alz = __ldg(&WA.loz[lane]);
     const float ahx = __ldg(&WA.hix[lane]), ahy = __ldg(&WA.hiy[lane]), ahz = __ldg(&WA.hiz[lane]);
+#if RG_TWO_UNCOND
+    // node B loaded unconditionally (node A again when there is no second node: L1
+    // hits), its children masked: no branch around the loads
+    int childB = __ldg(&WB.child[lane]);
+    const float blx = __ldg(&WB.lox[lane]), bly = __ldg(&WB.loy[lane]), blz = __ldg(&WB.loz[lane]);
+    const float bhx = __ldg(&WB.hix[lane]), bhy = __ldg(&WB.hiy[lane]), bhz = __ldg(&WB.hiz[lane]);
+    if (!two) childB = kWideEmpty;
+#else
     int childB = kWideEmpty;
     float blx = 0.f, bly = 0.f, blz = 0.f, bhx = 0.f, bhy = 0.f, bhz = 0.f;
     if (two) {
@@ -402,6 +414,7 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       blx = __ldg(&WB.lox[lane]); bly = __ldg(&WB.loy[lane]); blz = __ldg(&WB.loz[lane]);
       bhx = __ldg(&WB.hix[lane]); bhy = __ldg(&WB.hiy[lane]); bhz = __ldg(&WB.hiz[lane]);
     }
+#endif
     float tnA, tfA, tnB, tfB;
     box_t(alx, aly, alz, ahx, ahy, ahz, R.inv, R.oinv, tnA, tfA);
     box_t(blx, bly, blz, bhx, bhy, bhz, R.inv, R.oinv, tnB, tfB);
@@ -922,13 +935,13 @@ struct Lanes {
 };
 
 // sigma and sigma*c at this lane's sample from slots [e0, e1)
-template <int GW, int BASIS, class WM>
+template <int GW, int BASIS, bool PRED, class WM>
 __device__ __forceinline__ void eval_range(const WM& M, int e0, int e1, const Lanes<GW>& L,
                                            float tk, bool val, float& s, float& r, float& g,
                                            float& b, uint32_t& evals) {
   float2 rg2 = make_float2(r, g);
 #if RG_RANGE_BRANCHFREE
-  if (BASIS == 0) {
+  if (BASIS == 0 && PRED) {
 #pragma unroll 2
     for (int e = e0 + L.esub; e < e1; e += Lanes<GW>::ER) {
       const float4 a = M.e0[e];
@@ -1809,7 +1822,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
         const bool val = (g0 + L.j < B) && (tk < t1);
         float sg = 0.f, sr = 0.f, sgg = 0.f, sb = 0.f;
         uint32_t ev = 0;
-        eval_range<GW, BASIS>(M, 0, n_use, L, tk, val, sg, sr, sgg, sb, ev);
+        eval_range<GW, BASIS, BWD>(M, 0, n_use, L, tk, val, sg, sr, sgg, sb, ev);
         if (more) {   // slab set larger than the active list: stream the rest
           unsigned long long cur2 = cursor;
           int remaining = K - n_use;
@@ -1822,7 +1835,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
             if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, KA + (int)lane, R, pos);
             __syncwarp();
             if (!BWD && log_ok) log_fetch(got, KA);
-            eval_range<GW, BASIS>(M, KA, KA + got, L, tk, val, sg, sr, sgg, sb, ev);
+            eval_range<GW, BASIS, BWD>(M, KA, KA + got, L, tk, val, sg, sr, sgg, sb, ev);
             if (dbg && g0 == 0) dbg_put(P, ray, dbg_n, s, got, M, KA);
             if (g0 == 0 && lane == 0) cnt.pairs += got;
             remaining -= got;
@@ -2046,21 +2059,35 @@ __global__ void __launch_bounds__(256) k_finalize_app(const float* gbuf, int gst
        p += (gridDim.x * blockDim.x) >> 5) {
     const size_t i = order[p];
     const float* ap = gbuf + (size_t)p * gstride + 16;
-    for (int f = lane; f < nc3 + 7 * G; f += 32) {
+    // <= 97 values per row: up to 4 per lane, every load issued before the first use
+    // (the per-element read-modify-write chain was latency-bound)
+    constexpr int kPer = (3 * 16 + 7 * 7 + 31) / 32;
+    float v[kPer], o[kPer];
+    float* dst[kPer];
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int f = lane + 32 * t;
+      dst[t] = nullptr;
+      v[t] = 0.f;
       if (f < nc3) {
         const int m = f / 3, ch = f - 3 * m;
-        const float v = ap[ch * ncp + m];
-        bad += !isfinite(v);
-        if (out.sh) out.sh[i * nc3 + f] += v;
-      } else {
+        v[t] = ap[ch * ncp + m];
+        if (out.sh) dst[t] = out.sh + i * nc3 + f;
+      } else if (f < nc3 + 7 * G) {
         const int j = (f - nc3) / 7, r = (f - nc3) - 7 * j;
-        const float v = ap[3 * ncp + 8 * j + r];
-        bad += !isfinite(v);
+        v[t] = ap[3 * ncp + 8 * j + r];
         const size_t ij = i * G + j;
-        if (r < 3) { if (out.sg_amp) out.sg_amp[3 * ij + r] += v; }
-        else if (r == 3) { if (out.sg_sharp) out.sg_sharp[ij] += v; }
-        else if (out.sg_axis) out.sg_axis[3 * ij + r - 4] += v;
+        if (r < 3) dst[t] = out.sg_amp ? out.sg_amp + 3 * ij + r : nullptr;
+        else if (r == 3) dst[t] = out.sg_sharp ? out.sg_sharp + ij : nullptr;
+        else dst[t] = out.sg_axis ? out.sg_axis + 3 * ij + r - 4 : nullptr;
       }
+    }
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) o[t] = dst[t] ? *dst[t] : 0.f;
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      bad += !isfinite(v[t]);
+      if (dst[t]) *dst[t] = o[t] + v[t];
     }
   }
   bad = __reduce_add_sync(0xffffffffu, bad);
