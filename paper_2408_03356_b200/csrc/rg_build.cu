@@ -489,6 +489,9 @@ __global__ void __launch_bounds__(128) k_wide_refit(const float4* nodes, const f
 #ifndef RG_COLLAPSE_BLOCKS
 #define RG_COLLAPSE_BLOCKS 4
 #endif
+#ifndef RG_COLLAPSE_PREFETCH
+#define RG_COLLAPSE_PREFETCH 1   // prefetch each entry's binary record when it is placed
+#endif
 // Collapse of the binary tree into 32-wide nodes, one persistent launch over a
 // device work queue of (binary id, wide id) items.  The queue is pre-filled with
 // -1; an item is written with one 8-byte store after its slot is reserved.  A
@@ -542,6 +545,23 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
       id = lane == 0 ? c.x : c.y;
       for (int k = 0; k < 6; ++k) b[k] = w[6 * lane + k];
     }
+#if RG_COLLAPSE_PREFETCH
+    // each lane prefetches the binary record (child ids and boxes) of its entry as
+    // soon as it holds it, so opening an entry no longer waits on a dependent load
+    int2 pc = make_int2(-1, -1);
+    float pw[12];
+    auto prefetch = [&]() {
+      if (id >= 0) {
+        const float4* nd = nodes + 4 * (size_t)id;
+        const float4 n0 = nd[0], n1 = nd[1], n2 = nd[2], n3 = nd[3];
+        pw[0] = n0.x; pw[1] = n0.y; pw[2] = n0.z; pw[3] = n0.w;
+        pw[4] = n1.x; pw[5] = n1.y; pw[6] = n1.z; pw[7] = n1.w;
+        pw[8] = n2.x; pw[9] = n2.y; pw[10] = n2.z; pw[11] = n2.w;
+        pc = make_int2(__float_as_int(n3.x), __float_as_int(n3.y));
+      }
+    };
+    prefetch();
+#endif
     int m = 2;
     while (m < kWide) {
       const bool internal = lane < m && id >= 0;
@@ -574,13 +594,19 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
       int rid = -1;
       float rb[6];
       if (open) {                                     // left child in place, right one out
+#if RG_COLLAPSE_PREFETCH
+        id = pc.x;
+        rid = pc.y;
+        for (int k = 0; k < 6; ++k) { b[k] = pw[k]; rb[k] = pw[6 + k]; }
+#else
         const float* w = reinterpret_cast<const float*>(nodes + 4 * (size_t)id);
         const int4 c = *reinterpret_cast<const int4*>(nodes + 4 * (size_t)id + 3);
         id = c.x;
         rid = c.y;
         for (int k = 0; k < 6; ++k) { b[k] = w[k]; rb[k] = w[6 + k]; }
+#endif
       }
-      const unsigned om = __ballot_sync(full, open);
+      bool fresh = open;
       for (int j = 0; j < r; ++j) {                   // right child of rank j -> lane m + j
         const int src = __ffs(__ballot_sync(full, open && rank == j)) - 1;
         const int vid = __shfl_sync(full, rid, src);
@@ -589,9 +615,14 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
         if (lane == m + j) {
           id = vid;
           for (int k = 0; k < 6; ++k) b[k] = vb[k];
+          fresh = true;
         }
       }
-      (void)om;
+#if RG_COLLAPSE_PREFETCH
+      if (fresh) prefetch();
+#else
+      (void)fresh;
+#endif
       m += r;
     }
     // write the wide node; internal children become queue items

@@ -1634,7 +1634,8 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
           const float Tb = ex2_approx(-(tau + (incl - x)) * kLog2e);
           const float e_s = ex2_approx(-x * kLog2e);
           const float al = alpha_of(x, e_s);
-          const float inv_s = live0 ? 1.0f / sg : 0.f;
+          // value path (never a decision): MUFU reciprocal, ~1 ulp, no IEEE-division slow path
+          const float inv_s = live0 ? __fdividef(1.0f, sg) : 0.f;
           const float cr = sr * inv_s, cg = sgg * inv_s, cb = sb * inv_s;
           const float wgt = live0 ? Tb * al : 0.f;
           float p0 = wgt * cr, p1 = wgt * cg, p2 = wgt * cb;
@@ -1871,7 +1872,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
         const float Tb = ex2_approx(-(tau + excl) * kLog2e);   // T before this sample
         const float e_s = ex2_approx(-x * kLog2e);
         const float al = alpha_of(x, e_s);
-        const float inv_s = live ? 1.0f / sg : 0.f;
+        const float inv_s = live ? __fdividef(1.0f, sg) : 0.f;
         const float cr = sr * inv_s, cg = sgg * inv_s, cb = sb * inv_s;
         const float wgt = live ? Tb * al : 0.f;
         float p0 = wgt * cr, p1 = wgt * cg, p2 = wgt * cb;
