@@ -1336,10 +1336,12 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
   int dbg_n = 0;
   float gr0 = 0.f, gr1 = 0.f, gr2 = 0.f, Pp0 = 0.f, Pp1 = 0.f, Pp2 = 0.f;
   int replay_in = -1;
+  int lg0 = -1;   // backward: the ray's log header, loaded with the other per-ray inputs
   if (BWD) {
     gr0 = P.d_rgb[3 * ray]; gr1 = P.d_rgb[3 * ray + 1]; gr2 = P.d_rgb[3 * ray + 2];
     Pp0 = P.rgb_in[3 * ray]; Pp1 = P.rgb_in[3 * ray + 1]; Pp2 = P.rgb_in[3 * ray + 2];
     replay_in = P.replay_in[ray];
+    if (P.log) lg0 = P.log[(size_t)ray * kLogWords];
   }
   float t0 = 0.f, t1 = 0.f;
   const bool hit = inside && P.S.n > 0 && clip_exact(P.S.root_box, R.o, R.d, c.t_near, t0, t1);
@@ -1370,13 +1372,13 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
     __syncwarp();
     int& lp = M.ls.lp;
     int& log_ok = M.ls.ok;
-    const bool replay_log = BWD && lg != nullptr && lg[0] >= 0;
+    const bool replay_log = BWD && lg != nullptr && lg0 >= 0;
     // stored windows (forward: count so far; backward: how many the forward stored)
     int& nwin = M.ls.nwin;
     int& wlog = M.ls.wl;
     int& wcur = M.ls.wcur;
     int& fix_used = M.ls.fix;   // forward: pair slots used in the ray's own block
-    nwin = BWD ? (replay_log ? (lg[0] >> 16) : 0) : 0;
+    nwin = BWD ? (replay_log ? (lg0 >> 16) : 0) : 0;
     wlog = !BWD && log_ok;
     if (lane == 0) M.sst.valid = false;   // forward: persistent traversal restarts on first use
     __syncwarp();
