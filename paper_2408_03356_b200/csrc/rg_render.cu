@@ -44,6 +44,9 @@ namespace {
 #ifndef RG_GRAD_BRANCHFREE
 #define RG_GRAD_BRANCHFREE 1     // backward member loop predicated (medians of 9: backward
 #endif                           // 5.558 -> 5.025 ms; profiles/r2/ab_grad_branchfree.log)
+#ifndef RG_STORE_WINDOWS
+#define RG_STORE_WINDOWS 1       // forward stores the 4-slab windows' sums for the backward
+#endif
 #ifndef RG_TWO_UNCOND
 #define RG_TWO_UNCOND 0          // restart query: the second node's loads without a branch
 #endif
@@ -1379,7 +1382,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2
     int& wcur = M.ls.wcur;
     int& fix_used = M.ls.fix;   // forward: pair slots used in the ray's own block
     nwin = BWD ? (replay_log ? (lg0 >> 16) : 0) : 0;
-    wlog = !BWD && log_ok;
+    wlog = !BWD && log_ok && RG_STORE_WINDOWS;
     if (lane == 0) M.sst.valid = false;   // forward: persistent traversal restarts on first use
     __syncwarp();
     int nref = 0;                         // forward refills of this ray so far
