@@ -44,6 +44,9 @@ namespace {
 #ifndef RG_GRAD_BRANCHFREE
 #define RG_GRAD_BRANCHFREE 1     // backward member loop predicated (medians of 9: backward
 #endif                           // 5.558 -> 5.025 ms; profiles/r2/ab_grad_branchfree.log)
+#ifndef RG_PREFETCH_APP
+#define RG_PREFETCH_APP 0        // restart query: prefetch candidates' appearance records (A/B)
+#endif
 #ifndef RG_STORE_WINDOWS
 #define RG_STORE_WINDOWS 1       // forward stores the 4-slab windows' sums for the backward
 #endif
@@ -70,7 +73,11 @@ namespace {
 #define RG_MIN_BLOCKS 4                // resident blocks per SM the register budget targets (bwd)
 #endif
 #ifndef RG_MIN_BLOCKS_FWD
-#define RG_MIN_BLOCKS_FWD RG_MIN_BLOCKS   // forward (no WarpAcc: smem allows more blocks)
+// forward, 64-slot list (no WarpAcc: smem allows more blocks): 5 blocks -> 96 registers,
+// 20 warps/SM; medians of 9 (profiles/r2/ab_fwd_blocks.log): C1 forward 6.76 -> 6.36 ms
+// with 5, 6.76 with 6 (80 registers, 144 B of spills); the 128-slot list keeps 4 (C3
+// forward 230 -> 251 ms with 5)
+#define RG_MIN_BLOCKS_FWD 5
 #endif
 constexpr int kEvalUnroll = RG_EVAL_UNROLL;
 constexpr int kMemberUnroll = RG_MEMBER_UNROLL;
@@ -296,6 +303,16 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
         ck = ((unsigned long long)fkey(pg.te) << 32) | (uint32_t)__float_as_int(g3.z);
         cand = ck > cursor && ck < kth;
         if (!cand) ck = ~0ull;
+#if RG_PREFETCH_APP
+        if (cand) {   // its appearance record is read by the set-up if it survives the query
+          const char* ap = reinterpret_cast<const char*>(S.app + (size_t)cp * S.app_stride);
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            if (RG_PREFETCH_APP == 2) asm volatile("prefetch.global.L1 [%0];" ::"l"(ap + 128 * l));
+            else asm volatile("prefetch.global.L2 [%0];" ::"l"(ap + 128 * l));
+          }
+        }
+#endif
       }
     }
     // drop the consumed queue entries
@@ -1279,7 +1296,9 @@ __device__ __forceinline__ int held_le(const WM& M, int count, float x) {
 // INSTR: counters (rg_stats) and the debug dump; the uninstrumented variant
 // compiles them out (8 fewer live registers through the march)
 template <bool BWD, int GW, bool INSTR, int BASIS, int KA = kA>
-__global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS : (KA == kABig ? 2 : RG_MIN_BLOCKS_FWD))
+__global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS
+                                               : (KA == kA ? RG_MIN_BLOCKS_FWD
+                                                           : (KA == kAMid ? RG_MIN_BLOCKS : 2)))
     k_render(const RenderArgs P) {
   static_assert(KA != kABig || !BWD, "the large-list variant is forward only");
   // dynamic shared memory: per-warp WarpMem (+ WarpAcc in the backward) at fixed
