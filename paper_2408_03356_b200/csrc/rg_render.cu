@@ -99,7 +99,7 @@ static_assert(kA == 64, "expire/n_in handle two 32-slot chunks");
 // backward traverses only for rays whose fetch log overflowed and must stay within
 // its 48 KB block budget
 constexpr int kStkFwd = RG_STK_FWD;
-constexpr int kStkBwd = 192;
+constexpr int kStkBwd = 168;   // 5 Gaussian backward blocks per SM fit (static_assert below)
 constexpr unsigned kFull = 0xffffffffu;
 
 struct Counters {
@@ -211,11 +211,12 @@ using WMBig = WarpMemT<320, 1, 32, kABig, kABig + 32>;
 constexpr int kAMid = 128;
 using WMMid = WarpMemT<kStkFwd, 1, 32, kAMid, kAMid + 64>;
 using WMBwdMid = WarpMemT<kStkBwd, 1, 1, kAMid, kAMid + 64>;
-template <int SLOTS>
+template <int SLOTS, bool HASC = true>
 struct WarpAccT {
   float4 a[SLOTS];     // Sw, Sw1, Sw2, dc_r
   float2 b[SLOTS];     // dc_g, dc_b
-  float c[SLOTS];      // sum w dL/dw (dL/dsigma~ of non-Gaussian bases; = a.x for the Gaussian)
+  float c[HASC ? SLOTS : 1];   // sum w dL/dw (dL/dsigma~ of non-Gaussian bases; the
+                               // Gaussian's is a.x, so its kernels do not allocate it)
   float4 s0[32];
   float s1[32];        // per-sample backward values of the current group / window:
                           // {tk, dls, dc0, dc1}, {dc2, gc, inv, live}
@@ -1070,7 +1071,7 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, c
       const float4 v = A.a[base + lane];
       const float2 w = A.b[base + lane];
       nz = v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f || w.x != 0.f || w.y != 0.f ||
-           (BASIS != 0 && A.c[base + lane] != 0.f);
+           (BASIS != 0 && A.c[BASIS != 0 ? base + lane : 0] != 0.f);
     }
     mask = __ballot_sync(kFull, nz);
   }
@@ -1104,7 +1105,7 @@ __device__ RG_SCATTER_ATTR void scatter_batch(const SceneView& S, const WM& M, c
     const float s22 = fmaf(xp[2], v2, dv[2] * h2);
     RG_CHECK(pos >= 0 && pos < S.n);
     float4* row = reinterpret_cast<float4*>(gbuf + (size_t)pos * gstride);
-    atomicAdd(row + 0, make_float4(v0, v1, v2, (BASIS == 0 ? Sw : A.c[e]) / g0.w));
+    atomicAdd(row + 0, make_float4(v0, v1, v2, (BASIS == 0 ? Sw : A.c[BASIS != 0 ? e : 0]) / g0.w));
     atomicAdd(row + 1, make_float4(s00, s01, s02, s11));
     atomicAdd(row + 2, make_float4(s12, s22, 0.f, 0.f));
   }
@@ -1298,7 +1299,7 @@ __device__ __forceinline__ int held_le(const WM& M, int count, float x) {
 template <bool BWD, int GW, bool INSTR, int BASIS, int KA = kA>
 __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS
                                                : (KA == kA ? RG_MIN_BLOCKS_FWD
-                                                           : (KA == kAMid ? RG_MIN_BLOCKS : 2)))
+                                                           : (KA == kAMid ? 4 : 2)))
     k_render(const RenderArgs P) {
   static_assert(KA != kABig || !BWD, "the large-list variant is forward only");
   // dynamic shared memory: per-warp WarpMem (+ WarpAcc in the backward) at fixed
@@ -1311,7 +1312,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS
       BWD, std::conditional_t<KA == kA, WMBwd, WMBwdMid>,
       std::conditional_t<KA == kA, WMFwd, std::conditional_t<KA == kAMid, WMMid, WMBig>>>;
   WM& M = reinterpret_cast<WM*>(smem_raw)[wid];
-  using AC = WarpAccT<WM::kNSlots>;
+  using AC = WarpAccT<WM::kNSlots, BASIS != 0>;
   AC& A = reinterpret_cast<AC*>(smem_raw + sizeof(WM) * kWarps)[BWD ? wid : 0];
   constexpr int kRetK = KA + 32;       // backward: retired (expired, not yet scattered) slots
   int ray;
@@ -1558,7 +1559,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS
         if (BWD && (int)lane < got) {
           A.a[count + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
           A.b[count + lane] = make_float2(0.f, 0.f);
-          A.c[count + lane] = 0.f;
+          if (BASIS != 0) A.c[count + lane] = 0.f;
         }
         if (lane == 0) cnt.pairs += got;
         count += got;
@@ -1954,7 +1955,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS
               if ((int)lane < got) {
                 A.a[KA + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
                 A.b[KA + lane] = make_float2(0.f, 0.f);
-                A.c[KA + lane] = 0.f;
+                if (BASIS != 0) A.c[KA + lane] = 0.f;
               }
               __syncwarp();
               grad_range<GW, BASIS>(M, A, KA, KA + got);
@@ -2207,7 +2208,10 @@ void launch_gw(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
 
 constexpr size_t kSmemFwd = sizeof(WMFwd) * kWarps;
 constexpr size_t kSmemBwd = (sizeof(WMBwd) + sizeof(WarpAccT<WMBwd::kNSlots>)) * kWarps;
+constexpr size_t kSmemBwdG = (sizeof(WMBwd) + sizeof(WarpAccT<WMBwd::kNSlots, false>)) * kWarps;
 constexpr size_t kSmemBwdMid = (sizeof(WMBwdMid) + sizeof(WarpAccT<WMBwdMid::kNSlots>)) * kWarps;
+// the Gaussian backward (no per-slot c) fits RG_MIN_BLOCKS blocks per SM
+static_assert(RG_MIN_BLOCKS * (kSmemBwdG + 1024) <= 228 * 1024, "backward blocks per SM");
 // 4 resident backward blocks must fit the 196 KB shared-memory carve-out (1 KB
 // reserved per block): a larger carve-out halves L1 and costs ~6% (measured)
 static_assert(kSmemBwd <= 48 * 1024 + 128, "backward block exceeds the 196 KB carve-out budget");
@@ -2218,6 +2222,7 @@ static_assert(2 * (kSmemBig + 1024) <= 228 * 1024, "two large-list blocks per SM
 template <bool BWD>
 void launch_render(const RenderArgs& A, dim3 grid, size_t smem, cudaStream_t st) {
   const int B = A.c.slab_samples;
+  if (BWD && A.c.basis == 0) smem = kSmemBwdG;   // the Gaussian backward has no per-slot c
   // forward large-list variant (rg_config.list_capacity, Gaussian basis, B >= 5)
   if constexpr (!BWD) {
     const bool instr = A.stats != nullptr || A.dbg_rec != nullptr;
