@@ -99,7 +99,7 @@ static_assert(kA == 64, "expire/n_in handle two 32-slot chunks");
 // backward traverses only for rays whose fetch log overflowed and must stay within
 // its 48 KB block budget
 constexpr int kStkFwd = RG_STK_FWD;
-constexpr int kStkBwd = 168;   // 5 Gaussian backward blocks per SM fit (static_assert below)
+constexpr int kStkBwd = 192;   // C4 re-traversals need it (168 overflowed: stress gradients off)
 constexpr unsigned kFull = 0xffffffffu;
 
 struct Counters {
@@ -2210,7 +2210,8 @@ constexpr size_t kSmemFwd = sizeof(WMFwd) * kWarps;
 constexpr size_t kSmemBwd = (sizeof(WMBwd) + sizeof(WarpAccT<WMBwd::kNSlots>)) * kWarps;
 constexpr size_t kSmemBwdG = (sizeof(WMBwd) + sizeof(WarpAccT<WMBwd::kNSlots, false>)) * kWarps;
 constexpr size_t kSmemBwdMid = (sizeof(WMBwdMid) + sizeof(WarpAccT<WMBwdMid::kNSlots>)) * kWarps;
-// the Gaussian backward (no per-slot c) fits RG_MIN_BLOCKS blocks per SM
+// the Gaussian backward (no per-slot c) fits RG_MIN_BLOCKS (4) blocks per SM; 5 blocks
+// (96 registers) measured slower, 4.83 -> 5.38 ms (profiles/r2/ab_bwd_blocks.log)
 static_assert(RG_MIN_BLOCKS * (kSmemBwdG + 1024) <= 228 * 1024, "backward blocks per SM");
 // 4 resident backward blocks must fit the 196 KB shared-memory carve-out (1 KB
 // reserved per block): a larger carve-out halves L1 and costs ~6% (measured)
