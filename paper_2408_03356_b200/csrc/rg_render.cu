@@ -53,6 +53,9 @@ namespace {
 #ifndef RG_TWO_UNCOND
 #define RG_TWO_UNCOND 0          // restart query: the second node's loads without a branch
 #endif
+#ifndef RG_GRAD_FIXED
+#define RG_GRAD_FIXED 0          // backward member loop over the whole part (A/B knob)
+#endif
 #ifndef RG_RANGE_BRANCHFREE
 #define RG_RANGE_BRANCHFREE 1    // per-slab-path evaluation (eval_range) predicated in the
 #endif                           // backward (medians of 9: backward 5.18 -> 5.02 ms; the
@@ -1754,8 +1757,17 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS
                 kh = min(kh, min(last, part0 + P2 - 1));
 #if RG_GRAD_BRANCHFREE
                 if (BASIS == 0) {
+#if RG_GRAD_FIXED
+                  // the whole part, a fixed trip count: samples outside the support or
+                  // past the termination carry zero coefficients (A.s0 / A.s1) or fail
+                  // the interval test, so they add exactly nothing
+                  (void)kl; (void)kh;
+#pragma unroll 4
+                  for (int k = part0; k < part0 + P2; ++k) {
+#else
 #pragma unroll kMemberUnroll
                   for (int k = kl; k <= kh; ++k) {
+#endif
                     const float4 s0 = A.s0[k];
                     const float tkk = s0.x;
                     const float b2 = A.s1[k];
