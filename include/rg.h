@@ -133,8 +133,13 @@ typedef struct {
   int32_t n, sh_degree, sg_count, app_stride;
   const void* geom;        /* [n] 64-B records, Morton order */
   const float* app;        /* [n, app_stride] appearance, Morton order */
-  const void* nodes;       /* [n-1] 64-B internal nodes (child boxes + child ids) */
-  const void* wide;        /* 32-wide collapse of the Karras tree (traversal structure) */
+  const void* nodes;       /* [n-1] 64-B internal nodes (child boxes, child ids, the
+                              node's first and last leaf in Morton order) */
+  const void* wide;        /* 32-wide collapse of the Karras tree (traversal structure):
+                              896-B nodes, 6 SoA box planes + 32 child ids; id >= 0 a
+                              wide node, 0x7FFFFFFF empty, < 0 a leaf range
+                              ~((first << 3) | (count - 1)) of 1..8 consecutive
+                              Morton-order Gaussians (so n < 2^28) */
   const int32_t* wide_info;/* device [4]: wide node count, -, -, rounds left unfinished */
   const float* leaf_box;   /* [n,6] padded AABBs, Morton order */
   const float* root_box;   /* [6] scene bbox = union of active AABBs */
@@ -176,9 +181,9 @@ size_t rg_bvh_workspace_bytes(int32_t n, int32_t sh_degree, int32_t sg_count);
 
 /* Preprocess (R(q), M = S^-1 R^T, support radius, padded tight AABB: P:176-183,
    P:529-558), 30-bit Morton codes of the means, stable CUB-free LSD radix sort,
-   Karras hierarchy, bottom-up refit.  Errors: RG_ERR_INVALID_ARG for NULL
-   pointers, n < 0, sh_degree not in 0..3, sg_count not in 0..7, bad config;
-   RG_ERR_WORKSPACE_TOO_SMALL. */
+   Karras hierarchy, bottom-up refit, 32-wide collapse with leaf ranges.
+   Errors: RG_ERR_INVALID_ARG for NULL pointers, n < 0 or n >= 2^28, sh_degree
+   not in 0..3, sg_count not in 0..7, bad config; RG_ERR_WORKSPACE_TOO_SMALL. */
 rg_status rg_build_bvh(const rg_gaussians* g, const rg_config* cfg, void* ws, size_t ws_bytes,
                        rg_bvh* out, void* stream);
 

@@ -8,7 +8,20 @@
 #include <atomic>
 #include <mutex>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: a no-op unless a profiler injects
+
 using namespace rg;
+
+namespace {
+// one NVTX range per C-ABI call that enqueues GPU work (SURVEY §5 tracing)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
+#define RG_NVTX(name) NvtxRange nvtx_range_(name)
 
 namespace rg {
 // diagnostic: number of kernels this library enqueued (process-wide)
@@ -174,8 +187,10 @@ size_t rg_bvh_workspace_bytes(int32_t n, int32_t sh_degree, int32_t sg_count) {
 
 rg_status rg_build_bvh(const rg_gaussians* g, const rg_config* cfg, void* ws, size_t ws_bytes,
                        rg_bvh* out, void* stream) {
+  RG_NVTX("rg_build_bvh");
   if (!gaussians_ok(g) || !config_ok(cfg) || !ws || !out) return RG_ERR_INVALID_ARG;
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return RG_ERR_INVALID_ARG;
+  if (g->n >= kMaxLeafPos) return RG_ERR_INVALID_ARG;   // leaf-range encoding
   const BvhLayout L = bvh_layout(g->n, g->sh_degree, g->sg_count);
   if (ws_bytes < L.total) return RG_ERR_WORKSPACE_TOO_SMALL;
   char* w = static_cast<char*>(ws);
@@ -206,6 +221,7 @@ rg_status rg_build_bvh(const rg_gaussians* g, const rg_config* cfg, void* ws, si
 
 rg_status rg_refit_bvh(const rg_gaussians* g, const rg_config* cfg, void* ws, size_t ws_bytes,
                        rg_bvh* bvh, void* stream) {
+  RG_NVTX("rg_refit_bvh");
   if (!gaussians_ok(g) || !config_ok(cfg) || !ws || !bvh) return RG_ERR_INVALID_ARG;
   if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return RG_ERR_INVALID_ARG;
   const BvhLayout L = bvh_layout(g->n, g->sh_degree, g->sg_count);
@@ -233,6 +249,7 @@ bool arrays_ok(const rg_gaussian_grads* a, int32_t n, int32_t G) {
 rg_status rg_adam_step(const rg_adam_config* cfg, const rg_gaussian_grads* grad_act,
                        const rg_param_arrays* raw, const rg_param_arrays* m,
                        const rg_param_arrays* v, const rg_param_arrays* act_out, void* stream) {
+  RG_NVTX("rg_adam_step");
   if (!cfg || cfg->n < 0 || cfg->sh_degree < 0 || cfg->sh_degree > kMaxDeg || cfg->sg_count < 0 ||
       cfg->sg_count > kMaxLobes || cfg->step < 1)
     return RG_ERR_INVALID_ARG;
@@ -261,6 +278,7 @@ size_t rg_dssim_workspace_bytes(int32_t width, int32_t height) {
 rg_status rg_l1_dssim_loss_grad(const float* rgb, const float* target, int32_t width,
                                 int32_t height, float lambda, float* d_rgb, float* loss, void* ws,
                                 size_t ws_bytes, void* stream) {
+  RG_NVTX("rg_l1_dssim_loss_grad");
   if (width < 0 || height < 0 || !(lambda >= 0.f && lambda <= 1.f)) return RG_ERR_INVALID_ARG;
   if ((size_t)width * height == 0) return RG_OK;
   if (!rgb || !target || !d_rgb || !ws) return RG_ERR_INVALID_ARG;
@@ -273,6 +291,7 @@ rg_status rg_l1_dssim_loss_grad(const float* rgb, const float* target, int32_t w
 
 rg_status rg_supersample_resolve(const float* rgb_rays, int64_t n_pixels, int32_t spp,
                                  float* rgb_px, void* stream) {
+  RG_NVTX("rg_supersample_resolve");
   if (n_pixels < 0 || spp < 1 || (n_pixels > 0 && (!rgb_rays || !rgb_px))) return RG_ERR_INVALID_ARG;
   cudaGetLastError();
   return launch_ss_resolve(rgb_rays, n_pixels, spp, rgb_px, static_cast<cudaStream_t>(stream)) ==
@@ -281,6 +300,7 @@ rg_status rg_supersample_resolve(const float* rgb_rays, int64_t n_pixels, int32_
 
 rg_status rg_supersample_spread(const float* d_px, int64_t n_pixels, int32_t spp, float* d_rays,
                                 void* stream) {
+  RG_NVTX("rg_supersample_spread");
   if (n_pixels < 0 || spp < 1 || (n_pixels > 0 && (!d_px || !d_rays))) return RG_ERR_INVALID_ARG;
   cudaGetLastError();
   return launch_ss_spread(d_px, n_pixels, spp, d_rays, static_cast<cudaStream_t>(stream)) ==
@@ -289,6 +309,7 @@ rg_status rg_supersample_spread(const float* d_px, int64_t n_pixels, int32_t spp
 
 rg_status rg_densify_accumulate(const float* grad_mean, int32_t n, float* acc, int32_t* cnt,
                                 void* stream) {
+  RG_NVTX("rg_densify_accumulate");
   if (n < 0 || (n > 0 && (!grad_mean || !acc || !cnt))) return RG_ERR_INVALID_ARG;
   cudaGetLastError();
   return launch_dens_acc(grad_mean, n, acc, cnt, static_cast<cudaStream_t>(stream)) == cudaSuccess
@@ -301,6 +322,7 @@ rg_status rg_densify_plan(const rg_gaussians* g, const float* acc, const int32_t
                           float grad_eps, float extent, float sigma_eps, float percent_dense,
                           int32_t* action, void* ws, size_t ws_bytes, int32_t* counts,
                           void* stream) {
+  RG_NVTX("rg_densify_plan");
   if (!gaussians_ok(g) || !counts || !ws) return RG_ERR_INVALID_ARG;
   if (g->n > 0 && (!acc || !cnt || !action)) return RG_ERR_INVALID_ARG;
   if (!isfinite(grad_eps) || !(extent >= 0.f) || !isfinite(sigma_eps) || !(percent_dense >= 0.f))
@@ -315,6 +337,7 @@ rg_status rg_densify_plan(const rg_gaussians* g, const float* acc, const int32_t
 rg_status rg_densify_apply(const rg_gaussians* g, const rg_param_arrays* in,
                            const int32_t* action, const void* ws, const int32_t* counts,
                            const float* z, int32_t mode, const rg_param_arrays* out, void* stream) {
+  RG_NVTX("rg_densify_apply");
   if (!gaussians_ok(g) || !out || !ws || !counts || mode < 0 || mode > 2) return RG_ERR_INVALID_ARG;
   if (g->n > 0 && (!action || !z)) return RG_ERR_INVALID_ARG;
   rg_gaussian_grads src;
@@ -339,6 +362,7 @@ int64_t rg_camera_ray_count(const rg_camera* cam) {
 }
 
 rg_status rg_camera_rays(const rg_camera* cam, float* origin, float* dir, void* stream) {
+  RG_NVTX("rg_camera_rays");
   if (!cam || !rays_ok(nullptr, cam)) return RG_ERR_INVALID_ARG;
   const int64_t n = camera_ray_slots(*cam);
   if (n > 0 && (!origin || !dir)) return RG_ERR_INVALID_ARG;
@@ -352,6 +376,7 @@ rg_status rg_render_forward(const rg_gaussians* g, const rg_bvh* bvh, const rg_c
                             int32_t* replay, void* fetch_log, size_t log_bytes,
                             rg_stats* stats, int32_t debug_rays, int32_t debug_cap,
                             int32_t* debug_counts, int32_t* debug_records, void* stream) {
+  RG_NVTX("rg_render_forward");
   if (!gaussians_ok(g) || !config_ok(cfg) || !bvh_ok(bvh, g) || !rays_ok(rays, cam))
     return RG_ERR_INVALID_ARG;
   if (cfg->basis != 0 && cfg->slab_samples < 5) return RG_ERR_NOT_IMPLEMENTED;
@@ -388,6 +413,7 @@ rg_status rg_render_backward(const rg_gaussians* g, const rg_bvh* bvh, const rg_
                              size_t log_bytes, const float* d_rgb,
                              const rg_gaussian_grads* grads, rg_stats* stats, void* ws,
                              size_t ws_bytes, void* stream) {
+  RG_NVTX("rg_render_backward");
   if (!gaussians_ok(g) || !config_ok(cfg) || !bvh_ok(bvh, g) || !rays_ok(rays, cam) || !grads)
     return RG_ERR_INVALID_ARG;
   if (cfg->basis != 0 && cfg->slab_samples < 5) return RG_ERR_NOT_IMPLEMENTED;
@@ -408,6 +434,7 @@ rg_status rg_render_backward(const rg_gaussians* g, const rg_bvh* bvh, const rg_
 
 rg_status rg_l1_loss_grad(const float* rgb, const float* target, int64_t n_values, float scale,
                           float* d_rgb, float* loss, void* stream) {
+  RG_NVTX("rg_l1_loss_grad");
   if (n_values < 0 || (n_values > 0 && (!rgb || !target || !d_rgb || !loss)))
     return RG_ERR_INVALID_ARG;
   return launch_l1(rgb, target, n_values, scale, d_rgb, loss, static_cast<cudaStream_t>(stream)) ==

@@ -233,20 +233,83 @@ __global__ void __launch_bounds__(1024) k_radix_scan(uint32_t* hist, int total) 
   }
 }
 
+// Onesweep (Adinets & Merrill 2022) building blocks: the digit counts of every
+// pass from ONE read of the keys (LSD passes permute the keys, never change them)
+constexpr int kOsPasses = 7;              // 3 fine-code + 4 code passes
+#ifndef RG_ONESWEEP
+#define RG_ONESWEEP 1
+#endif
+constexpr bool kOnesweep = RG_ONESWEEP != 0;
+__global__ void __launch_bounds__(kThreads) k_digit_hist(const uint32_t* keys, int n, int npass,
+                                                         uint32_t* gcount) {
+  __shared__ uint32_t h[4][256];
+  for (int p = 0; p < 4; ++p) h[p][threadIdx.x] = 0;
+  __syncthreads();
+  for (int i = blockIdx.x * kThreads + threadIdx.x; i < n; i += gridDim.x * kThreads) {
+    const uint32_t k = keys[i];
+    for (int p = 0; p < npass; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xFF], 1u);
+  }
+  __syncthreads();
+  for (int p = 0; p < npass; ++p)
+    if (h[p][threadIdx.x]) atomicAdd(&gcount[p * 256 + threadIdx.x], h[p][threadIdx.x]);
+}
+
+// Stable scatter of one LSD pass.  OS = false: the tile's digit offsets come from
+// k_radix_hist + k_radix_scan (hist, digit-major).  OS = true (Onesweep): one launch
+// per pass; tiles are taken in launch order from a counter, each publishes its digit
+// counts (flag | count in one word: 1 = aggregate, 2 = inclusive prefix) and looks
+// back over its predecessors' words (decoupled look-back) for its exclusive prefix;
+// the digit bases are the exclusive scan of the pass's global counts.
+constexpr uint32_t kOsAgg = 1u << 30, kOsInc = 2u << 30, kOsVal = (1u << 30) - 1u;
+template <bool OS>
 __global__ void __launch_bounds__(kThreads) k_radix_scatter(const uint32_t* kin, const uint32_t* vin,
                                                             uint32_t* kout, uint32_t* vout, int n,
                                                             int shift, const uint32_t* hist,
-                                                            int tiles) {
+                                                            int tiles, const uint32_t* gcount,
+                                                            uint32_t* status, int* tile_ctr) {
   constexpr int kWarps = kThreads / 32;
   __shared__ uint32_t base_off[256];
   __shared__ uint32_t run[256];
   __shared__ uint32_t wcnt[kWarps][256];   // (round << 16) | count
+  __shared__ int tile_s;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  base_off[t] = hist[t * tiles + blockIdx.x];
+  int tile = blockIdx.x;
+  if (!OS) {
+    base_off[t] = hist[t * tiles + blockIdx.x];
+  } else {
+    if (t == 0) tile_s = atomicAdd(tile_ctr, 1);
+    run[t] = 0;
+    base_off[t] = gcount[t];
+    __syncthreads();
+    tile = tile_s;
+    for (int r = 0; r < kItems; ++r) {                // this tile's digit counts
+      const int i = tile * kTile + r * kThreads + t;
+      if (i < n) atomicAdd(&run[(kin[i] >> shift) & 0xFF], 1u);
+    }
+    for (int off = 1; off < 256; off <<= 1) {         // inclusive scan of the digit bases
+      const uint32_t v = t >= off ? base_off[t - off] : 0u;
+      __syncthreads();
+      base_off[t] += v;
+      __syncthreads();
+    }
+    const uint32_t c = run[t];
+    volatile uint32_t* vs = status;
+    vs[(size_t)tile * 256 + t] = (tile == 0 ? kOsInc : kOsAgg) | c;
+    uint32_t excl = 0;
+    for (int p = tile - 1; p >= 0;) {                 // look-back (predecessors are resident:
+      const uint32_t v = vs[(size_t)p * 256 + t];     // they took smaller tickets)
+      if (!(v & (kOsAgg | kOsInc))) continue;
+      excl += v & kOsVal;
+      if (v & kOsInc) break;
+      --p;
+    }
+    if (tile > 0) vs[(size_t)tile * 256 + t] = kOsInc | (excl + c);
+    base_off[t] = base_off[t] - gcount[t] + excl;     // exclusive digit base + tile prefix
+  }
   run[t] = 0;
   for (int w = 0; w < kWarps; ++w) wcnt[w][t] = 0xFFFF0000u;
   __syncthreads();
-  const int tbase = blockIdx.x * kTile;
+  const int tbase = tile * kTile;
   const uint32_t lt = (1u << lane) - 1u;
   for (int r = 0; r < kItems; ++r) {
     const int i = tbase + r * kThreads + t;
@@ -367,7 +430,8 @@ __global__ void __launch_bounds__(kThreads) k_karras(const uint32_t* k, int n, f
   const int gamma = i + s * d + min(d, 0);
   const int left = (min(i, j) == gamma) ? ~gamma : gamma;
   const int right = (max(i, j) == gamma + 1) ? ~(gamma + 1) : gamma + 1;
-  nodes[4 * (size_t)i + 3] = make_float4(__int_as_float(left), __int_as_float(right), 0.f, 0.f);
+  nodes[4 * (size_t)i + 3] = make_float4(__int_as_float(left), __int_as_float(right),
+                                         __int_as_float(min(i, j)), __int_as_float(max(i, j)));
   if (left < 0) parent_leaf[~left] = i; else parent_int[left] = i;
   if (right < 0) parent_leaf[~right] = i; else parent_int[right] = i;
   if (i == 0) parent_int[0] = -1;
@@ -464,8 +528,14 @@ __global__ void __launch_bounds__(128) k_wide_refit(const float4* nodes, const f
     const int child = W.child[lane];
     if (child == kWideEmpty) continue;
     float b[6];
-    if (child < 0) {
-      for (int k = 0; k < 6; ++k) b[k] = leaf_box[6 * (size_t)(~child) + k];
+    if (child < 0) {                                  // union of the range's leaf boxes
+      const int f = leaf_range_first(child), c = leaf_range_count(child);
+      for (int k = 0; k < 6; ++k) b[k] = leaf_box[6 * (size_t)f + k];
+      for (int r = 1; r < c; ++r)
+        for (int k = 0; k < 3; ++k) {
+          b[k] = fminf(b[k], leaf_box[6 * (size_t)(f + r) + k]);
+          b[3 + k] = fmaxf(b[3 + k], leaf_box[6 * (size_t)(f + r) + 3 + k]);
+        }
     } else {
       const float* x = reinterpret_cast<const float*>(nodes + 4 * (size_t)wide_src[child]);
       for (int k = 0; k < 3; ++k) {
@@ -537,12 +607,16 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
       continue;
     }
     // entries 0, 1: the binary node's children
-    int id = -1;
+    // each entry also carries its leaf range [f, f + cnt) (Morton order)
+    int id = -1, f = 0, cnt = 0;
     float b[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
     if (lane < 2) {
       const float* w = reinterpret_cast<const float*>(nodes + 4 * (size_t)jb);
       const int4 c = *reinterpret_cast<const int4*>(nodes + 4 * (size_t)jb + 3);
       id = lane == 0 ? c.x : c.y;
+      const int gamma = c.x >= 0 ? c.x : ~c.x;        // left child's last leaf
+      f = lane == 0 ? c.z : gamma + 1;
+      cnt = lane == 0 ? gamma - c.z + 1 : c.w - gamma;
       for (int k = 0; k < 6; ++k) b[k] = w[6 * lane + k];
     }
 #if RG_COLLAPSE_PREFETCH
@@ -565,9 +639,14 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
     int m = 2;
     while (m < kWide) {
       const bool internal = lane < m && id >= 0;
-      const unsigned cm = __ballot_sync(full, internal);
-      if (!cm) break;
-      const float area = internal ? box_area(b) : -2.f;
+      if (!__ballot_sync(full, internal)) break;
+      // subtrees of more than kLeafRange leaves open first (largest area); the
+      // small ones (future leaf ranges) only open while slots remain
+      const bool big = internal && (kLeafRange == 1 || cnt > kLeafRange);
+      const unsigned bm = __ballot_sync(full, big);
+      const bool cand = bm ? big : internal;
+      const unsigned cm = __ballot_sync(full, cand);
+      const float area = cand ? box_area(b) : -2.f;
       int rank = 0;                                   // by area, descending (ties: lane)
       if (RG_COLLAPSE_OPEN <= 2) {
         // only ranks < 2 open: the largest areas, lowest lane on ties (reductions
@@ -590,8 +669,8 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
         }
       }
       const int r = min(min(__popc(cm), kWide - m), RG_COLLAPSE_OPEN);
-      const bool open = internal && rank < r;
-      int rid = -1;
+      const bool open = cand && rank < r;
+      int rid = -1, rf = 0, rcnt = 0;
       float rb[6];
       if (open) {                                     // left child in place, right one out
 #if RG_COLLAPSE_PREFETCH
@@ -605,15 +684,25 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
         rid = c.y;
         for (int k = 0; k < 6; ++k) { b[k] = w[k]; rb[k] = w[6 + k]; }
 #endif
+        if (kLeafRange > 1) {                         // ranges tracked only when used
+          const int gamma = id >= 0 ? id : ~id;
+          rf = gamma + 1;
+          rcnt = f + cnt - 1 - gamma;
+          cnt = gamma - f + 1;
+        }
       }
       bool fresh = open;
       for (int j = 0; j < r; ++j) {                   // right child of rank j -> lane m + j
         const int src = __ffs(__ballot_sync(full, open && rank == j)) - 1;
         const int vid = __shfl_sync(full, rid, src);
+        const int vf = kLeafRange > 1 ? __shfl_sync(full, rf, src) : 0;
+        const int vc = kLeafRange > 1 ? __shfl_sync(full, rcnt, src) : 0;
         float vb[6];
         for (int k = 0; k < 6; ++k) vb[k] = __shfl_sync(full, open ? rb[k] : 0.f, src);
         if (lane == m + j) {
           id = vid;
+          f = vf;
+          cnt = vc;
           for (int k = 0; k < 6; ++k) b[k] = vb[k];
           fresh = true;
         }
@@ -625,9 +714,10 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
 #endif
       m += r;
     }
-    // write the wide node; internal children become queue items
+    // write the wide node; internal children of more than kLeafRange leaves become
+    // queue items, the others leaf ranges (single leaves: ranges of one)
     const bool live = lane < m;
-    const bool internal = live && id >= 0;
+    const bool internal = live && id >= 0 && (kLeafRange == 1 || cnt > kLeafRange);
     const unsigned im = __ballot_sync(full, internal);
     const int nint = __popc(im);
     int wid0 = 0, qs0 = 0;
@@ -637,7 +727,7 @@ __global__ void __launch_bounds__(128) k_collapse_warp(const float4* nodes, Wide
     }
     wid0 = __shfl_sync(full, wid0, 0);
     qs0 = __shfl_sync(full, qs0, 0);
-    int child = live ? id : kWideEmpty;
+    int child = !live ? kWideEmpty : id < 0 ? leaf_range_enc(~id, 1) : leaf_range_enc(f, cnt);
     if (internal) {
       const int rk = __popc(im & ((1u << lane) - 1u));
       const int wid = wid0 + rk;
@@ -696,7 +786,9 @@ BvhLayout bvh_layout(int n, int deg, int lobes) {
   L.parent_leaf = take(4 * nn);
   L.refit_cnt = take(4 * ni);
   L.bounds = take(32);
-  L.hist = take(4 * 256 * (size_t)L.tiles);
+  // hist: [256 * tiles] of the per-pass hist/scan sort, or the Onesweep words:
+  // [kOsPasses][tiles][256] status, [kOsPasses][256] digit counts, [8] tile counters
+  L.hist = take(4 * ((size_t)kOsPasses * 256 * (L.tiles + 1) + 8));
   L.wide = take(sizeof(WideNode) * wide_capacity(n));
   L.wq_a = take(8 * nn);
   L.wide_src = take(8 * nn);
@@ -713,7 +805,9 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
   k_init<<<1, 32, 0, st>>>(bounds, root_box);
   count_launches(1);
   if (n == 0) return cudaGetLastError();
-  count_launches(n > 1 ? 28 : 27);
+  // preprocess, morton, gather, pack, pack_app (+ karras, refit) and the sort: 7 x 3
+  // launches, or 7 Onesweep passes + 2 digit histograms
+  count_launches((n > 1 ? 28 : 27) - (kOnesweep ? 12 : 0));
   const int blocks = (n + kThreads - 1) / kThreads;
   float* box_orig = reinterpret_cast<float*>(ws + L.box_orig);
   int* flags = reinterpret_cast<int*>(ws + L.flags);
@@ -734,19 +828,36 @@ cudaError_t launch_build(const rg_gaussians& g, const rg_config& c, char* ws, co
       opted = true;
     }
   }
+  uint32_t* os_status = hist;
+  uint32_t* os_count = hist + (size_t)kOsPasses * 256 * L.tiles;
+  int* os_ctr = reinterpret_cast<int*>(os_count + kOsPasses * 256);
+  const int hblocks = min(L.tiles, 148 * 2);
+  if (kOnesweep)
+    cudaMemsetAsync(hist, 0, 4 * ((size_t)kOsPasses * 256 * (L.tiles + 1) + 8), st);
+  int os_pass = 0;
   auto radix_pass = [&](const uint32_t* ki, const uint32_t* vi, uint32_t* ko, uint32_t* vo,
                         int shift) {
+    if (kOnesweep) {
+      k_radix_scatter<true><<<L.tiles, kThreads, 0, st>>>(
+          ki, vi, ko, vo, n, shift, nullptr, L.tiles, os_count + 256 * os_pass,
+          os_status + (size_t)256 * L.tiles * os_pass, os_ctr + os_pass);
+      ++os_pass;
+      return;
+    }
     k_radix_hist<<<L.tiles, kThreads, 0, st>>>(ki, n, shift, hist, L.tiles);
     k_radix_scan<<<1, 1024, scan_smem, st>>>(hist, 256 * L.tiles);
-    k_radix_scatter<<<L.tiles, kThreads, 0, st>>>(ki, vi, ko, vo, n, shift, hist, L.tiles);
+    k_radix_scatter<false><<<L.tiles, kThreads, 0, st>>>(ki, vi, ko, vo, n, shift, hist, L.tiles,
+                                                         nullptr, nullptr, nullptr);
   };
   // stable LSD sort by (code, fine code, index) (L34): first the 21-bit fine code
   // (3 passes, ending in kb/vb), then the 30-bit code (4 passes, ending in ka/va)
+  if (kOnesweep) k_digit_hist<<<hblocks, kThreads, 0, st>>>(ka, n, 3, os_count);
   radix_pass(ka, va, kb, vb, 0);
   radix_pass(kb, vb, ka, va, 8);
   radix_pass(ka, va, kb, vb, 16);
   k_gather_codes<<<blocks, kThreads, 0, st>>>(reinterpret_cast<const uint32_t*>(ws + L.codes), vb,
                                               ka, va, n);
+  if (kOnesweep) k_digit_hist<<<hblocks, kThreads, 0, st>>>(ka, n, 4, os_count + 3 * 256);
   for (int pass = 0; pass < 4; ++pass) {
     const int shift = 8 * pass;
     if (pass & 1) radix_pass(kb, vb, ka, va, shift);

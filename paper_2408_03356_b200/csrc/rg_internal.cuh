@@ -70,20 +70,42 @@ __host__ __device__ inline int grad_stride(int deg, int lobes) {
 //  g0 = {mu.x, mu.y, mu.z, sigma~}   g1 = {M0, M1, M2, M3}
 //  g2 = {M4, M5, M6, M7}             g3 = {M8, r2 (<0: inactive), idx bits, 0}
 // node record, 64 B: n0 = {L.lo.xyz, L.hi.x} n1 = {L.hi.yz, R.lo.xy}
-//                    n2 = {R.lo.z, R.hi.xyz} n3 = {left, right (int bits), 0, 0}
-// child id >= 0: internal node, < 0: leaf ~pos.
+//                    n2 = {R.lo.z, R.hi.xyz} n3 = {left, right (int bits), first, last}
+// child id >= 0: internal node, < 0: leaf ~pos; [first, last]: the node's leaf
+// range in Morton order (Karras: its split gamma is left or ~left).
 
 // 32-wide BVH node (collapse of the Karras tree, one child per warp lane):
-// SoA child boxes and child ids; child >= 0: wide node, < 0: leaf ~pos,
-// kWideEmpty: unused slot (its box is empty).
+// SoA child boxes and child ids; child >= 0: wide node, < 0: a leaf RANGE
+// ~((first << 3) | (count - 1)) of 1..kLeafRange consecutive Morton-order
+// Gaussians (a binary subtree of <= kLeafRange leaves is not made a wide node
+// of its own: its leaves are queued for the exact test directly, and its box is
+// the union of theirs), kWideEmpty: unused slot (its box is empty).
 constexpr int kWide = 32;
 constexpr int kWideEmpty = 0x7FFFFFFF;
+// leaf ranges of up to RG_LEAF_RANGE Gaussians: measured (medians of 9, C1):
+// R = 1 forward 6.33 / backward 4.83 ms, R = 2 6.80 / 5.33, R = 4 6.72 / 5.34,
+// R = 8 9.52 / 5.58 -- R = 4 cuts node visits by 20% (C1) and 45% (C3) but the
+// extra exact tests cost more (C3 forward +23%): single leaves by default
+#ifndef RG_LEAF_RANGE
+#define RG_LEAF_RANGE 1
+#endif
+constexpr int kLeafRange = RG_LEAF_RANGE;
+static_assert(kLeafRange >= 1 && kLeafRange <= 8, "leaf ranges: 3-bit count");
+constexpr int kMaxLeafPos = 1 << 28;   // n limit of the range encoding
+__host__ __device__ __forceinline__ int leaf_range_enc(int first, int count) {
+  return ~((first << 3) | (count - 1));
+}
+__host__ __device__ __forceinline__ int leaf_range_first(int child) {
+  return (int)((unsigned)~child >> 3);
+}
+__host__ __device__ __forceinline__ int leaf_range_count(int child) { return (~child & 7) + 1; }
 struct WideNode {
   float lox[kWide], loy[kWide], loz[kWide], hix[kWide], hiy[kWide], hiz[kWide];
   int child[kWide];
 };
 // Upper bound on the wide-node count of the greedy collapse: a wide node with
-// fewer than 32 entries holds only leaves (>= 2 of them), so there are at most
+// fewer than 32 entries holds only single leaves (>= 2 of them: it was made
+// for a subtree of > kLeafRange >= 1 leaves, or is the root), so there are at most
 // n/2 such nodes; every other node has 32 entries, and entries = (W - 1) + n,
 // which bounds the full ones by (n - 1 - W_partial)/31.  Hence
 // W <= n/2 + (n/2)/31 + 1 (a balanced grid scene reaches 33825 of 33827 at

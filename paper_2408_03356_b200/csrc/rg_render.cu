@@ -173,7 +173,15 @@ struct WarpMemT {
       uint32_t lqk[NCAP > 1 ? 96 : 1];   // box-entry lower bounds of the queued leaves (fkey)
     } s;
   } u;
-  uint32_t lq[96];     // queued leaves awaiting the exact test (< 32 + 2 x 32)
+  // queued Gaussians awaiting the exact test (fetch): kept in the transient slots'
+  // e2 words, dead during a query; < 32 left over + the leaf ranges of kLqGroup
+  // lanes at a time
+  static constexpr int kLq = (SLOTS - KA) * 4;
+  static constexpr int kLqGroup = 31 + 32 * kLeafRange <= kLq ? 32 : 31 + 16 * kLeafRange <= kLq ? 16 : 8;
+  static_assert(31 + kLqGroup * kLeafRange <= kLq, "leaf queue");
+#if RG_STREAM
+  uint32_t lq[96];     // stream_next's leaf queue
+#endif
   Stream sst;          // stream_next state between refills (registers only inside the call)
   // fetch-log bookkeeping of the ray (warp-uniform, rarely touched): kept here, not in
   // registers, to relieve the register pressure of the march loops
@@ -198,6 +206,7 @@ struct WarpMemT {
 #define RG_STREAM_FROM 0       // forward refills served by restart queries before the stream
 #endif
 constexpr bool kStream = RG_STREAM != 0;
+static_assert(!kStream || kLeafRange == 1, "stream_next queues single leaves (RG_LEAF_RANGE=1)");
 constexpr int kNCap = kStream ? RG_NCAP : 1;   // forward node-frontier capacity (stream_next)
 constexpr int kCCap = kStream ? RG_CCAP : 32;  // forward candidate capacity (stream_next)
 static_assert(kCCap % 32 == 0 && kCCap <= 128, "candidate merge reads CCAP/32 entries per lane");
@@ -281,6 +290,7 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
   // candidate sort scratch aliases the transient slots, dead during every fetch
   unsigned long long* const kscr = reinterpret_cast<unsigned long long*>(&M.e0[WM::kTr]);
   uint32_t* const pscr = reinterpret_cast<uint32_t*>(&M.e1[WM::kTr]);
+  uint32_t* const lq = reinterpret_cast<uint32_t*>(&M.e2[WM::kTr]);
   key = ~0ull;
   pos = 0;
   int nk = 0;
@@ -294,9 +304,10 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
   // Exact leaf tests are batched: box-passing leaves are queued in shared
   // memory and tested 32 at a time (all lanes busy), then the candidates are
   // bitonic-sorted and bitonic-merged into the k-buffer.
-  auto flush = [&](int n) {
+  // ---- fq exact test
+  auto flush = [&](int off, int n) {   // exact tests of lq[off, off + n), n <= 32
     __syncwarp();
-    const uint32_t cp = (int)lane < n ? M.lq[lane] : 0u;
+    const uint32_t cp = (int)lane < n ? lq[off + lane] : 0u;
     bool cand = false;
     unsigned long long ck = ~0ull;
     if ((int)lane < n) {
@@ -319,18 +330,11 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
 #endif
       }
     }
-    // drop the consumed queue entries
-    const int rem = qn - n;   // < 64 left over (two nodes' leaves per iteration)
-    const uint32_t mv = (int)lane < rem ? M.lq[n + lane] : 0u;
-    const uint32_t mv2 = (int)lane + 32 < rem ? M.lq[n + 32 + lane] : 0u;
-    __syncwarp();
-    if ((int)lane < rem) M.lq[lane] = mv;
-    if ((int)lane + 32 < rem) M.lq[32 + lane] = mv2;
-    qn = rem;
     const unsigned cmask = __ballot_sync(kFull, cand);
     if (!cmask) return;
     uint32_t cpos;
     const int ncand = __popc(cmask);
+    // ---- fq rank sort
     // sort the candidates by rank (O(#candidates)): place, then read back in order
     // (a 32-bit-key variant for distinct t_entry keys, MATCH + vote first, measured
     // no faster: forward 7.247 -> 7.281 ms, medians of 9)
@@ -350,6 +354,7 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       cpos = pscr[lane];
       __syncwarp();
     }
+    // ---- fq merge
     // the 32 smallest of (k-buffer, candidates) form a bitonic sequence: merge
     {
       const unsigned long long rk = shfl64(ck, 31 - (int)lane);
@@ -369,11 +374,49 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       te_lim = fkey_inv((uint32_t)(kth >> 32));
     }
   };
+  // ---- fq drain
+  // exact tests of the full 32-entry groups; the < 32 left over move to the front
+  auto drain = [&]() {
+    if (qn < 32) return;
+    int off = 0;
+    do { flush(off, 32); off += 32; } while (qn - off >= 32);
+    const int rem = qn - off;
+    const uint32_t mv = (int)lane < rem ? lq[off + lane] : 0u;
+    __syncwarp();
+    if ((int)lane < rem) lq[lane] = mv;
+    qn = rem;
+  };
+  // queue the Gaussians of one node's hit leaf ranges (lane order), kLqGroup lanes
+  // at a time
+  auto enqueue = [&](bool lf, int child) {
+    const int f0 = leaf_range_first(child);
+#pragma unroll
+    for (int g = 0; g < 32; g += WM::kLqGroup) {
+      if (g) drain();
+      const bool in = lf && (int)lane >= g && (int)lane < g + WM::kLqGroup;
+      const int c = in ? leaf_range_count(child) : 0;
+      int inc = c;                                    // inclusive warp scan of the counts
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, inc, o);
+        if ((int)lane >= o) inc += v;
+      }
+      const int tot = __shfl_sync(kFull, inc, 31);
+      RG_CHECK(qn + tot <= WM::kLq);
+      const int w = qn + inc - c;
+#pragma unroll
+      for (int r = 0; r < kLeafRange; ++r)
+        if (r < c) lq[w + r] = (uint32_t)(f0 + r);
+      qn += tot;
+      __syncwarp();
+    }
+  };
   // Best-first-ish DFS: each iteration pops the two nodes with the smallest entry
   // distances among the top 32 stack entries and visits both (their 14 child-box
   // loads per lane are in flight together); when even the nearest lies beyond the
   // k-th key, all 32 are dropped.  Pushes are unordered (the pop selects).
   while (sp > 0) {
+    // ---- fq pop
     int nodeA, nodeB = -1;
     {
       const int nwin = min(sp, 32);
@@ -418,6 +461,7 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
     }
     if (lane == 0) cnt.nodes += nodeB >= 0 ? 2 : 1;
     const bool two = nodeB >= 0;
+    // ---- fq node loads
     const WideNode& WA = S.wide[nodeA];
     const WideNode& WB = S.wide[two ? nodeB : nodeA];
     const int childA = __ldg(&WA.child[lane]);
@@ -439,6 +483,7 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       bhx = __ldg(&WB.hix[lane]); bhy = __ldg(&WB.hiy[lane]); bhz = __ldg(&WB.hiz[lane]);
     }
 #endif
+    // ---- fq box test
     float tnA, tfA, tnB, tfB;
     box_t(alx, aly, alz, ahx, ahy, ahz, R.inv, R.oinv, tnA, tfA);
     box_t(blx, bly, blz, bhx, bhy, bhz, R.inv, R.oinv, tnB, tfB);
@@ -446,18 +491,29 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
                       tnA <= te_lim + slack;
     const bool hitB = childB != kWideEmpty && tnB <= tfB && tfB >= lo_s && tnB <= hi_s &&
                       tnB <= te_lim + slack;
-    // queue box-passing leaves (A's, then B's)
+    // ---- fq leaf queue
+    // queue the Gaussians of box-passing leaf ranges (A's, then B's)
     {
-      const unsigned lmA = __ballot_sync(kFull, hitA && childA < 0);
-      const unsigned lmB = __ballot_sync(kFull, hitB && childB < 0);
+      const bool lfA = hitA && childA < 0, lfB = hitB && childB < 0;
+      const unsigned lmA = __ballot_sync(kFull, lfA);
+      const unsigned lmB = __ballot_sync(kFull, lfB);
       if (lmA | lmB) {
         __syncwarp();
-        RG_CHECK(qn + __popc(lmA) + __popc(lmB) <= 96);
-        if (hitA && childA < 0) M.lq[qn + __popc(lmA & lt_mask)] = (uint32_t)(~childA);
-        if (hitB && childB < 0) M.lq[qn + __popc(lmA) + __popc(lmB & lt_mask)] = (uint32_t)(~childB);
-        qn += __popc(lmA) + __popc(lmB);
+        if (kLeafRange == 1) {
+          RG_CHECK(qn + __popc(lmA) + __popc(lmB) <= WM::kLq);
+          if (lfA) lq[qn + __popc(lmA & lt_mask)] = (uint32_t)leaf_range_first(childA);
+          if (lfB) lq[qn + __popc(lmA) + __popc(lmB & lt_mask)] = (uint32_t)leaf_range_first(childB);
+          qn += __popc(lmA) + __popc(lmB);
+        } else {
+          enqueue(lfA, childA);
+          if (lmB) {
+            drain();                                  // < 32 left before B's ranges
+            enqueue(lfB, childB);
+          }
+        }
       }
     }
+    // ---- fq push
     // internal children, any order (the pop selects)
     const unsigned imA = __ballot_sync(kFull, hitA && childA >= 0);
     const unsigned imB = __ballot_sync(kFull, hitB && childB >= 0);
@@ -482,9 +538,9 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       }
       __syncwarp();
     }
-    while (qn >= 32) flush(32);
+    drain();
   }
-  while (qn > 0) flush(min(qn, 32));
+  for (int off = 0; off < qn; off += 32) flush(off, min(qn - off, 32));
   return nk;
 }
 
@@ -525,6 +581,7 @@ __device__ __forceinline__ void stream_flush(const SceneView& S, WM& M, Stream& 
   const unsigned lane = lane_id();
   unsigned long long* const kscr = reinterpret_cast<unsigned long long*>(&M.e0[WM::kTr]);
   uint32_t* const pscr = reinterpret_cast<uint32_t*>(&M.e1[WM::kTr]);
+  uint32_t* const lq = reinterpret_cast<uint32_t*>(&M.e2[WM::kTr]);
   __syncwarp();
   const uint32_t cp = (int)lane < n ? M.lq[lane] : 0u;
   bool cand = false;

@@ -279,7 +279,8 @@ class BVH:
         )
 
     def wide_nodes(self):
-        """[count, 7, 32] view of the 32-wide nodes (6 box planes + child ids)."""
+        """[count, 7, 32] view of the 32-wide nodes (6 box planes + child ids; a
+        negative id is a leaf range ~((first << 3) | (count - 1)), include/rg.h)."""
         info = self.debug_views()["wide_info"].cpu()
         cnt = int(info[0])
         base = self.h.wide - self.ws.data_ptr()

@@ -48,9 +48,13 @@ def _check_refit_tree(b, boxes_morton, root):
             ch = wi[w, 6, k]
             if ch == 0x7FFFFFFF:
                 continue
-            sub = boxes_morton[~ch] if ch < 0 else walk(ch)
-            if ch < 0:
-                seen[~ch] += 1
+            if ch < 0:                                 # leaf range ~((first << 3) | (count - 1))
+                f, c = (~int(ch)) >> 3, ((~int(ch)) & 7) + 1
+                lb = boxes_morton[f:f + c]
+                sub = np.concatenate([lb[:, :3].min(0), lb[:, 3:].max(0)])
+                seen[f:f + c] += 1
+            else:
+                sub = walk(ch)
             assert np.array_equal(wf[w, :6, k], sub)
             lo = np.minimum(lo, sub[:3]); hi = np.maximum(hi, sub[3:])
         return np.concatenate([lo, hi])

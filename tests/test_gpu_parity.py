@@ -104,10 +104,12 @@ def test_build_bitexact(oracle, kind, n):
 
 def check_wide_tree(b, ref, n):
     """32-wide collapse (vectorised, any n): every wide child box equals the
-    exact box of what it points at (a leaf's padded AABB, or the union of the
-    child wide node's boxes), every leaf appears exactly once, every wide node
-    but the root is referenced exactly once and is reachable from the root,
-    the root's union is the scene box, no collapse error was flagged."""
+    exact box of what it points at (a leaf range's union of padded AABBs -- a
+    range ~((first << 3) | (count - 1)) covers 1..8 consecutive Morton-order
+    leaves --, or the union of the child wide node's boxes), every leaf appears
+    exactly once, every wide node but the root is referenced exactly once and is
+    reachable from the root, the root's union is the scene box, no collapse error
+    was flagged."""
     info = b.debug_views()["wide_info"].cpu().numpy()
     assert info[3] == 0
     wf, wi = b.wide_nodes()
@@ -118,10 +120,17 @@ def check_wide_tree(b, ref, n):
     empty = ch == 0x7FFFFFFF
     leaf = (ch < 0) & ~empty
     inner = (ch >= 0) & ~empty
-    # leaves exactly once
-    lid = ~ch[leaf]
+    # leaves exactly once (ranges expanded); a range's box = union of its leaves'
+    enc = (~ch[leaf]).astype(np.int64)
+    first, cnt = enc >> 3, (enc & 7) + 1
+    assert cnt.min() >= 1 and cnt.max() <= 8
+    lid = np.repeat(first, cnt) + (np.arange(cnt.sum()) - np.repeat(np.cumsum(cnt) - cnt, cnt))
     assert np.array_equal(np.sort(lid), np.arange(n))
-    assert np.array_equal(box[leaf], ref.leaf_boxes[lid])
+    srt = np.argsort(first)                            # the ranges tile [0, n)
+    rb = np.empty((enc.size, 6), np.float32)
+    rb[srt, :3] = np.minimum.reduceat(ref.leaf_boxes[:, :3], first[srt], axis=0)
+    rb[srt, 3:] = np.maximum.reduceat(ref.leaf_boxes[:, 3:], first[srt], axis=0)
+    assert np.array_equal(box[leaf], rb)
     # union of each wide node's live child boxes
     lo = np.where(empty[..., None], np.inf, box[..., :3]).min(1)
     hi = np.where(empty[..., None], -np.inf, box[..., 3:]).max(1)
