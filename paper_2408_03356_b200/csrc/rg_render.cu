@@ -150,9 +150,14 @@ struct Stream {
   bool valid;
 };
 
+#ifndef RG_STK64
+#define RG_STK64 0   // restart-query stack entries as one 8-B word (medians of 9: forward
+                     // 6.231 -> 6.304 ms; kept as an A/B knob)
+#endif
 template <int STK, int NCAP, int CCAP, int KA = kA, int SLOTS = kSlots>
 struct WarpMemT {
   static constexpr int kStack = STK;
+  static constexpr bool k64 = RG_STK64 != 0 && STK <= 256;   // the 520-list keeps 6-B entries
   static constexpr int kNCap = NCAP;
   static constexpr int kCCap = CCAP;
   static constexpr int kList = KA;     // active-list capacity
@@ -161,9 +166,10 @@ struct WarpMemT {
   float4 e0[SLOTS], e1[SLOTS], e2[SLOTS];
   union {
     struct {             // restart query (fetch)
-      uint32_t stk[STK];   // stacked wide node ids
-      uint16_t stn[STK];   // their boxes' entry distances as 16-bit order keys (fp16 rounded
-                           // down): pop-time selection and pruning
+      uint2 st2[k64 ? STK : 1];   // {wide node id, 16-bit entry key}: one 8-B access
+      uint32_t stk[k64 ? 1 : STK];   // or: stacked wide node ids
+      uint16_t stn[k64 ? 1 : STK];   // their boxes' entry distances as 16-bit order keys
+                                     // (fp16 rounded down): pop-time selection and pruning
     } r;
     struct {             // persistent per-ray traversal (stream_next); clobbered by fetch
       uint32_t nk[NCAP];   // node frontier: fkey of a lower bound on every t_entry below
@@ -276,11 +282,28 @@ __device__ __forceinline__ float stn_dec(unsigned k) {
   return __half2float(__ushort_as_half((unsigned short)b));
 }
 
+template <class WM>
+__device__ __forceinline__ void stk_put(WM& M, int i, uint32_t nid, unsigned k16) {
+  if constexpr (WM::k64) M.u.r.st2[i] = make_uint2(nid, k16);
+  else { M.u.r.stk[i] = nid; M.u.r.stn[i] = (uint16_t)k16; }
+}
+template <class WM>
+__device__ __forceinline__ void stk_get(const WM& M, int i, uint32_t& nid, unsigned& k16) {
+  if constexpr (WM::k64) {
+    const uint2 e = M.u.r.st2[i];
+    nid = e.x; k16 = e.y;
+  } else {
+    nid = M.u.r.stk[i]; k16 = M.u.r.stn[i];
+  }
+}
+
 // Warp-cooperative k-nearest query on the 32-wide BVH: the kmax (<= 32)
 // smallest keys (t_entry bits, index) > cursor among Gaussians whose exact
 // support interval satisfies t_exit >= seg_lo and t_entry <= seg_hi.
 // Result: lane l < return value holds the l-th smallest key and its position.
-template <class WM>
+// KEYCMP: pop-time pruning in the 16-bit key domain (forward: medians of 9, 6.355 ->
+// 6.231 ms); the backward keeps the float compare (its register budget: 4.83 vs 4.91 ms)
+template <class WM, bool KEYCMP = true>
 __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, float seg_hi,
                      unsigned long long cursor, int kmax, unsigned long long& key, uint32_t& pos,
                      Counters& cnt) {
@@ -295,11 +318,15 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
   pos = 0;
   int nk = 0;
   float te_lim = INFINITY;
+  // pop-time pruning in the 16-bit key domain: stn_dec(k) > te_lim + slack  <=>
+  // k > stn_enc(te_lim + slack) (stn_enc rounds down to the largest fp16 <= its
+  // argument, stn_dec is strictly monotone; the bound is never -0: slack > 0)
+  unsigned klim = KEYCMP ? stn_enc(INFINITY) : 0u;
   unsigned long long kth = ~0ull;
   const float slack = 1e-5f * (fabsf(seg_lo) + fabsf(seg_hi)) + 1e-6f;
   const float lo_s = seg_lo - slack, hi_s = seg_hi + slack;
   int sp = 1, qn = 0;
-  if (lane == 0) { M.u.r.stk[0] = 0; M.u.r.stn[0] = stn_enc(-INFINITY); }
+  if (lane == 0) stk_put(M, 0, 0u, stn_enc(-INFINITY));
   __syncwarp();
   // Exact leaf tests are batched: box-passing leaves are queued in shared
   // memory and tested 32 at a time (all lanes busy), then the candidates are
@@ -372,6 +399,7 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
     if (nk == kmax) {
       kth = shfl64(key, kmax - 1);
       te_lim = fkey_inv((uint32_t)(kth >> 32));
+      if (KEYCMP) klim = stn_enc(te_lim + slack);
     }
   };
   // ---- fq drain
@@ -421,13 +449,13 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
     {
       const int nwin = min(sp, 32);
       unsigned k16 = 0xFFFFu, nid = 0;
-      if ((int)lane < nwin) { k16 = M.u.r.stn[sp - 1 - (int)lane]; nid = M.u.r.stk[sp - 1 - (int)lane]; }
+      if ((int)lane < nwin) stk_get(M, sp - 1 - (int)lane, nid, k16);
       // (key, lane) packed: one reduction yields the minimum and its lane (ties
       // to the lowest lane; a key reduction + ballot + ffs was 2.2% slower)
       const unsigned kl = (k16 << 5) | lane;
       const unsigned klmin = __reduce_min_sync(kFull, kl);
       const unsigned kmin = klmin >> 5;
-      if (stn_dec(kmin) > te_lim + slack) {
+      if (KEYCMP ? kmin > klim : stn_dec(kmin) > te_lim + slack) {
         sp -= nwin;
         continue;
       }
@@ -438,7 +466,8 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       const unsigned k16b = (int)lane == srcA ? 0xFFFFu : k16;
       const unsigned klmin2 = __reduce_min_sync(kFull, (k16b << 5) | lane);
       const unsigned kmin2 = klmin2 >> 5;
-      if (kmin2 != 0xFFFFu && stn_dec(kmin2) <= te_lim + slack) {
+      if (KEYCMP ? kmin2 <= klim                      // (empty lanes: 0xFFFF > klim)
+                 : kmin2 != 0xFFFFu && stn_dec(kmin2) <= te_lim + slack) {
         srcB = (int)(klmin2 & 31u);
         nodeB = (int)__shfl_sync(kFull, nid, srcB);
       }
@@ -446,7 +475,7 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       // remove the popped entries: the surviving top entries (lanes 0, 1) fill the
       // holes the popped ones leave further down
       if (srcB < 0) {
-        if (lane == 0 && srcA != 0) { M.u.r.stk[sp - 1 - srcA] = nid; M.u.r.stn[sp - 1 - srcA] = (uint16_t)k16; }
+        if (lane == 0 && srcA != 0) stk_put(M, sp - 1 - srcA, nid, k16);
         sp -= 1;
       } else {
         const bool m0 = srcA != 0 && srcB != 0, m1 = srcA != 1 && srcB != 1;
@@ -454,7 +483,7 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
         int hole = -1;
         if (lane == 0 && m0) hole = h1;
         if (lane == 1 && m1) hole = m0 ? h2 : h1;
-        if (hole >= 2) { M.u.r.stk[sp - 1 - hole] = nid; M.u.r.stn[sp - 1 - hole] = (uint16_t)k16; }
+        if (hole >= 2) stk_put(M, sp - 1 - hole, nid, k16);
         sp -= 2;
       }
       __syncwarp();
@@ -523,11 +552,11 @@ __device__ int fetch(const SceneView& S, WM& M, const Ray& R, float seg_lo, floa
       if (sp + np <= WM::kStack) {
         if (hitA && childA >= 0) {
           const int r = sp + __popc(imA & lt_mask);
-          M.u.r.stk[r] = (uint32_t)childA; M.u.r.stn[r] = stn_enc(tnA);
+          stk_put(M, r, (uint32_t)childA, stn_enc(tnA));
         }
         if (hitB && childB >= 0) {
           const int r = sp + npA + __popc(imB & lt_mask);
-          M.u.r.stk[r] = (uint32_t)childB; M.u.r.stn[r] = stn_enc(tnB);
+          stk_put(M, r, (uint32_t)childB, stn_enc(tnB));
         }
         sp += np;
 #ifdef RG_STACK_PROBE
@@ -1601,14 +1630,14 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS
           got = read_fetch(count);
         } else {
           if constexpr (BWD) {
-            got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
+            got = fetch<WM, !BWD>(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
           } else {
             // the first RG_STREAM_FROM refills of a ray by restart queries (most C1 rays
             // need one or two), later ones by the persistent traversal
             if constexpr (!kStream || KA != kA) {
-              got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
+              got = fetch<WM, !BWD>(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
             } else {
-              if (nref < RG_STREAM_FROM) got = fetch(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
+              if (nref < RG_STREAM_FROM) got = fetch<WM, !BWD>(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
               else got = stream_next(P.S, M, R, tlo, t1, cursor, want, key, pos, cnt);
             }
             ++nref;
@@ -1904,7 +1933,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS
       } else if (INSTR && !BWD && n_in == K && n_in == KA && !exhausted) {   // counter only
         unsigned long long pk;
         uint32_t pp;
-        if (fetch(P.S, M, R, tlo, thi, cursor, 1, pk, pp, cnt) > 0 && lane == 0) cnt.overflows++;
+        if (fetch<WM, !BWD>(P.S, M, R, tlo, thi, cursor, 1, pk, pp, cnt) > 0 && lane == 0) cnt.overflows++;
       }
       if (!BWD && (more || (INSTR && n_in == K && n_in == KA && !exhausted))) {
         __syncwarp();                        // a restart query reused the traversal memory
@@ -1926,7 +1955,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS
             const int want = min(32, remaining);
             unsigned long long key;
             uint32_t pos;
-            const int got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
+            const int got = fetch<WM, !BWD>(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
             if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, KA + (int)lane, R, pos);
             __syncwarp();
             if (!BWD && log_ok) log_fetch(got, KA);
@@ -1941,7 +1970,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS
           if (INSTR && g0 == 0 && remaining == 0 && full_last) {   // overflow counter only
             unsigned long long pk;
             uint32_t pp;
-            if (fetch(P.S, M, R, tlo, thi, cur2, 1, pk, pp, cnt) > 0 && lane == 0) cnt.overflows++;
+            if (fetch<WM, !BWD>(P.S, M, R, tlo, thi, cur2, 1, pk, pp, cnt) > 0 && lane == 0) cnt.overflows++;
           }
         }
         cnt.evals += ev;
@@ -2018,7 +2047,7 @@ __global__ void __launch_bounds__(kBlock, BWD ? RG_MIN_BLOCKS
               if (replay_log) {           // the forward logged this chunk's set-up pairs
                 got = read_fetch(KA);
               } else {
-                got = fetch(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
+                got = fetch<WM, !BWD>(P.S, M, R, tlo, thi, cur2, want, key, pos, cnt);
                 if ((int)lane < got) setup_pair<!BWD, BASIS>(P.S, M, KA + (int)lane, R, pos);
               }
               if ((int)lane < got) {
