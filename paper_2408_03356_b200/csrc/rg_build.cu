@@ -3,9 +3,12 @@
 //   k_preprocess : validity, support radius, padded tight AABB (ARITH-1..4),
 //                  block-reduced bbox of valid means (ordered-int atomics)
 //   k_morton     : 30-bit Morton codes of the means (ARITH-6)
-//   k_radix_*    : stable LSD radix sort, 4 x 8-bit passes, CUB-free
-//                  (tile histogram -> single-block scan -> stable tile scatter
-//                  ranked with __match_any_sync)
+//   k_digit_hist + k_radix_scatter<true> : stable LSD radix sort, 3 + 4 x 8-bit
+//                  passes, CUB-free, Onesweep (all digit counts of a key set in
+//                  one read; one launch per pass with decoupled look-back over the
+//                  tiles; stable tile scatter ranked with __match_any_sync);
+//                  RG_ONESWEEP=0: tile histogram -> single-block scan -> scatter
+//   k_collapse_* : 32-wide collapse (leaf children as ranges, rg_internal.cuh)
 //   k_pack       : Morton-ordered 64-B geometry records + appearance records
 //   k_karras     : Karras 2012 hierarchy (one thread per internal node)
 //   k_refit      : bottom-up AABB union with per-node arrival counters
