@@ -556,8 +556,10 @@ __global__ void __launch_bounds__(128) k_wide_refit(const float4* nodes, const f
 // open 1 / 16 blocks 0.911 ms, open 1 / 4 blocks 0.838 ms (more spinning warps contend
 // on the queue counters), open 2 / 16 blocks 0.797 ms with the forward +0.014 ms (the
 // two-per-round cut is a slightly worse tree, far less than the build time it saves)
+// Re-measured on the final round-2 code (profiles/r2/ab_knobs_final.log): open 1 builds
+// in 0.695 ms against 0.779 ms for open 2, forward 6.223 vs 6.237 ms -> 1 again
 #ifndef RG_COLLAPSE_OPEN
-#define RG_COLLAPSE_OPEN 2
+#define RG_COLLAPSE_OPEN 1
 #endif
 #ifndef RG_COLLAPSE_BLOCKS
 #define RG_COLLAPSE_BLOCKS 4
